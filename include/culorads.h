@@ -1,0 +1,171 @@
+/*
+ * culorads.h -- C ABI of the B200 (sm_100a) kernels behind the lrsdp solve path.
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t
+ * passed as void*. Nothing here knows about torch; the Python host
+ * (paper_2407_15049_b200) allocates device memory through torch and binds
+ * these symbols with ctypes. Return value: 0 on success, otherwise a
+ * cudaError_t (launch failure) or a CL_E* code below (bad arguments).
+ *
+ * Layout conventions
+ *   factor     n x r fp64 factor stored row-major with a padded leading
+ *              dimension ld (ld = r rounded up to even, padding columns are
+ *              zero) so one factor row is a 16-byte aligned run of ld doubles.
+ *   pattern    CSR over the n x n position grid: int64 indptr[n+1], int32
+ *              indices[nnz]; each slot carries its coefficient either from
+ *              objective values cv[] and/or from an adjoint row (int64
+ *              at_ptr[nnz+1], int32 at_con[], double at_val[]) contracted
+ *              with one or two m-vectors.
+ *   constraint CSR of the stacked constraint operator (m rows) with the
+ *              position of every nonzero pre-resolved: int64 indptr[m+1],
+ *              int32 pi[], pj[] (row/col of the n x n position), double val[].
+ *
+ * Reductions are deterministic: per-block partial sums in a fixed grid,
+ * then one block folds the partials in a fixed order. `ws` is a device
+ * scratch of CL_WS_ALLOC doubles, zero-initialised once, private to the calling
+ * stream (its last word is the completion counter, left at 0 after every call).
+ */
+#ifndef CULORADS_H
+#define CULORADS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CL_MAXIN 20          /* operands of one streaming combination        */
+#define CL_MAXDOT 48         /* dot products reduced by one launch           */
+#define CL_MAXY 4            /* extra row operands of a pattern product      */
+#define CL_RED_BLOCKS 1184   /* 148 SMs x 8: reduction grid upper bound       */
+#define CL_WS_DOUBLES (CL_RED_BLOCKS * CL_MAXDOT)
+#define CL_WS_ALLOC (CL_WS_DOUBLES + 8)   /* + completion counter */
+
+#define CL_OK 0
+#define CL_EARG 1001          /* inconsistent arguments                      */
+#define CL_ENODEV 1002        /* no usable sm_100 device                     */
+
+/* Operand index meaning "the freshly computed output" in dot specifications. */
+#define CL_OUT 255
+
+/* Streaming combination over flat arrays of N doubles (factors are flat
+ * n*ld arrays; m-vectors are flat m arrays):
+ *   out[k] = sum_j coef[j] * in[j][k]                  (skipped if out==NULL)
+ *   dots[d] = sum_k op(da[d])[k] * op(db[d])[k]       op(CL_OUT) = out value
+ * `out` may alias one of the inputs (in-place update).
+ * Replaces the numpy expressions of the reference's vector algebra:
+ *   lbfgs_direction two-loop (alm.py:98), R + tau*D (alm.py:306),
+ *   history push <y,s> (alm.py:84), CG updates (admm.py:87-96), norms. */
+#define CL_DOT_PAIRS 0      /* <= 7 inputs, <= 8 dots between arbitrary operands (da/db) */
+#define CL_DOT_OUT_ALL 1    /* dots out·in[j] for every input, then out·out (nin+1 dots)  */
+#define CL_DOT_FIRST_TWO 2  /* no out; [j] = in0·in[j], [CL_MAXIN+j-1] = in1·in[j] (j>=1) */
+
+typedef struct {
+    int32_t nin;
+    int32_t mode;           /* CL_DOT_* */
+    int32_t ndot;           /* CL_DOT_PAIRS: number of (da,db) pairs; other modes: 0 = no dots */
+    const double* in[CL_MAXIN];
+    double coef[CL_MAXIN];
+    double* out;
+    uint8_t da[CL_MAXDOT];
+    uint8_t db[CL_MAXDOT];
+} cl_lincomb_args;
+
+int cl_lincomb(const cl_lincomb_args* args, int64_t N, double* dots_out, double* ws, void* stream);
+
+/* Coefficients of an n x n pattern matrix (linops.py:100 AdjointOperator.assemble):
+ *   S[s] = c_coeff * cv[s] + sum_{u in at row s} at_val[u] * w1[at_con[u]]
+ *                           + sum_{u in at row s} at_val[u] * w2[at_con[u]]
+ * Any of cv / at_ptr / w1 / w2 may be NULL (term dropped). */
+typedef struct {
+    int64_t nrows;
+    const int64_t* indptr;
+    const int32_t* indices;
+    const double* cv;
+    double c_coeff;
+    const int64_t* at_ptr;
+    const int32_t* at_con;
+    const double* at_val;
+    const double* w1;
+    const double* w2;
+} cl_pattern;
+
+/* Pattern times factor with a fused epilogue (linops.py:199 spmm, and the
+ * products S R of alm.py:245, S V of admm.py:49/62):
+ *   out[i,:] = alpha * (S X)[i,:] + sum_{j<ny} ycoef[j] * Y[j][i,:]
+ *   dots[d]  = sum op(da[d]) * op(db[d])   over all n*ld entries,
+ *              operand 0..ny-1 = Y[j], CL_OUT = out, 16+j = Z[j].       */
+typedef struct {
+    int32_t ny;
+    const double* Y[CL_MAXY];
+    double ycoef[CL_MAXY];
+    int32_t nz;
+    const double* Z[CL_MAXY];
+    int32_t ndot;
+    uint8_t da[8];
+    uint8_t db[8];
+} cl_epilogue;
+
+int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alpha,
+                    const cl_epilogue* epi, double* out, double* dots_out, double* ws,
+                    void* stream);
+
+/* Fused compressed outer product + stacked constraint product
+ * (linops.py:49 outer_product then linops.py:62 apply, i.e. A(X Y^T)):
+ *   out1[c] = sum_{t in row c} val[t] * (X1[pi]·Y1[pj] + X2[pi]·Y2[pj])   (X2 may be NULL)
+ *   out2[c] = sum_{t in row c} val[t] * (X3[pi]·Y3[pj])                   (X3 may be NULL)
+ * The second output serves the line search (alm.py:153-154): q1 and q2
+ * from one pass over the constraint nonzeros. */
+int cl_constraint_eval(int64_t m, const int64_t* indptr, const int32_t* pi, const int32_t* pj,
+                       const double* val, int32_t ld,
+                       const double* X1, const double* Y1, const double* X2, const double* Y2,
+                       double* out1, const double* X3, const double* Y3, double* out2,
+                       void* stream);
+
+/* Gathered outer product at K positions (linops.py:49), x[k] = X[imap[k]]·Y[jmap[k]]. */
+int cl_sddmm(int64_t K, const int32_t* imap, const int32_t* jmap, int32_t ld,
+             const double* X, const double* Y, double* x, void* stream);
+
+/* Diagonal-constraint fast path for problems whose constraint c is the single
+ * diagonal entry a_c * e_c e_c^T (m == n; MaxCut, problem.py:387): the ALM
+ * step update and gradient (alm.py:306-318) become row-local and fuse into one pass.
+ *   R  += tau*D;  CR += tau*CD;  ax_out[c] = ax[c] + tau*q1[c] + tau^2*q2[c]
+ *   w[c] = lam[c] + rho*(ax[c]-b[c]);  g_new = 2*(w[row]*a*R + scale*CR)
+ *   y = g_new - g_old
+ * plus dots: <CR,R>, <g_new,g_new>, <y, tau D>, lam·res, res·res and the
+ * multi-dots of g_new and y against up to `nh` history vectors H[]:
+ *   dots[0]=<CR,R> [1]=<g,g> [2]=<y,D> [3]=lam·res [4]=res·res [5]=<y,y>
+ *   [6]=<g,y>  [7+h]=<g,H_h>  [7+CL_MAXIN+h]=<y,H_h>   (dots_out: 7+2*CL_MAXIN) */
+typedef struct {
+    int64_t n;
+    int32_t ld;
+    const double* aval;          /* a_c */
+    double tau, rho, scale;
+    double* R; const double* D; double* CR; const double* CD;
+    const double* ax; double* ax_out; const double* q1; const double* q2;
+    const double* lam; const double* b;
+    const double* g_old; double* g_new; double* y;
+    int32_t nh;
+    const double* H[CL_MAXIN];
+    int32_t refresh;             /* 1: ax/CR were recomputed, skip tau updates */
+} cl_diag_update_args;
+
+int cl_diag_alm_update(const cl_diag_update_args* a, double* dots_out, double* ws, void* stream);
+
+/* Dense block Gram helpers for the Lanczos basis (spectral.py:55-56):
+ *   h[t] = sum_k Q[t][k] * v[k]            t < k_cnt   (Q row-major, ldq)
+ *   v[k] -= sum_t h[t] * Q[t][k]                                          */
+int cl_basis_project(const double* Q, int64_t ldq, int32_t k_cnt, int64_t n, const double* v,
+                     double* h, double* ws, void* stream);
+int cl_basis_subtract(const double* Q, int64_t ldq, int32_t k_cnt, int64_t n, const double* h,
+                      double* v, void* stream);
+
+/* Library identity, for load checks. */
+const char* cl_version(void);
+int cl_device_ok(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CULORADS_H */

@@ -1,0 +1,105 @@
+"""ctypes binding of libculorads (include/culorads.h).
+
+The shared library is built in-tree by ``paper_2407_15049_b200.build_ext``
+(``nvcc -gencode arch=compute_100a,code=sm_100a``). There is no fallback:
+if the library or an sm_100 device is missing, ``lib()`` raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libculorads.so")
+
+CL_MAXIN = 20
+CL_MAXDOT = 48
+CL_MAXY = 4
+CL_RED_BLOCKS = 1184
+CL_WS_DOUBLES = CL_RED_BLOCKS * CL_MAXDOT
+CL_WS_ALLOC = CL_WS_DOUBLES + 8
+CL_OUT = 255
+CL_DOT_PAIRS, CL_DOT_OUT_ALL, CL_DOT_FIRST_TWO = 0, 1, 2
+CL_EARG = 1001
+
+EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_sddmm",
+           "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
+           "cl_version", "cl_device_ok")
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+I32 = ctypes.c_int32
+D = ctypes.c_double
+
+
+class LincombArgs(ctypes.Structure):
+    _fields_ = [("nin", I32), ("mode", I32), ("ndot", I32),
+                ("inp", P * CL_MAXIN), ("coef", D * CL_MAXIN), ("out", P),
+                ("da", ctypes.c_uint8 * CL_MAXDOT), ("db", ctypes.c_uint8 * CL_MAXDOT)]
+
+
+class Pattern(ctypes.Structure):
+    _fields_ = [("nrows", I64), ("indptr", P), ("indices", P), ("cv", P), ("c_coeff", D),
+                ("at_ptr", P), ("at_con", P), ("at_val", P), ("w1", P), ("w2", P)]
+
+
+class Epilogue(ctypes.Structure):
+    _fields_ = [("ny", I32), ("Y", P * CL_MAXY), ("ycoef", D * CL_MAXY),
+                ("nz", I32), ("Z", P * CL_MAXY),
+                ("ndot", I32), ("da", ctypes.c_uint8 * 8), ("db", ctypes.c_uint8 * 8)]
+
+
+class DiagUpdateArgs(ctypes.Structure):
+    _fields_ = [("n", I64), ("ld", I32), ("aval", P), ("tau", D), ("rho", D), ("scale", D),
+                ("R", P), ("D", P), ("CR", P), ("CD", P),
+                ("ax", P), ("ax_out", P), ("q1", P), ("q2", P),
+                ("lam", P), ("b", P), ("g_old", P), ("g_new", P), ("y", P),
+                ("nh", I32), ("H", P * CL_MAXIN), ("refresh", I32)]
+
+
+_LIB = None
+_LOCK = threading.Lock()
+
+
+class CulLoradsError(RuntimeError):
+    pass
+
+
+def _declare(lib):
+    lib.cl_lincomb.argtypes = [ctypes.POINTER(LincombArgs), I64, P, P, P]
+    lib.cl_pattern_spmm.argtypes = [ctypes.POINTER(Pattern), P, I32, D, ctypes.POINTER(Epilogue),
+                                    P, P, P, P]
+    lib.cl_constraint_eval.argtypes = [I64, P, P, P, P, I32, P, P, P, P, P, P, P, P, P]
+    lib.cl_sddmm.argtypes = [I64, P, P, I32, P, P, P, P]
+    lib.cl_diag_alm_update.argtypes = [ctypes.POINTER(DiagUpdateArgs), P, P, P]
+    lib.cl_basis_project.argtypes = [P, I64, I32, I64, P, P, P, P]
+    lib.cl_basis_subtract.argtypes = [P, I64, I32, I64, P, P, P]
+    lib.cl_version.restype = ctypes.c_char_p
+    lib.cl_device_ok.restype = ctypes.c_int
+    for name in EXPORTS:
+        if name not in ("cl_version", "cl_device_ok"):
+            getattr(lib, name).restype = ctypes.c_int
+
+
+def load(require_device=True):
+    """Load (once) and return the library handle; raise loudly if unusable."""
+    global _LIB
+    with _LOCK:
+        if _LIB is None:
+            if not os.path.exists(LIB_PATH):
+                raise CulLoradsError(
+                    f"{LIB_PATH} is missing: build it with "
+                    "`python -m paper_2407_15049_b200.build_ext` (no CPU fallback exists)")
+            lib = ctypes.CDLL(LIB_PATH)
+            _declare(lib)
+            _LIB = lib
+    if require_device and not _LIB.cl_device_ok():
+        raise CulLoradsError("no sm_100 (B200) CUDA device visible; the solver has no CPU path")
+    return _LIB
+
+
+def check(rc, what):
+    if rc != 0:
+        raise CulLoradsError(f"{what} failed with code {rc}")

@@ -1,0 +1,397 @@
+"""Stage two: splitting ADMM on X = U V^T with matrix-free CG half-steps.
+
+Device restatement of the reference's lrsdp/admm.py. Each half-step solves
+
+    rho * A*(A(W Wf^T)) Wf + rho W = -scale*C Wf - A*(lam) Wf + rho A*(b) Wf + rho Wf
+
+by CG (Algorithm 2). On the device the operator is one fused constraint
+launch (A(W Wf^T) over the constraint nonzeros) plus one Omega_A pattern
+product whose epilogue adds rho*W and reduces <p, Q>; the right-hand side
+assembles -scale*C - A*(lam) + rho*A*(b) inside the SpMM coefficients.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from collections import deque
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .alm import DualVector
+from .device import F64, padded_ld
+from .exceptions import DivergedError, SpdViolationError
+from .linops import objective_dev, to_factor, to_vec
+
+
+@dataclass
+class CgWorkspace:
+    """Tolerance and cap of one CG solve (admm.py:31)."""
+
+    eps: float
+    max_iter: int
+    residual: object = None
+    direction: object = None
+    op_output: object = None
+
+    def __post_init__(self):
+        if not self.eps > 0:
+            raise ValueError("CG tolerance must be positive")
+
+
+class HalfStep:
+    """Device buffers + the SPD operator of a half-step (admm.py:45)."""
+
+    S_CG = 400       # slab offsets
+    S_RHS = 410
+
+    def __init__(self, ops, n, ld):
+        self.ops, self.dev, self.n, self.ld = ops, ops.dev, n, ld
+        m = ops.problem.m
+        dev = self.dev
+        self.y = dev.empty(m)
+        self.r = dev.empty(n, ld)
+        self.p = dev.empty(n, ld)
+        self.Q = dev.empty(n, ld)
+        self.nlam = dev.empty(m)
+        self.rhob = dev.empty(m)
+
+    def apply(self, W, Wf, rho, out, dot_with=None, at=None):
+        """out = rho*(A*(A(W Wf^T)) Wf + W); optional <dot_with, out> -> slab[at]."""
+        ops, dev = self.ops, self.dev
+        dev.constraint_eval(ops.cop.con, self.ld, W, Wf, self.y)
+        dots = [(("y", 0), "out")] if dot_with is not None else None
+        dev.spmm(ops.adj.apat, Wf, self.ld, alpha=rho, out=out, Y=[W], ycoef=[rho], w1=self.y,
+                 dots=dots, at=at if at is not None else 0)
+        return out
+
+    def rhs(self, Wf, lam, rho, scale, out, at):
+        """out = S_b Wf + rho Wf with S_b = -scale C - A*(lam) + rho A*(b); ||out||^2 -> slab[at]."""
+        ops, dev = self.ops, self.dev
+        dev.lincomb(self.nlam, [lam], [-1.0])
+        dev.lincomb(self.rhob, [ops.b], [rho])
+        dev.spmm(ops.adj.omega, Wf, self.ld, alpha=1.0, out=out, Y=[Wf], ycoef=[rho],
+                 c_coeff=-scale, w1=self.nlam, w2=self.rhob, dots=[("out", "out")], at=at)
+        return out
+
+    def cg(self, x, Wf, rho, rhs, eps, max_iter):
+        """admm.py:65 in place on x (a device factor). Returns (iterations, residual)."""
+        dev = self.dev
+        r, p, Q = self.r, self.p, self.Q
+        A = self.S_CG
+        self.apply(x, Wf, rho, Q)
+        dev.lincomb(r, [rhs, Q], [1.0, -1.0], dots=[("out", "out")], at=A)
+        qr = float(dev.fetch(A + 1)[A])
+        rnorm = math.sqrt(qr)
+        if rnorm <= eps:
+            return 0, rnorm
+        dev.lincomb(p, [r], [1.0])
+        its = 0
+        for k in range(max_iter):
+            self.apply(p, Wf, rho, Q, dot_with=p, at=A + 1)
+            pq = float(dev.fetch(A + 2)[A + 1])
+            if not math.isfinite(pq):
+                raise DivergedError("CG produced non-finite curvature", last_iterate=x)
+            if pq <= 0.0:
+                raise SpdViolationError(f"non-positive curvature {pq:.3e} in CG (operator not SPD)")
+            alpha = qr / pq
+            dev.lincomb(x, [x, p], [1.0, alpha])
+            dev.lincomb(r, [r, Q], [1.0, -alpha], dots=[("out", "out")], at=A + 2)
+            qn = float(dev.fetch(A + 3)[A + 2])
+            rnorm = math.sqrt(qn)
+            its = k + 1
+            if rnorm <= eps:
+                break
+            dev.lincomb(p, [r, p], [1.0, qn / qr])
+            qr = qn
+        dev.lincomb(None, [x], [0.0], dots=[(0, 0)], at=A + 3)
+        if not math.isfinite(float(dev.fetch(A + 4)[A + 3])):
+            raise DivergedError("CG iterate diverged", last_iterate=x)
+        return its, rnorm
+
+
+def subproblem_apply(W, W_fixed, rho, ops):
+    """rho*(A*(A(W Wf^T)) Wf + W)  (admm.py:45)."""
+    r = W.shape[1]
+    ld = padded_ld(r)
+    hs = HalfStep(ops, W.shape[0], ld)
+    out = hs.apply(to_factor(W, ops.dev, ld), to_factor(W_fixed, ops.dev, ld), rho,
+                   ops.dev.empty(W.shape[0], ld))
+    out = out[:, :r]
+    return out if isinstance(W, torch.Tensor) else out.cpu().numpy()
+
+
+def subproblem_rhs(W_fixed, dual: DualVector, ops, scale=1.0, S_b=None):
+    """Right-hand side of a half-step system (admm.py:52)."""
+    r = W_fixed.shape[1]
+    ld = padded_ld(r)
+    hs = HalfStep(ops, W_fixed.shape[0], ld)
+    out = ops.dev.empty(W_fixed.shape[0], ld)
+    if S_b is not None:
+        Wf = to_factor(W_fixed, ops.dev, ld)
+        S_b.matmul_dev(Wf, ld, out=out, Y=[Wf], ycoef=[dual.rho])
+    else:
+        hs.rhs(to_factor(W_fixed, ops.dev, ld), to_vec(dual.lam, ops.dev), dual.rho, scale, out,
+               at=HalfStep.S_RHS)
+    out = out[:, :r]
+    return out if isinstance(W_fixed, torch.Tensor) else out.cpu().numpy()
+
+
+def cg_solve(x0, apply_op, rhs, ws: CgWorkspace):
+    """CG with Frobenius products for an arbitrary operator callback (admm.py:65).
+
+    Generic (host-orchestrated) form used by tests and callers with their own
+    operator; the solver's hot path uses ``HalfStep.cg``. Operands may be
+    numpy or device tensors; the vector algebra always runs on the device.
+    """
+    from .device import default_device
+    dev = default_device()
+    host = not isinstance(x0, torch.Tensor)
+    shape = tuple(x0.shape)
+    ld = padded_ld(shape[1]) if len(shape) == 2 else None
+
+    def dv(a):
+        if len(shape) == 2:
+            return to_factor(a, dev, ld)
+        return to_vec(a, dev).clone()
+
+    def back(t):
+        return t[:, :shape[1]] if len(shape) == 2 else t
+
+    def op(t):
+        res = apply_op(back(t) if not host else back(t).cpu().numpy())
+        return dv(res)
+
+    x = dv(x0).clone()
+    b = dv(rhs)
+    r = dev.empty(*x.shape)
+    dev.lincomb(r, [b, op(x)], [1.0, -1.0], dots=[("out", "out")], at=420)
+    qr = float(dev.fetch(421)[420])
+    rnorm = math.sqrt(qr)
+    if rnorm <= ws.eps:
+        ws.residual = r
+        return (back(x).cpu().numpy() if host else back(x)), 0, rnorm
+    p = r.clone()
+    its = 0
+    for k in range(ws.max_iter):
+        Q = op(p)
+        dev.lincomb(None, [p, Q], [0.0, 0.0], dots=[(0, 1)], at=421)
+        pq = float(dev.fetch(422)[421])
+        if not math.isfinite(pq):
+            raise DivergedError("CG produced non-finite curvature", last_iterate=x)
+        if pq <= 0.0:
+            raise SpdViolationError(f"non-positive curvature {pq:.3e} in CG (operator not SPD)")
+        alpha = qr / pq
+        dev.lincomb(x, [x, p], [1.0, alpha])
+        dev.lincomb(r, [r, Q], [1.0, -alpha], dots=[("out", "out")], at=422)
+        qn = float(dev.fetch(423)[422])
+        rnorm = math.sqrt(qn)
+        its = k + 1
+        if rnorm <= ws.eps:
+            break
+        dev.lincomb(p, [r, p], [1.0, qn / qr])
+        qr = qn
+    if not bool(torch.isfinite(x).all()):
+        raise DivergedError("CG iterate diverged", last_iterate=x)
+    ws.residual, ws.direction = r, p
+    return (back(x).cpu().numpy() if host else back(x)), its, rnorm
+
+
+@dataclass
+class AdmmState:
+    """Factor halves (device n x ld), shared dual, cached A(U V^T) (admm.py:105)."""
+
+    U: object
+    V: object
+    dual: DualVector
+    ax: object = None
+    r: int = 0
+
+    def set_factors(self, U=None, V=None):
+        if U is not None:
+            self.U = U
+        if V is not None:
+            self.V = V
+        self.ax = None
+
+    def constraint_values(self, ops):
+        if self.ax is None:
+            ld = self.U.shape[1]
+            self.ax = ops.cop.apply_pair_dev(self.U, self.V, ld)
+        return self.ax
+
+
+@dataclass
+class StepStats:
+    cg_iters_u: int
+    cg_iters_v: int
+    resid_u: float
+    resid_v: float
+    hit_cap: bool
+
+
+def _resid(ops, ax, res, at):
+    ops.dev.lincomb(res, [ax, ops.b], [1.0, -1.0], dots=[("out", "out")], at=at)
+
+
+def admm_step(state: AdmmState, ops, *, scale=1.0, cg_cap=200, cg_rel_floor=1e-10,
+              cg_primal_coeff=0.05, hs=None, pool=None) -> StepStats:
+    """U half-solve, V half-solve, dual ascent (admm.py:136)."""
+    dev = ops.dev
+    p = ops.problem
+    dual = state.dual
+    rho = dual.rho
+    n, ld = state.U.shape
+    hs = hs or HalfStep(ops, n, ld)
+    ax = state.constraint_values(ops)
+    _resid(ops, ax, hs.y, 430)
+    pmeas = math.sqrt(float(dev.fetch(431)[430])) / (1.0 + p.b_norminf)
+    rel = max(cg_rel_floor, min(1e-2, cg_primal_coeff * pmeas))
+    lam = dual.lam
+
+    rhs = pool.get() if pool else dev.empty(n, ld)
+    hs.rhs(state.V, lam, rho, scale, rhs, at=431)
+    eps_u = max(rel * math.sqrt(float(dev.fetch(432)[431])), 1e-300)
+    U = pool.get() if pool else dev.empty(n, ld)
+    dev.lincomb(U, [state.U], [1.0])
+    it_u, res_u = hs.cg(U, state.V, rho, rhs, eps_u, cg_cap)
+    state.set_factors(U=U)
+
+    hs.rhs(U, lam, rho, scale, rhs, at=432)
+    eps_v = max(rel * math.sqrt(float(dev.fetch(433)[432])), 1e-300)
+    V = pool.get() if pool else dev.empty(n, ld)
+    dev.lincomb(V, [state.V], [1.0])
+    it_v, res_v = hs.cg(V, U, rho, rhs, eps_v, cg_cap)
+    state.set_factors(V=V)
+    if pool:
+        pool.put(rhs)
+
+    ax = state.constraint_values(ops)
+    _resid(ops, ax, hs.y, 433)
+    dev.lincomb(lam, [lam, hs.y], [1.0, rho])          # lam += rho*(A(UV^T) - b)
+    state.last_pnorm2 = float(dev.fetch(434)[433])
+    hit_cap = (it_u >= cg_cap and res_u > eps_u) or (it_v >= cg_cap and res_v > eps_v)
+    return StepStats(it_u, it_v, res_u, res_v, hit_cap)
+
+
+@dataclass
+class AdmmResult:
+    steps: int
+    err1: float
+    primal_scaled_inf: float
+    cg_iterations: int
+    hit_deadline: bool
+    hit_cap: bool
+    stalled: bool = False
+    gap: float | None = None
+
+
+class _Pool:
+    def __init__(self, dev, n, ld):
+        self.dev, self.n, self.ld, self.free = dev, n, ld, []
+
+    def get(self):
+        return self.free.pop() if self.free else self.dev.empty(self.n, self.ld)
+
+    def put(self, t):
+        self.free.append(t)
+
+
+def admm_run(state: AdmmState, ops, *, scale=1.0, eps=1e-5, gap_eps=None, min_steps=0,
+             step_cap=20000, cg_cap=200, rho_balance_mu=10.0, rho_balance_tau=2.0,
+             rho_balance_every=5, rho_min=1e-6, rho_max=1e8, stall_window=60,
+             stall_ratio=0.995, escalate=None, recorder=None, deadline=None) -> AdmmResult:
+    """ADMM iterations with residual balancing and the gap-stall exit (admm.py:184).
+
+    ``state.U/V`` are device n x ld factors of logical rank ``state.r``;
+    ``escalate(U, V, r) -> (U_new, V_new, r_new) or None``.
+    """
+    dev = ops.dev
+    p = ops.problem
+    b1, binf = p.b_norm1, p.b_norminf
+    n, ld = state.U.shape
+    hs = HalfStep(ops, n, ld)
+    pool = _Pool(dev, n, ld)
+    res = dev.empty(p.m)
+
+    def measures():
+        ax = state.constraint_values(ops)
+        _resid(ops, ax, res, 440)
+        pn = math.sqrt(float(dev.fetch(441)[440]))
+        return pn, pn / (1.0 + b1), pn / (1.0 + binf)
+
+    def objective_and_gap():
+        # <C, U V^T> and lam.b in one fetch
+        dev.spmm(ops.c_mat.cpat, state.V, state.U.shape[1], out=None, Z=[state.U],
+                 dots=[("out", ("z", 0))], at=442, c_coeff=1.0)
+        dev.lincomb(None, [state.dual.lam, ops.b], [0.0, 0.0], dots=[(0, 1)], at=443)
+        s = dev.fetch(444)
+        obj = float(s[442])
+        lam_b = -float(s[443]) / scale
+        return obj, abs(obj - lam_b) / (1.0 + abs(obj) + abs(lam_b))
+
+    pnorm, err1, p0 = measures()
+    g3 = objective_and_gap()[1] if gap_eps is not None else None
+    if p0 <= eps and (gap_eps is None or g3 < gap_eps) and min_steps == 0:
+        return AdmmResult(steps=0, err1=err1, primal_scaled_inf=p0, cg_iterations=0,
+                          hit_deadline=False, hit_cap=False, gap=g3)
+    cg_total = 0
+    cap_streak = 0
+    steps = 0
+    hit_deadline = False
+    stalled = False
+    gap_hist = deque(maxlen=stall_window)
+    for step in range(1, step_cap + 1):
+        if deadline is not None and time.perf_counter() > deadline:
+            hit_deadline = True
+            break
+        U_prev, V_prev = state.U, state.V
+        stats = admm_step(state, ops, scale=scale, cg_cap=cg_cap, hs=hs, pool=pool)
+        cg_total += stats.cg_iters_u + stats.cg_iters_v
+        steps = step
+        pnorm = math.sqrt(state.last_pnorm2)
+        err1, p0 = pnorm / (1.0 + b1), pnorm / (1.0 + binf)
+        obj = None
+        if gap_eps is not None or recorder is not None:
+            obj, g3v = objective_and_gap()
+            g3 = g3v if gap_eps is not None else None
+        if recorder is not None:
+            recorder.record("admm", scale * obj, err1, max(stats.resid_u, stats.resid_v),
+                            state.dual.rho, state.r)
+        done = p0 <= eps and (gap_eps is None or g3 < gap_eps) and step >= min_steps
+        balance = (not done) and step % rho_balance_every == 0
+        if balance:
+            dev.lincomb(None, [state.U, U_prev], [1.0, -1.0], dots=[("out", "out")], at=445)
+            dev.lincomb(None, [state.V, V_prev], [1.0, -1.0], dots=[("out", "out")], at=446)
+        pool.put(U_prev)
+        pool.put(V_prev)
+        if done:
+            break
+        if gap_eps is not None and p0 <= eps:
+            gap_hist.append(g3)
+            if len(gap_hist) == stall_window and gap_hist[-1] > stall_ratio * gap_hist[0]:
+                stalled = True
+                break
+        else:
+            gap_hist.clear()
+        if balance:
+            s = dev.fetch(447)
+            dual_surrogate = state.dual.rho * (math.sqrt(float(s[445])) + math.sqrt(float(s[446])))
+            if pnorm > rho_balance_mu * dual_surrogate:
+                state.dual.rho = min(state.dual.rho * rho_balance_tau, rho_max)
+            elif dual_surrogate > rho_balance_mu * pnorm:
+                state.dual.rho = max(state.dual.rho / rho_balance_tau, rho_min)
+        cap_streak = cap_streak + 1 if stats.hit_cap else 0
+        if cap_streak >= 2 and escalate is not None:
+            grown = escalate(state.U, state.V, state.r)
+            if grown is not None:
+                U2, V2, state.r = grown
+                state.set_factors(U=U2, V=V2)
+                n, ld = U2.shape
+                hs = HalfStep(ops, n, ld)
+                pool = _Pool(dev, n, ld)
+            cap_streak = 0
+    return AdmmResult(steps=steps, err1=err1, primal_scaled_inf=p0, cg_iterations=cg_total,
+                      hit_deadline=hit_deadline, hit_cap=cap_streak > 0, stalled=stalled, gap=g3)

@@ -1,0 +1,707 @@
+// culorads.cu -- sm_100a kernels for the low-rank SDP solve path (see include/culorads.h).
+//
+// All arithmetic is fp64. The work is HBM-bound gather/stream traffic over
+// n x ld factors (no GEMM-shaped contraction exists on this path), so the
+// kernels are built around: 16-byte (double2) loads of factor rows, one
+// lane group per pattern/constraint row sized to the padded rank, index and
+// coefficient loads done cooperatively by the group and broadcast with
+// shuffles, grids sized in multiples of the 148 SMs, and deterministic
+// two-level reductions (per-block partials, the last block folds them in a
+// fixed order).
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "culorads.h"
+
+#define NT 256
+#define NWARP (NT / 32)
+#define NSM 148
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// deterministic reductions
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Reduce acc[0..ndot) over the block, store per-block partials, and let the
+// last block to finish fold all partials (fixed order) into out[0..ndot).
+// ws layout: [CL_RED_BLOCKS * CL_MAXDOT partials][1 counter word].
+template <int ND>
+__device__ __forceinline__ void reduce_and_finish(const double (&acc)[ND], int ndot, double* ws,
+                                                  double* out) {
+    __shared__ double sh[NWARP][ND > 0 ? ND : 1];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+        if (d < ndot) {
+            double v = warp_sum(acc[d]);
+            if (lane == 0) sh[wid][d] = v;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < ndot) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < NWARP; ++w) s += sh[w][threadIdx.x];
+        ws[(size_t)blockIdx.x * CL_MAXDOT + threadIdx.x] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    unsigned int* counter = reinterpret_cast<unsigned int*>(ws + CL_WS_DOUBLES);
+    if (threadIdx.x == 0) {
+        unsigned int prev = atomicAdd(counter, 1u);
+        last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // one warp per dot, lanes stride over the block partials
+    for (int d = wid; d < ndot; d += NWARP) {
+        double s = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32)
+            s += __ldcg(ws + (size_t)b * CL_MAXDOT + d);
+        s = warp_sum(s);
+        if (lane == 0) out[d] = s;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+}
+
+__device__ __forceinline__ double2 ld2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ double2 ld2cs(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+__device__ __forceinline__ double dot2(double2 a, double2 b) { return a.x * b.x + a.y * b.y; }
+__device__ __forceinline__ double2 axpy2(double a, double2 x, double2 y) {
+    return make_double2(fma(a, x.x, y.x), fma(a, x.y, y.y));
+}
+
+template <int K>
+__device__ __forceinline__ double2 select2(const double2 (&v)[K], int idx) {
+    double2 r = v[0];
+#pragma unroll
+    for (int j = 1; j < K; ++j)
+        if (idx == j) r = v[j];
+    return r;
+}
+
+int red_grid(int64_t work_items) {
+    int64_t g = (work_items + NT - 1) / NT;
+    if (g < 1) g = 1;
+    if (g > CL_RED_BLOCKS) g = CL_RED_BLOCKS;
+    return (int)g;
+}
+
+// ---------------------------------------------------------------------------
+// streaming combination
+// ---------------------------------------------------------------------------
+
+struct LcDev {
+    int nin, ndot;
+    const double* in[CL_MAXIN];
+    double coef[CL_MAXIN];
+    double* out;
+    uint8_t da[CL_MAXDOT], db[CL_MAXDOT];
+};
+
+// MODE 0: up to 7 inputs, <= 8 arbitrary pair dots (operand 7 = out)
+// MODE 1: up to CL_MAXIN inputs, dots out·in[j] (j < nin) then out·out
+// MODE 2: up to CL_MAXIN inputs (no out), dots in0·in[j] (j < nin) then in1·in[j] (1 <= j < nin)
+template <int MODE>
+__global__ void __launch_bounds__(NT) lincomb_kernel(LcDev a, int64_t n2, int tail, double* ws,
+                                                     double* dots_out) {
+    constexpr int KIN = MODE == 0 ? 7 : CL_MAXIN;
+    constexpr int ND = MODE == 0 ? 8 : (MODE == 1 ? CL_MAXIN + 1 : 2 * CL_MAXIN - 1);
+    double acc[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) acc[d] = 0.0;
+    const int nin = a.nin;
+    const int64_t stride = (int64_t)gridDim.x * NT;
+    // element loop over double2 units; the odd tail element is handled by
+    // the first thread with a scalar pass folded into the same accumulators
+    for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < n2 + (tail ? 1 : 0); k += stride) {
+        const bool is_tail = (k == n2);
+        double2 v[KIN + 1];
+#pragma unroll
+        for (int j = 0; j < KIN; ++j) {
+            if (j < nin) {
+                if (!is_tail) v[j] = ld2cs(a.in[j] + 2 * k);
+                else v[j] = make_double2(a.in[j][2 * k], 0.0);
+            } else {
+                v[j] = make_double2(0.0, 0.0);
+            }
+        }
+        double2 o = make_double2(0.0, 0.0);
+        if (a.out != nullptr || MODE != 2) {
+#pragma unroll
+            for (int j = 0; j < KIN; ++j)
+                if (j < nin) o = axpy2(a.coef[j], v[j], o);
+            if (a.out != nullptr) {
+                if (!is_tail) st2(a.out + 2 * k, o);
+                else a.out[2 * k] = o.x;
+            }
+        }
+        v[KIN] = o;
+        if (MODE == 0) {
+#pragma unroll
+            for (int d = 0; d < 8; ++d)
+                if (d < a.ndot) {
+                    int ia = a.da[d] == CL_OUT ? KIN : a.da[d];
+                    int ib = a.db[d] == CL_OUT ? KIN : a.db[d];
+                    acc[d] += dot2(select2(v, ia), select2(v, ib));
+                }
+        } else if (MODE == 1) {
+#pragma unroll
+            for (int j = 0; j < KIN; ++j)
+                if (j < nin) acc[j] += dot2(o, v[j]);
+            acc[ND - 1] += dot2(o, o);
+        } else {
+#pragma unroll
+            for (int j = 0; j < KIN; ++j)
+                if (j < nin) acc[j] += dot2(v[0], v[j]);
+#pragma unroll
+            for (int j = 1; j < KIN; ++j)
+                if (j < nin) acc[KIN + j - 1] += dot2(v[1], v[j]);
+        }
+    }
+    // MODE 2 output layout is fixed: [j] = in0·in_j, [CL_MAXIN + j - 1] = in1·in_j
+    if (a.ndot > 0) reduce_and_finish<ND>(acc, a.ndot, ws, dots_out);
+}
+
+// ---------------------------------------------------------------------------
+// pattern (CSR over positions) times factor, fused coefficient assembly
+// ---------------------------------------------------------------------------
+
+struct PatDev {
+    int64_t nrows;
+    const int64_t* indptr;
+    const int32_t* indices;
+    const double* cv;
+    double c_coeff;
+    const int64_t* at_ptr;
+    const int32_t* at_con;
+    const double* at_val;
+    const double* w1;
+    const double* w2;
+};
+
+struct EpiDev {
+    int ny;
+    const double* Y[CL_MAXY];
+    double ycoef[CL_MAXY];
+    int nz;
+    const double* Z[CL_MAXY];
+    int ndot;
+    uint8_t da[8], db[8];
+};
+
+__device__ __forceinline__ double slot_coef(const PatDev& P, int64_t s) {
+    // same association as linops.py:184-194: data = At@w1 + At@w2 + c*cv
+    double data = 0.0;
+    if (P.at_ptr != nullptr) {
+        const int64_t u0 = __ldg(P.at_ptr + s), u1 = __ldg(P.at_ptr + s + 1);
+        if (P.w1 != nullptr) {
+            double t = 0.0;
+            for (int64_t u = u0; u < u1; ++u) t += __ldg(P.at_val + u) * __ldg(P.w1 + __ldg(P.at_con + u));
+            data += t;
+        }
+        if (P.w2 != nullptr) {
+            double t = 0.0;
+            for (int64_t u = u0; u < u1; ++u) t += __ldg(P.at_val + u) * __ldg(P.w2 + __ldg(P.at_con + u));
+            data += t;
+        }
+    }
+    if (P.cv != nullptr) data += P.c_coeff * __ldg(P.cv + s);
+    return data;
+}
+
+// One group of G lanes per row; lane l owns columns {2l, 2l+1} + 2G*c.
+// VEC = 1 only for ld == 1 (Lanczos vectors).
+template <int G, int VEC>
+__global__ void __launch_bounds__(NT) pattern_spmm_kernel(PatDev P, const double* __restrict__ X, int ld,
+                                                          double alpha, EpiDev E, double* out,
+                                                          double* ws, double* dots_out) {
+    constexpr int NOPS = 2 * CL_MAXY + 1;   // Y[0..3], out(4)->index CL_MAXY, Z[0..3] at 5..8
+    double acc[8];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) acc[d] = 0.0;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G;                       // lane within group
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - gl));
+    const int64_t groups_total = (int64_t)gridDim.x * (NT / G);
+    const int64_t g0 = ((int64_t)blockIdx.x * NT + threadIdx.x) / G;
+    const int ncol_chunk = G * VEC;
+
+    for (int64_t row = g0; row < P.nrows + 0; row += groups_total) {
+        const int64_t s0 = __ldg(P.indptr + row), s1 = __ldg(P.indptr + row + 1);
+        for (int c0 = 0; c0 < ld; c0 += ncol_chunk) {
+            const int col = c0 + gl * VEC;
+            const bool active = col < ld;
+            double2 sum = make_double2(0.0, 0.0);
+            for (int64_t base = s0; base < s1; base += G) {
+                const int64_t s = base + gl;
+                int jj = 0;
+                double cc = 0.0;
+                if (s < s1) {
+                    jj = __ldg(P.indices + s);
+                    cc = slot_coef(P, s);
+                }
+                const int cnt = (int)min((int64_t)G, s1 - base);
+#pragma unroll 4
+                for (int t = 0; t < cnt; ++t) {
+                    const int j = __shfl_sync(gmask, jj, (lane - gl) + t);
+                    const double c = __shfl_sync(gmask, cc, (lane - gl) + t);
+                    if (active) {
+                        if (VEC == 2) {
+                            double2 x = ld2(X + (int64_t)j * ld + col);
+                            sum.x = fma(c, x.x, sum.x);
+                            sum.y = fma(c, x.y, sum.y);
+                        } else {
+                            sum.x = fma(c, __ldg(X + (int64_t)j * ld + col), sum.x);
+                        }
+                    }
+                }
+            }
+            if (active) {
+                const int64_t off = row * (int64_t)ld + col;
+                double2 ops[NOPS];
+                double2 o = make_double2(alpha * sum.x, alpha * sum.y);
+#pragma unroll
+                for (int j = 0; j < CL_MAXY; ++j) {
+                    if (j < E.ny) {
+                        double2 y = VEC == 2 ? ld2cs(E.Y[j] + off) : make_double2(E.Y[j][off], 0.0);
+                        ops[j] = y;
+                        o = axpy2(E.ycoef[j], y, o);
+                    } else {
+                        ops[j] = make_double2(0.0, 0.0);
+                    }
+                }
+                if (VEC == 1) o.y = 0.0;
+                ops[CL_MAXY] = o;
+#pragma unroll
+                for (int j = 0; j < CL_MAXY; ++j) {
+                    if (j < E.nz) ops[CL_MAXY + 1 + j] = VEC == 2 ? ld2cs(E.Z[j] + off) : make_double2(E.Z[j][off], 0.0);
+                    else ops[CL_MAXY + 1 + j] = make_double2(0.0, 0.0);
+                }
+                if (out != nullptr) {
+                    if (VEC == 2) st2(out + off, o);
+                    else out[off] = o.x;
+                }
+#pragma unroll
+                for (int d = 0; d < 8; ++d)
+                    if (d < E.ndot) {
+                        int ia = E.da[d] == CL_OUT ? CL_MAXY : (E.da[d] >= 16 ? CL_MAXY + 1 + (E.da[d] - 16) : E.da[d]);
+                        int ib = E.db[d] == CL_OUT ? CL_MAXY : (E.db[d] >= 16 ? CL_MAXY + 1 + (E.db[d] - 16) : E.db[d]);
+                        acc[d] += dot2(select2(ops, ia), select2(ops, ib));
+                    }
+            }
+        }
+    }
+    if (E.ndot > 0) reduce_and_finish<8>(acc, E.ndot, ws, dots_out);
+}
+
+// ---------------------------------------------------------------------------
+// fused A(X Y^T): compressed outer product + stacked constraint product
+// ---------------------------------------------------------------------------
+
+template <int G, int VEC>
+__device__ __forceinline__ double group_dot(const double* __restrict__ X, const double* __restrict__ Y,
+                                            int64_t i, int64_t j, int ld, int gl, unsigned gmask) {
+    double p = 0.0;
+    for (int col = gl * VEC; col < ld; col += G * VEC) {
+        if (VEC == 2) p += dot2(ld2(X + i * ld + col), ld2(Y + j * ld + col));
+        else p += __ldg(X + i * ld + col) * __ldg(Y + j * ld + col);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) p += __shfl_xor_sync(gmask, p, o);
+    return p;
+}
+
+template <int G, int VEC>
+__global__ void __launch_bounds__(NT) constraint_kernel(int64_t m, const int64_t* __restrict__ indptr,
+                                                        const int32_t* __restrict__ pi,
+                                                        const int32_t* __restrict__ pj,
+                                                        const double* __restrict__ val, int ld,
+                                                        const double* X1, const double* Y1,
+                                                        const double* X2, const double* Y2, double* out1,
+                                                        const double* X3, const double* Y3, double* out2) {
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - gl));
+    const int64_t groups_total = (int64_t)gridDim.x * (NT / G);
+    for (int64_t c = ((int64_t)blockIdx.x * NT + threadIdx.x) / G; c < m; c += groups_total) {
+        const int64_t t0 = __ldg(indptr + c), t1 = __ldg(indptr + c + 1);
+        double a1 = 0.0, a2 = 0.0;
+        for (int64_t t = t0; t < t1; ++t) {
+            const int64_t i = __ldg(pi + t), j = __ldg(pj + t);
+            const double v = __ldg(val + t);
+            double x = group_dot<G, VEC>(X1, Y1, i, j, ld, gl, gmask);
+            if (X2 != nullptr) x += group_dot<G, VEC>(X2, Y2, i, j, ld, gl, gmask);
+            a1 += v * x;
+            if (X3 != nullptr) a2 += v * group_dot<G, VEC>(X3, Y3, i, j, ld, gl, gmask);
+        }
+        if (gl == 0) {
+            out1[c] = a1;
+            if (X3 != nullptr) out2[c] = a2;
+        }
+    }
+}
+
+template <int G, int VEC>
+__global__ void __launch_bounds__(NT) sddmm_kernel(int64_t K, const int32_t* __restrict__ imap,
+                                                   const int32_t* __restrict__ jmap, int ld,
+                                                   const double* X, const double* Y, double* x) {
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - gl));
+    const int64_t groups_total = (int64_t)gridDim.x * (NT / G);
+    for (int64_t k = ((int64_t)blockIdx.x * NT + threadIdx.x) / G; k < K; k += groups_total) {
+        double p = group_dot<G, VEC>(X, Y, __ldg(imap + k), __ldg(jmap + k), ld, gl, gmask);
+        if (gl == 0) x[k] = p;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// diagonal-constraint (MaxCut-shaped) fused ALM update
+// ---------------------------------------------------------------------------
+
+struct DiagDev {
+    int64_t n;
+    int ld;
+    const double* aval;
+    double tau, rho, scale;
+    double* R; const double* D; double* CR; const double* CD;
+    const double* ax; double* ax_out; const double* q1; const double* q2;
+    const double* lam; const double* b;
+    const double* g_old; double* g_new; double* y;
+    int nh;
+    const double* H[CL_MAXIN];
+    int refresh;
+};
+
+// Dots (fixed layout, see culorads.h):
+//  0 <CR,R>  1 <g,g>  2 <y,D>  3 lam·res  4 res·res  5 <y,y>  6 <g,y>
+//  7+h <g,H_h>   7+CL_MAXIN+h <y,H_h>
+// One thread per double2 of the flat n*ld factor; every thread of a row
+// recomputes the row's constraint scalars from the (read-only) m-vectors and
+// the row owner (first double2 of the row) writes ax_out and adds the m-dots.
+__global__ void __launch_bounds__(NT) diag_update_kernel(DiagDev a, double* ws, double* dots_out) {
+    constexpr int ND = 7 + 2 * CL_MAXIN;
+    double acc[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) acc[d] = 0.0;
+    const int half = a.ld >> 1;
+    const int64_t n2 = a.n * half;
+    const int64_t stride = (int64_t)gridDim.x * NT;
+    for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < n2; k += stride) {
+        const int64_t row = k / half;
+        const bool owner = (k - row * half) == 0;
+        double axr = __ldg(a.ax + row);
+        if (!a.refresh) axr = axr + a.tau * __ldg(a.q1 + row) + a.tau * a.tau * __ldg(a.q2 + row);
+        const double res = axr - __ldg(a.b + row);
+        const double lam = __ldg(a.lam + row);
+        const double w = lam + a.rho * res;
+        if (owner) {
+            a.ax_out[row] = axr;
+            acc[3] += lam * res;
+            acc[4] += res * res;
+        }
+        const double wa = w * __ldg(a.aval + row);
+        const int64_t off = 2 * k;
+        double2 R = ld2cs(a.R + off), CR = ld2cs(a.CR + off);
+        const double2 D = ld2cs(a.D + off);
+        if (!a.refresh) {
+            const double2 CD = ld2cs(a.CD + off);
+            R = axpy2(a.tau, D, R);
+            CR = axpy2(a.tau, CD, CR);
+            st2(a.R + off, R);
+            st2(a.CR + off, CR);
+        }
+        // g = 2 S R with S = scale*C + A*(w): 2*(w_i a_i R_i + scale*CR_i)  (alm.py:245)
+        double2 g;
+        g.x = 2.0 * (wa * R.x + a.scale * CR.x);
+        g.y = 2.0 * (wa * R.y + a.scale * CR.y);
+        const double2 go = ld2cs(a.g_old + off);
+        const double2 y = make_double2(g.x - go.x, g.y - go.y);
+        st2(a.g_new + off, g);
+        st2(a.y + off, y);
+        acc[0] += dot2(CR, R);
+        acc[1] += dot2(g, g);
+        acc[2] += dot2(y, D);
+        acc[5] += dot2(y, y);
+        acc[6] += dot2(g, y);
+#pragma unroll
+        for (int h = 0; h < CL_MAXIN; ++h)
+            if (h < a.nh) {
+                const double2 hv = ld2cs(a.H[h] + off);
+                acc[7 + h] += dot2(g, hv);
+                acc[7 + CL_MAXIN + h] += dot2(y, hv);
+            }
+    }
+    reduce_and_finish<ND>(acc, ND, ws, dots_out);
+}
+
+// ---------------------------------------------------------------------------
+// Lanczos basis projections
+// ---------------------------------------------------------------------------
+
+#define BP_TILE 8
+#define BP_CHUNKS NSM
+
+__global__ void __launch_bounds__(NT) basis_project_kernel(const double* __restrict__ Q, int64_t ldq, int kc,
+                                                           int64_t n, const double* __restrict__ v,
+                                                           double* ws) {
+    const int chunk = blockIdx.x;
+    const int t0 = blockIdx.y * BP_TILE;
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t k0 = chunk * per, k1 = min(n, k0 + per);
+    double acc[BP_TILE];
+#pragma unroll
+    for (int t = 0; t < BP_TILE; ++t) acc[t] = 0.0;
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += NT) {
+        const double vk = __ldg(v + k);
+#pragma unroll
+        for (int t = 0; t < BP_TILE; ++t)
+            if (t0 + t < kc) acc[t] += __ldg(Q + (int64_t)(t0 + t) * ldq + k) * vk;
+    }
+    __shared__ double sh[NWARP][BP_TILE];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int t = 0; t < BP_TILE; ++t) {
+        double s = warp_sum(acc[t]);
+        if (lane == 0) sh[wid][t] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < BP_TILE && t0 + threadIdx.x < kc) {
+        double s = 0.0;
+        for (int w = 0; w < NWARP; ++w) s += sh[w][threadIdx.x];
+        ws[(int64_t)chunk * kc + t0 + threadIdx.x] = s;
+    }
+}
+
+__global__ void basis_project_finish(const double* ws, int nchunks, int kc, double* h) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < kc; t += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < nchunks; ++c) s += ws[(int64_t)c * kc + t];
+        h[t] = s;
+    }
+}
+
+__global__ void __launch_bounds__(NT) basis_subtract_kernel(const double* __restrict__ Q, int64_t ldq, int kc,
+                                                            int64_t n, const double* __restrict__ h,
+                                                            double* v) {
+    extern __shared__ double hs[];
+    for (int t = threadIdx.x; t < kc; t += NT) hs[t] = h[t];
+    __syncthreads();
+    for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < n; k += (int64_t)gridDim.x * NT) {
+        double s = 0.0;
+        for (int t = 0; t < kc; ++t) s += hs[t] * __ldg(Q + (int64_t)t * ldq + k);
+        v[k] -= s;
+    }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+const char* cl_version(void) { return "culorads-b200 0.1 sm_100a"; }
+
+int cl_device_ok(void) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return 0;
+    return p.major == 10 ? 1 : 0;
+}
+
+int cl_lincomb(const cl_lincomb_args* args, int64_t N, double* dots_out, double* ws, void* stream) {
+    if (args == nullptr || N < 0 || args->nin < 0 || args->nin > CL_MAXIN) return CL_EARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    LcDev d;
+    d.nin = args->nin;
+    d.ndot = args->ndot;
+    d.out = args->out;
+    for (int j = 0; j < CL_MAXIN; ++j) {
+        d.in[j] = j < args->nin ? args->in[j] : nullptr;
+        d.coef[j] = j < args->nin ? args->coef[j] : 0.0;
+        if (j < args->nin && (!aligned16(args->in[j]) || args->in[j] == nullptr)) return CL_EARG;
+    }
+    if (d.out != nullptr && !aligned16(d.out)) return CL_EARG;
+    for (int j = 0; j < CL_MAXDOT; ++j) { d.da[j] = args->da[j]; d.db[j] = args->db[j]; }
+    int mode = args->mode;
+    if (mode < 0 || mode > 2) return CL_EARG;
+    if (mode == 0 && args->ndot == 0 && args->nin > 7) mode = 1;   // plain wide combination
+    if (mode == 0 && (args->nin > 7 || args->ndot > 8)) return CL_EARG;
+    if (mode == 1) d.ndot = args->ndot > 0 ? args->nin + 1 : 0;
+    if (mode == 2) {
+        if (args->out != nullptr || args->nin < 2) return CL_EARG;
+        d.ndot = args->ndot > 0 ? 2 * CL_MAXIN - 1 : 0;
+    }
+    if (d.ndot > 0 && (dots_out == nullptr || ws == nullptr)) return CL_EARG;
+    const int64_t n2 = N / 2;
+    const int tail = (int)(N & 1);
+    const int grid = red_grid(n2 + tail);
+    if (N == 0) {
+        if (d.ndot > 0) cudaMemsetAsync(dots_out, 0, sizeof(double) * d.ndot, st);
+        return CL_OK;
+    }
+    switch (mode) {
+        case 0: lincomb_kernel<0><<<grid, NT, 0, st>>>(d, n2, tail, ws, dots_out); break;
+        case 1: lincomb_kernel<1><<<grid, NT, 0, st>>>(d, n2, tail, ws, dots_out); break;
+        default: lincomb_kernel<2><<<grid, NT, 0, st>>>(d, n2, tail, ws, dots_out); break;
+    }
+    return (int)cudaGetLastError();
+}
+
+int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alpha, const cl_epilogue* epi,
+                    double* out, double* dots_out, double* ws, void* stream) {
+    if (S == nullptr || X == nullptr || ld < 1 || (ld > 1 && (ld & 1))) return CL_EARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    PatDev P;
+    P.nrows = S->nrows; P.indptr = S->indptr; P.indices = S->indices; P.cv = S->cv; P.c_coeff = S->c_coeff;
+    P.at_ptr = S->at_ptr; P.at_con = S->at_con; P.at_val = S->at_val; P.w1 = S->w1; P.w2 = S->w2;
+    EpiDev E;
+    E.ny = 0; E.nz = 0; E.ndot = 0;
+    for (int j = 0; j < CL_MAXY; ++j) { E.Y[j] = nullptr; E.Z[j] = nullptr; E.ycoef[j] = 0.0; }
+    for (int j = 0; j < 8; ++j) { E.da[j] = 0; E.db[j] = 0; }
+    if (epi != nullptr) {
+        if (epi->ny > CL_MAXY || epi->nz > CL_MAXY || epi->ndot > 8) return CL_EARG;
+        E.ny = epi->ny; E.nz = epi->nz; E.ndot = epi->ndot;
+        for (int j = 0; j < CL_MAXY; ++j) {
+            E.Y[j] = epi->Y[j]; E.Z[j] = epi->Z[j]; E.ycoef[j] = epi->ycoef[j];
+            if (ld > 1 && ((j < E.ny && !aligned16(E.Y[j])) || (j < E.nz && !aligned16(E.Z[j])))) return CL_EARG;
+        }
+        for (int j = 0; j < 8; ++j) { E.da[j] = epi->da[j]; E.db[j] = epi->db[j]; }
+    }
+    if (ld > 1 && (!aligned16(X) || (out != nullptr && !aligned16(out)))) return CL_EARG;
+    if (E.ndot > 0 && (dots_out == nullptr || ws == nullptr)) return CL_EARG;
+    if (P.nrows == 0) {
+        if (E.ndot > 0) cudaMemsetAsync(dots_out, 0, sizeof(double) * E.ndot, st);
+        return CL_OK;
+    }
+    int G;
+    if (ld == 1) G = 1;
+    else if (ld <= 2) G = 1;
+    else if (ld <= 4) G = 2;
+    else if (ld <= 8) G = 4;
+    else if (ld <= 16) G = 8;
+    else if (ld <= 32) G = 16;
+    else G = 32;
+    const int64_t threads = P.nrows * G;
+    const int grid = red_grid(threads);
+    if (ld == 1) {
+        pattern_spmm_kernel<1, 1><<<grid, NT, 0, st>>>(P, X, ld, alpha, E, out, ws, dots_out);
+    } else {
+        switch (G) {
+            case 1: pattern_spmm_kernel<1, 2><<<grid, NT, 0, st>>>(P, X, ld, alpha, E, out, ws, dots_out); break;
+            case 2: pattern_spmm_kernel<2, 2><<<grid, NT, 0, st>>>(P, X, ld, alpha, E, out, ws, dots_out); break;
+            case 4: pattern_spmm_kernel<4, 2><<<grid, NT, 0, st>>>(P, X, ld, alpha, E, out, ws, dots_out); break;
+            case 8: pattern_spmm_kernel<8, 2><<<grid, NT, 0, st>>>(P, X, ld, alpha, E, out, ws, dots_out); break;
+            case 16: pattern_spmm_kernel<16, 2><<<grid, NT, 0, st>>>(P, X, ld, alpha, E, out, ws, dots_out); break;
+            default: pattern_spmm_kernel<32, 2><<<grid, NT, 0, st>>>(P, X, ld, alpha, E, out, ws, dots_out); break;
+        }
+    }
+    return (int)cudaGetLastError();
+}
+
+int cl_constraint_eval(int64_t m, const int64_t* indptr, const int32_t* pi, const int32_t* pj, const double* val,
+                       int32_t ld, const double* X1, const double* Y1, const double* X2, const double* Y2,
+                       double* out1, const double* X3, const double* Y3, double* out2, void* stream) {
+    if (m < 0 || ld < 1 || (ld > 1 && (ld & 1)) || X1 == nullptr || Y1 == nullptr || out1 == nullptr) return CL_EARG;
+    if ((X2 == nullptr) != (Y2 == nullptr) || (X3 == nullptr) != (Y3 == nullptr)) return CL_EARG;
+    if (X3 != nullptr && out2 == nullptr) return CL_EARG;
+    if (m == 0) return CL_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int G = ld <= 2 ? 1 : ld <= 4 ? 2 : ld <= 8 ? 4 : ld <= 16 ? 8 : ld <= 32 ? 16 : 32;
+    const int64_t threads = m * G;
+    int64_t g = (threads + NT - 1) / NT;
+    const int grid = (int)(g > 65535 * 8 ? 65535 * 8 : g);
+#define CL_CK(GG)                                                                                           \
+    constraint_kernel<GG, 2><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2)
+    if (ld == 1) {
+        constraint_kernel<1, 1><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2);
+    } else {
+        switch (G) {
+            case 1: CL_CK(1); break;
+            case 2: CL_CK(2); break;
+            case 4: CL_CK(4); break;
+            case 8: CL_CK(8); break;
+            case 16: CL_CK(16); break;
+            default: CL_CK(32); break;
+        }
+    }
+#undef CL_CK
+    return (int)cudaGetLastError();
+}
+
+int cl_sddmm(int64_t K, const int32_t* imap, const int32_t* jmap, int32_t ld, const double* X, const double* Y,
+             double* x, void* stream) {
+    if (K < 0 || ld < 1 || (ld > 1 && (ld & 1))) return CL_EARG;
+    if (K == 0) return CL_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int G = ld <= 2 ? 1 : ld <= 4 ? 2 : ld <= 8 ? 4 : ld <= 16 ? 8 : ld <= 32 ? 16 : 32;
+    int64_t g = (K * G + NT - 1) / NT;
+    const int grid = (int)(g > 65535 * 8 ? 65535 * 8 : g);
+    if (ld == 1) { sddmm_kernel<1, 1><<<grid, NT, 0, st>>>(K, imap, jmap, ld, X, Y, x); }
+    else switch (G) {
+        case 1: sddmm_kernel<1, 2><<<grid, NT, 0, st>>>(K, imap, jmap, ld, X, Y, x); break;
+        case 2: sddmm_kernel<2, 2><<<grid, NT, 0, st>>>(K, imap, jmap, ld, X, Y, x); break;
+        case 4: sddmm_kernel<4, 2><<<grid, NT, 0, st>>>(K, imap, jmap, ld, X, Y, x); break;
+        case 8: sddmm_kernel<8, 2><<<grid, NT, 0, st>>>(K, imap, jmap, ld, X, Y, x); break;
+        case 16: sddmm_kernel<16, 2><<<grid, NT, 0, st>>>(K, imap, jmap, ld, X, Y, x); break;
+        default: sddmm_kernel<32, 2><<<grid, NT, 0, st>>>(K, imap, jmap, ld, X, Y, x); break;
+    }
+    return (int)cudaGetLastError();
+}
+
+int cl_diag_alm_update(const cl_diag_update_args* a, double* dots_out, double* ws, void* stream) {
+    if (a == nullptr || a->ld < 2 || (a->ld & 1) || a->nh < 0 || a->nh > CL_MAXIN) return CL_EARG;
+    if (dots_out == nullptr || ws == nullptr) return CL_EARG;
+    DiagDev d;
+    d.n = a->n; d.ld = a->ld; d.aval = a->aval; d.tau = a->tau; d.rho = a->rho; d.scale = a->scale;
+    d.R = a->R; d.D = a->D; d.CR = a->CR; d.CD = a->CD; d.ax = a->ax; d.ax_out = a->ax_out;
+    d.q1 = a->q1; d.q2 = a->q2;
+    d.lam = a->lam; d.b = a->b; d.g_old = a->g_old; d.g_new = a->g_new; d.y = a->y; d.nh = a->nh;
+    d.refresh = a->refresh;
+    for (int j = 0; j < CL_MAXIN; ++j) d.H[j] = j < a->nh ? a->H[j] : nullptr;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t n2 = a->n * (a->ld / 2);
+    diag_update_kernel<<<red_grid(n2), NT, 0, st>>>(d, ws, dots_out);
+    return (int)cudaGetLastError();
+}
+
+int cl_basis_project(const double* Q, int64_t ldq, int32_t k_cnt, int64_t n, const double* v, double* h, double* ws,
+                     void* stream) {
+    if (k_cnt < 0 || (int64_t)k_cnt * BP_CHUNKS > CL_WS_DOUBLES) return CL_EARG;
+    if (k_cnt == 0) return CL_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    dim3 grid(BP_CHUNKS, (k_cnt + BP_TILE - 1) / BP_TILE);
+    basis_project_kernel<<<grid, NT, 0, st>>>(Q, ldq, k_cnt, n, v, ws);
+    basis_project_finish<<<(k_cnt + 127) / 128, 128, 0, st>>>(ws, BP_CHUNKS, k_cnt, h);
+    return (int)cudaGetLastError();
+}
+
+int cl_basis_subtract(const double* Q, int64_t ldq, int32_t k_cnt, int64_t n, const double* h, double* v,
+                      void* stream) {
+    if (k_cnt < 0 || k_cnt > 4096) return CL_EARG;
+    if (k_cnt == 0 || n == 0) return CL_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int64_t g = (n + NT - 1) / NT;
+    const int grid = (int)(g > NSM * 16 ? NSM * 16 : g);
+    basis_subtract_kernel<<<grid, NT, k_cnt * sizeof(double), st>>>(Q, ldq, k_cnt, n, h, v);
+    return (int)cudaGetLastError();
+}
+
+}  // extern "C"

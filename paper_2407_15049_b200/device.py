@@ -1,0 +1,190 @@
+"""Device runtime: stream, reduction workspace, scalar slab, kernel launchers.
+
+torch supplies device memory and the stream (plumbing only); every compute
+launch goes through libculorads (``_lib``). Reductions land in a device
+"scalar slab"; the host reads a prefix of it with one pinned copy + stream
+sync at each decision point of the algorithm (``fetch``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import CL_MAXDOT, CL_MAXIN, CL_MAXY, CL_OUT, check
+
+F64 = torch.float64
+I32 = torch.int32
+I64 = torch.int64
+
+SLAB = 4096
+
+
+def ptr(t):
+    """Raw device address of a tensor (or None -> NULL)."""
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def padded_ld(r):
+    """Leading dimension of an n x r factor: r rounded up to even (16-byte rows)."""
+    return max(2, r + (r & 1))
+
+
+class Device:
+    """Per-solve device context (one CUDA stream, one workspace)."""
+
+    def __init__(self, device=None):
+        self.lib = _lib.load(require_device=True)
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.dev = torch.device(device)
+        self.stream = torch.cuda.current_stream(self.dev)
+        self.ws = torch.zeros(_lib.CL_WS_ALLOC, dtype=F64, device=self.dev)
+        self.slab = torch.zeros(SLAB, dtype=F64, device=self.dev)
+        self.host = torch.zeros(SLAB, dtype=F64, pin_memory=True)
+        self.launches = 0
+
+    # -- plumbing ---------------------------------------------------------
+    @property
+    def sp(self):
+        return ctypes.c_void_p(self.stream.cuda_stream)
+
+    def slot(self, k, count=1):
+        """Device pointer to slab[k:k+count]."""
+        return ctypes.c_void_p(self.slab.data_ptr() + 8 * k)
+
+    def fetch(self, count):
+        """Copy slab[:count] to the host (pinned) and wait; returns numpy view."""
+        self.host[:count].copy_(self.slab[:count], non_blocking=True)
+        self.stream.synchronize()
+        return self.host[:count].numpy()
+
+    def zeros(self, *shape):
+        return torch.zeros(*shape, dtype=F64, device=self.dev)
+
+    def empty(self, *shape):
+        return torch.empty(*shape, dtype=F64, device=self.dev)
+
+    def put(self, a, dtype=F64):
+        a = np.ascontiguousarray(a)
+        return torch.as_tensor(a).to(device=self.dev, dtype=dtype, non_blocking=False)
+
+    # -- launches ---------------------------------------------------------
+    def lincomb(self, out, ins, coefs, dots=None, at=0, mode=_lib.CL_DOT_PAIRS, N=None):
+        """out = sum coefs[j]*ins[j]; dots -> slab[at:].
+
+        dots: list of (a, b) operand pairs (mode PAIRS; use 'out' or input index),
+        or True for modes OUT_ALL / FIRST_TWO.
+        """
+        a = _lib.LincombArgs()
+        a.nin = len(ins)
+        a.mode = mode
+        if len(ins) > CL_MAXIN:
+            raise ValueError("too many operands")
+        for j, (t, c) in enumerate(zip(ins, coefs)):
+            a.inp[j] = t.data_ptr()
+            a.coef[j] = float(c)
+        a.out = out.data_ptr() if out is not None else None
+        ndot = 0
+        if mode == _lib.CL_DOT_PAIRS and dots:
+            for d, (x, y) in enumerate(dots):
+                a.da[d] = CL_OUT if x == "out" else x
+                a.db[d] = CL_OUT if y == "out" else y
+            ndot = len(dots)
+        elif dots:
+            ndot = 1
+        a.ndot = ndot
+        if N is None:
+            N = (out if out is not None else ins[0]).numel()
+        rc = self.lib.cl_lincomb(ctypes.byref(a), int(N), self.slot(at) if ndot else None,
+                                 ptr(self.ws) if ndot else None, self.sp)
+        self.launches += 1
+        check(rc, "cl_lincomb")
+
+    def spmm(self, pat, X, ld, alpha=1.0, out=None, Y=(), ycoef=(), Z=(), dots=None, at=0,
+             c_coeff=None, w1=None, w2=None, use_cv=True, use_at=True):
+        """out = alpha * S X + sum ycoef*Y over a device pattern (see linops.DevicePattern)."""
+        P = pat.struct(c_coeff=c_coeff, w1=w1, w2=w2, use_cv=use_cv, use_at=use_at)
+        e = _lib.Epilogue()
+        e.ny = len(Y)
+        for j, (t, c) in enumerate(zip(Y, ycoef)):
+            e.Y[j] = t.data_ptr()
+            e.ycoef[j] = float(c)
+        e.nz = len(Z)
+        for j, t in enumerate(Z):
+            e.Z[j] = t.data_ptr()
+        nd = 0
+        if dots:
+            for d, (x, y) in enumerate(dots):
+                e.da[d] = _op_code(x)
+                e.db[d] = _op_code(y)
+            nd = len(dots)
+        e.ndot = nd
+        rc = self.lib.cl_pattern_spmm(ctypes.byref(P), ptr(X), int(ld), float(alpha), ctypes.byref(e),
+                                      ptr(out), self.slot(at) if nd else None,
+                                      ptr(self.ws) if nd else None, self.sp)
+        self.launches += 1
+        check(rc, "cl_pattern_spmm")
+
+    def constraint_eval(self, con, ld, X1, Y1, out1, X2=None, Y2=None, X3=None, Y3=None, out2=None):
+        rc = self.lib.cl_constraint_eval(int(con.m), ptr(con.indptr), ptr(con.pi), ptr(con.pj),
+                                         ptr(con.val), int(ld), ptr(X1), ptr(Y1), ptr(X2), ptr(Y2),
+                                         ptr(out1), ptr(X3), ptr(Y3), ptr(out2), self.sp)
+        self.launches += 1
+        check(rc, "cl_constraint_eval")
+
+    def sddmm(self, imap, jmap, ld, X, Y, out):
+        rc = self.lib.cl_sddmm(int(imap.numel()), ptr(imap), ptr(jmap), int(ld), ptr(X), ptr(Y),
+                               ptr(out), self.sp)
+        self.launches += 1
+        check(rc, "cl_sddmm")
+
+    def diag_update(self, args, at=0):
+        rc = self.lib.cl_diag_alm_update(ctypes.byref(args), self.slot(at), ptr(self.ws), self.sp)
+        self.launches += 1
+        check(rc, "cl_diag_alm_update")
+
+    def basis_project(self, Q, kc, n, v, h):
+        rc = self.lib.cl_basis_project(ptr(Q), int(Q.shape[1]), int(kc), int(n), ptr(v), ptr(h),
+                                       ptr(self.ws), self.sp)
+        self.launches += 2
+        check(rc, "cl_basis_project")
+
+    def basis_subtract(self, Q, kc, n, h, v):
+        rc = self.lib.cl_basis_subtract(ptr(Q), int(Q.shape[1]), int(kc), int(n), ptr(h), ptr(v),
+                                        self.sp)
+        self.launches += 1
+        check(rc, "cl_basis_subtract")
+
+
+def _op_code(x):
+    """Epilogue operand code: ('y', j) -> j, 'out' -> CL_OUT, ('z', j) -> 16 + j."""
+    if x == "out":
+        return CL_OUT
+    kind, j = x
+    if kind == "y":
+        return j
+    if kind == "z":
+        return 16 + j
+    raise ValueError(x)
+
+
+_DEFAULT = {}
+
+
+def default_device():
+    """Process-wide Device for the current CUDA device (created lazily)."""
+    key = torch.cuda.current_device()
+    d = _DEFAULT.get(key)
+    if d is None:
+        d = Device()
+        _DEFAULT[key] = d
+    return d
+
+
+assert CL_MAXDOT >= 48 and CL_MAXY == 4
