@@ -1,0 +1,51 @@
+"""Seeded synthetic MaxCut graphs for benchmarks and scaling runs.
+
+* ``random_sparse`` -- uniform random simple graph with about n*deg/2 unit
+  edges (BASELINE configs: "synthetic random sparse graph, avg degree ~6").
+* ``delaunay_like`` -- triangulated periodic lattice with randomly permuted
+  vertex labels: every vertex has degree 6 like a planar Delaunay mesh
+  (the paper's 10^7-scale instances are delaunay_n23/n24), no locality.
+
+Edges are returned sorted by (u, v) with u < v, which lets ``build_maxcut``
+take its linear-time ordering path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .problem import GraphEdgeList
+
+
+def _finish(n, u, v, rng, target=None):
+    a = np.minimum(u, v)
+    b = np.maximum(u, v)
+    keep = a != b
+    code = np.unique(a[keep] * n + b[keep])
+    if target is not None and code.size > target:
+        code = np.sort(rng.choice(code, size=target, replace=False))
+    return GraphEdgeList(n, code // n, code % n, np.ones(code.size))
+
+
+def random_sparse(n, deg=6.0, seed=0):
+    rng = np.random.default_rng(seed)
+    me = int(round(n * deg / 2))
+    # loops and repeats are dropped (a ~deg/n fraction), so |E| is just under n*deg/2
+    u = rng.integers(0, n, size=me, dtype=np.int64)
+    v = rng.integers(0, n, size=me, dtype=np.int64)
+    return _finish(n, u, v, rng)
+
+
+def delaunay_like(n, seed=0):
+    rng = np.random.default_rng(seed)
+    side = int(round(np.sqrt(n)))
+    n = side * side
+    i, j = np.divmod(np.arange(n, dtype=np.int64), side)
+    vid = lambda a, b: (a % side) * side + (b % side)  # noqa: E731
+    u = np.concatenate([np.arange(n, dtype=np.int64)] * 3)
+    v = np.concatenate([vid(i, j + 1), vid(i + 1, j), vid(i + 1, j + 1)])
+    perm = rng.permutation(n).astype(np.int64)
+    return _finish(n, perm[u], perm[v], rng)
+
+
+GENERATORS = {"random_sparse": random_sparse, "delaunay_like": delaunay_like}

@@ -62,6 +62,20 @@ def random_graph(rng, n, deg):
     return rprob.GraphEdgeList(n, code // n, code % n, np.ones(len(code)))
 
 
+def lattice(side, rng):
+    """Triangulated periodic lattice, random labels (Delaunay-like, degree 6)."""
+    n = side * side
+    i, j = np.divmod(np.arange(n), side)
+    vid = lambda a, b: (a % side) * side + (b % side)  # noqa: E731
+    u = np.concatenate([np.arange(n)] * 3)
+    v = np.concatenate([vid(i, j + 1), vid(i + 1, j), vid(i + 1, j + 1)])
+    perm = rng.permutation(n)
+    u, v = perm[u], perm[v]
+    a, b = np.minimum(u, v), np.maximum(u, v)
+    code = np.unique(a * n + b)
+    return rprob.GraphEdgeList(n, code // n, code % n, np.ones(len(code)))
+
+
 def completion(rng, n2, n1, rank, frac):
     A = rng.standard_normal((n2, rank))
     B = rng.standard_normal((n1, rank))
@@ -140,9 +154,46 @@ def spectral_case():
                         residual=est.residual, basis=est.basis_size)
 
 
+def _trace(rep):
+    return np.array([r[2:7] for r in rep.trace_rows], dtype=np.float64).reshape(-1, 5)
+
+
+def _first_dev(tr, ref, tol=1e-9):
+    """First trace row where objective or err1 leaves the reference by > tol (relative)."""
+    k = min(len(tr), len(ref))
+    d = np.abs(tr[:k, 0] - ref[:k, 0]) / np.maximum(1.0, np.abs(ref[:k, 0]))
+    e = np.abs(tr[:k, 1] - ref[:k, 1]) / (1e-4 + np.abs(ref[:k, 1]))
+    bad = np.nonzero((d > tol) | (e > tol))[0]
+    return int(bad[0]) if bad.size else k
+
+
+def perturbed_runs(p, cfg, ref_trace, factors=(1.0, -1.0, 2.0, -2.0)):
+    """Re-run the reference with its L-BFGS direction scaled by (1 + f*2^-52).
+
+    The reference is chaotic: a one-ulp change of one vector moves later
+    iterates. The spread of these runs is the reference's own reproducibility
+    envelope, against which the device solver is judged.
+    """
+    orig = ralm.lbfgs_direction
+    out = []
+    try:
+        for f in factors:
+            scale = 1.0 + f * 2.0 ** -52
+            ralm.lbfgs_direction = lambda g, h, _s=scale: orig(g, h) * _s
+            rep = rdrv.solve(p, rdrv.SolverConfig(**cfg))
+            out.append((_first_dev(_trace(rep), ref_trace), rep.objective, len(rep.trace_rows),
+                        rep.status))
+    finally:
+        ralm.lbfgs_direction = orig
+    return out
+
+
 def solve_case(name, p, **cfg):
     rep = rdrv.solve(p, rdrv.SolverConfig(**cfg))
     out = prob_arrays(p)
+    pert = perturbed_runs(p, cfg, _trace(rep))
+    out.update(ulp_horizon=np.array([x[0] for x in pert]), ulp_objective=np.array([x[1] for x in pert]),
+               ulp_rows=np.array([x[2] for x in pert]), ulp_status=np.array([x[3] for x in pert]))
     tr = np.array([r[2:7] for r in rep.trace_rows], dtype=np.float64).reshape(-1, 5)
     stage = np.array([0 if r[0] == "alm" else 1 for r in rep.trace_rows], dtype=np.int8)
     out.update(trace=tr, trace_stage=stage, objective=rep.objective, err1=rep.err1,
@@ -153,7 +204,8 @@ def solve_case(name, p, **cfg):
                status=rep.status, cfg=json.dumps(cfg))
     np.savez_compressed(os.path.join(HERE, f"solve_{name}.npz"), **out)
     print(name, rep.status, rep.objective, rep.err1, rep.err2, rep.err3, rep.rank_history,
-          rep.alm_inner_iterations, rep.admm_steps, rep.reopt_rounds, rep.time_total_s, flush=True)
+          rep.alm_inner_iterations, rep.admm_steps, rep.reopt_rounds, rep.time_total_s,
+          "ulp:", pert, flush=True)
 
 
 def main():
@@ -170,7 +222,9 @@ def main():
     solve_case("single_edge", rprob.build_maxcut(rprob.GraphEdgeList.from_edges(2, [(0, 1, 3.0)])))
     solve_case("g1_like", rprob.build_maxcut(random_graph(np.random.default_rng(1), 800, 48)))
     solve_case("maxcut_2k_deg6", rprob.build_maxcut(random_graph(np.random.default_rng(2), 2000, 6)),
-               time_limit=120.0)
+               admm_step_cap=1500, max_reopts=0)
+    solve_case("delaunay_45", rprob.build_maxcut(lattice(45, np.random.default_rng(5))),
+               admm_step_cap=1500, max_reopts=1)
     solve_case("completion_30", rprob.build_matrix_completion(
         completion(np.random.default_rng(3), 30, 30, 2, 0.4)))
     solve_case("random_sdp", random_problem(np.random.default_rng(4), 10, 5, density=0.3,

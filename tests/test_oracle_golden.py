@@ -70,7 +70,7 @@ def test_oracle_lanczos_matches_reference():
     assert abs(res - float(z["residual"])) <= 1e-12
 
 
-@pytest.mark.parametrize("case", [c for c in solve_cases() if c != "maxcut_2k_deg6"])
+@pytest.mark.parametrize("case", solve_cases())
 def test_oracle_solve_trace_matches_reference(case):
     z = load(f"solve_{case}.npz")
     p = problem_from(z)
