@@ -338,10 +338,12 @@ class AlmCore:
 
     # gradient + value (+ pair inner products) -------------------------
     def grad_value(self, R, lam, rho, scale, g_old, g_new, ybuf, H, D=None, CD=None, tau=0.0,
-                   refresh=True):
+                   refresh=True, fetch=True):
         """Step (unless refresh), gradient 2 S R and the Lagrangian pieces.
 
-        Returns dict: crr, gg, yd, lres, rr, yy, gy, gH[list], yH[list]."""
+        Returns dict: crr, gg, yd, lres, rr, yy, gy, gH[list], yH[list]; with
+        ``fetch=False`` (diagonal path only) the launch is queued and None is
+        returned -- the reductions stay in the device slab."""
         dev, ops = self.dev, self.ops
         b = ops.b
         nh = len(H)
@@ -366,6 +368,8 @@ class AlmCore:
             dev.diag_update(a, at=self.S_UPD)
             if not refresh:
                 self.ax, self.ax2 = self.ax2, self.ax
+            if not fetch:
+                return None
             s = dev.fetch(self.S_UPD + 7 + 2 * _lib.CL_MAXIN)[self.S_UPD:]
             return dict(crr=s[0], gg=s[1], yd=s[2], lres=s[3], rr=s[4], yy=s[5], gy=s[6],
                         gH=list(s[7:7 + nh]), yH=list(s[7 + _lib.CL_MAXIN:7 + _lib.CL_MAXIN + nh]))
