@@ -88,13 +88,25 @@ typedef struct {
     const double* at_val;
     const double* w1;
     const double* w2;
+    int64_t nnz;            /* slots (indptr[nrows]); the host knows it, the launch needs it */
+    double* scratch;        /* nnz+16 doubles for assembled coefficients, or NULL */
 } cl_pattern;
 
-/* Pattern times factor with a fused epilogue (linops.py:199 spmm, and the
+/* Pattern times factor with a fused epilogue (linops.py:122 spmm, and the
  * products S R of alm.py:245, S V of admm.py:49/62):
  *   out[i,:] = alpha * (S X)[i,:] + sum_{j<ny} ycoef[j] * Y[j][i,:]
  *   dots[d]  = sum op(da[d]) * op(db[d])   over all n*ld entries,
- *              operand 0..ny-1 = Y[j], CL_OUT = out, 16+j = Z[j].       */
+ *              operand 0..ny-1 = Y[j], CL_OUT = out, 16+j = Z[j].
+ * Execution: a persistent tiled kernel stages each tile's row pointers,
+ * column indices and slot values in shared memory with bulk copies (TMA
+ * engine, mbarrier-completed, one tile ahead), so only the factor-row
+ * gathers are global loads on the critical path. Slot values are cv
+ * (c_coeff folded into alpha) or, when adjoint rows are active, coefficients
+ * assembled into `scratch` by a streaming pre-pass. The copies read 16-byte
+ * aligned supersets: indptr, indices, cv and scratch must stay readable for
+ * 16 elements past their logical end (the Python host pads every array).
+ * Without scratch (adjoint rows active) the coefficients are assembled
+ * inside a row-group kernel instead.                                     */
 typedef struct {
     int32_t ny;
     const double* Y[CL_MAXY];
@@ -122,12 +134,20 @@ int cl_constraint_eval(int64_t m, const int64_t* indptr, const int32_t* pi, cons
                        double* out1, const double* X3, const double* Y3, double* out2,
                        void* stream);
 
+/* Diagonal-constraint form of cl_constraint_eval (constraint c is the single
+ * entry a_c e_c e_c^T, m == n; MaxCut, problem.py:435 build_maxcut): the same
+ * outputs from row dot products, out1[c] = a_c (X1[c].Y1[c] + X2[c].Y2[c]),
+ * out2[c] = a_c X3[c].Y3[c], with no index traffic. */
+int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const double* X1, const double* Y1,
+                            const double* X2, const double* Y2, double* out1, const double* X3, const double* Y3,
+                            double* out2, void* stream);
+
 /* Gathered outer product at K positions (linops.py:49), x[k] = X[imap[k]]·Y[jmap[k]]. */
 int cl_sddmm(int64_t K, const int32_t* imap, const int32_t* jmap, int32_t ld,
              const double* X, const double* Y, double* x, void* stream);
 
 /* Diagonal-constraint fast path for problems whose constraint c is the single
- * diagonal entry a_c * e_c e_c^T (m == n; MaxCut, problem.py:387): the ALM
+ * diagonal entry a_c * e_c e_c^T (m == n; MaxCut, problem.py:435): the ALM
  * step update and gradient (alm.py:306-318) become row-local and fuse into one pass.
  *   R  += tau*D;  CR += tau*CD;  ax_out[c] = ax[c] + tau*q1[c] + tau^2*q2[c]
  *   w[c] = lam[c] + rho*(ax[c]-b[c]);  g_new = 2*(w[row]*a*R + scale*CR)

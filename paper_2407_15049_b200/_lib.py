@@ -24,7 +24,7 @@ CL_OUT = 255
 CL_DOT_PAIRS, CL_DOT_OUT_ALL, CL_DOT_FIRST_TWO = 0, 1, 2
 CL_EARG = 1001
 
-EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_sddmm",
+EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_diag_constraint_eval", "cl_sddmm",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
            "cl_version", "cl_device_ok")
 
@@ -42,7 +42,8 @@ class LincombArgs(ctypes.Structure):
 
 class Pattern(ctypes.Structure):
     _fields_ = [("nrows", I64), ("indptr", P), ("indices", P), ("cv", P), ("c_coeff", D),
-                ("at_ptr", P), ("at_con", P), ("at_val", P), ("w1", P), ("w2", P)]
+                ("at_ptr", P), ("at_con", P), ("at_val", P), ("w1", P), ("w2", P),
+                ("nnz", I64), ("scratch", P)]
 
 
 class Epilogue(ctypes.Structure):
@@ -72,6 +73,7 @@ def _declare(lib):
     lib.cl_pattern_spmm.argtypes = [ctypes.POINTER(Pattern), P, I32, D, ctypes.POINTER(Epilogue),
                                     P, P, P, P]
     lib.cl_constraint_eval.argtypes = [I64, P, P, P, P, I32, P, P, P, P, P, P, P, P, P]
+    lib.cl_diag_constraint_eval.argtypes = [I64, P, I32, P, P, P, P, P, P, P, P, P]
     lib.cl_sddmm.argtypes = [I64, P, P, I32, P, P, P, P]
     lib.cl_diag_alm_update.argtypes = [ctypes.POINTER(DiagUpdateArgs), P, P, P]
     lib.cl_basis_project.argtypes = [P, I64, I32, I64, P, P, P, P]

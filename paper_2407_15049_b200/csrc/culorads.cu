@@ -35,7 +35,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // ws layout: [CL_RED_BLOCKS * CL_MAXDOT partials][1 counter word].
 template <int ND>
 __device__ __forceinline__ void reduce_and_finish(const double (&acc)[ND], int ndot, double* ws,
-                                                  double* out) {
+                                                  double* out, int gap_at = ND, int gap = 0) {
     __shared__ double sh[NWARP][ND > 0 ? ND : 1];
     __shared__ bool last;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -69,7 +69,7 @@ __device__ __forceinline__ void reduce_and_finish(const double (&acc)[ND], int n
         for (int b = lane; b < (int)gridDim.x; b += 32)
             s += __ldcg(ws + (size_t)b * CL_MAXDOT + d);
         s = warp_sum(s);
-        if (lane == 0) out[d] = s;
+        if (lane == 0) out[d + (d >= gap_at ? gap : 0)] = s;
     }
     if (threadIdx.x == 0) *counter = 0u;
 }
@@ -367,6 +367,129 @@ __global__ void __launch_bounds__(NT) sddmm_kernel(int64_t K, const int32_t* __r
     }
 }
 
+// Diagonal constraints (constraint c is a_c e_c e_c^T, MaxCut): the stacked
+// product collapses to row dot products, streamed with no index traffic.
+// The host resolves operand aliasing (the line search passes R and D in six
+// roles) into <= 6 distinct streams; each group loads the distinct rows of DR
+// rows in one batch, then reduces every product exactly like group_dot, so
+// results equal constraint_kernel's bit for bit.
+struct DiagCon {
+    int64_t n;
+    const double* aval;
+    int ld;
+    int nop;                  // distinct operand streams
+    const double* op[6];
+    int pidx[6];              // (x, y) stream of product 1, 2, 3
+    int nprod1;               // products summed into out1 (1 or 2)
+    double* out1;
+    double* out2;             // product 3 (NULL: none)
+};
+
+template <int VEC>
+__device__ __forceinline__ double2 ldrow(const double* p, int64_t off) {
+    return VEC == 2 ? ld2(p + off) : make_double2(__ldg(p + off), 0.0);
+}
+
+template <int G, int VEC, int NOP>
+__global__ void __launch_bounds__(NT, 4) diag_constraint_kernel(DiagCon a) {
+    constexpr int DR = NOP <= 2 ? 2 : 1;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - gl));
+    const int64_t gt = (int64_t)gridDim.x * (NT / G);
+    const bool two = a.nprod1 == 2, three = a.out2 != nullptr;
+    const int ld = a.ld;
+    for (int64_t cb = ((int64_t)blockIdx.x * NT + threadIdx.x) / G; cb < a.n; cb += DR * gt) {
+        double p[DR][3];
+#pragma unroll
+        for (int u = 0; u < DR; ++u) p[u][0] = p[u][1] = p[u][2] = 0.0;
+        for (int col = gl * VEC; col < ld; col += G * VEC) {
+            double2 v[DR][NOP];
+#pragma unroll
+            for (int u = 0; u < DR; ++u) {
+                const int64_t c = cb + u * gt;
+                const int64_t off = c * ld + col;
+#pragma unroll
+                for (int k = 0; k < NOP; ++k)
+                    v[u][k] = (k < a.nop && c < a.n) ? ldrow<VEC>(a.op[k], off) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < DR; ++u) {
+                p[u][0] += dot2(select2(v[u], a.pidx[0]), select2(v[u], a.pidx[1]));
+                if (two) p[u][1] += dot2(select2(v[u], a.pidx[2]), select2(v[u], a.pidx[3]));
+                if (three) p[u][2] += dot2(select2(v[u], a.pidx[4]), select2(v[u], a.pidx[5]));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < DR; ++u) {
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) {
+                p[u][0] += __shfl_xor_sync(gmask, p[u][0], o);
+                if (two) p[u][1] += __shfl_xor_sync(gmask, p[u][1], o);
+                if (three) p[u][2] += __shfl_xor_sync(gmask, p[u][2], o);
+            }
+            const int64_t c = cb + u * gt;
+            if (gl == 0 && c < a.n) {
+                const double w = __ldg(a.aval + c);
+                const double x = two ? p[u][0] + p[u][1] : p[u][0];
+                a.out1[c] = 0.0 + w * x;
+                if (three) a.out2[c] = 0.0 + w * p[u][2];
+            }
+        }
+    }
+}
+
+// Flat variant for even ld: a block streams RB whole rows as one contiguous
+// run of double2 units (every warp load is 512 contiguous bytes, U loads in
+// flight per thread), parks the per-unit products in shared memory and lets
+// one thread per row fold its units in order. Products 1 and 2 are summed
+// per unit (q1 = A(R D^T + D R^T) in the line search).
+#define DC_U 8
+template <int NOP>
+__global__ void __launch_bounds__(NT) diag_constraint_flat_kernel(DiagCon a) {
+    __shared__ double part[2][NT * DC_U];
+    const int h2 = a.ld >> 1;
+    const int rb = (NT * DC_U) / h2;                  // rows per block iteration (>= 1)
+    const bool two = a.nprod1 == 2, three = a.out2 != nullptr;
+    const int64_t nblk = (a.n + rb - 1) / rb;
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int64_t r0 = blk * rb;
+        const int nr = (int)min((int64_t)rb, a.n - r0);
+        const int units = nr * h2;
+        const int64_t base = r0 * (int64_t)h2;         // first double2 unit
+        double2 v[DC_U][NOP];
+#pragma unroll
+        for (int u = 0; u < DC_U; ++u) {
+            const int e = threadIdx.x + u * NT;
+#pragma unroll
+            for (int k = 0; k < NOP; ++k)
+                v[u][k] = (e < units && k < a.nop) ? ld2(a.op[k] + 2 * (base + e)) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < DC_U; ++u) {
+            const int e = threadIdx.x + u * NT;
+            if (e < units) {
+                double x = dot2(select2(v[u], a.pidx[0]), select2(v[u], a.pidx[1]));
+                if (two) x += dot2(select2(v[u], a.pidx[2]), select2(v[u], a.pidx[3]));
+                part[0][e] = x;
+                if (three) part[1][e] = dot2(select2(v[u], a.pidx[4]), select2(v[u], a.pidx[5]));
+            }
+        }
+        __syncthreads();
+        for (int r = threadIdx.x; r < nr; r += NT) {
+            double s1 = 0.0, s3 = 0.0;
+            for (int q = 0; q < h2; ++q) {
+                s1 += part[0][r * h2 + q];
+                if (three) s3 += part[1][r * h2 + q];
+            }
+            const double w = __ldg(a.aval + r0 + r);
+            a.out1[r0 + r] = w * s1;
+            if (three) a.out2[r0 + r] = w * s3;
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------------------
 // diagonal-constraint (MaxCut-shaped) fused ALM update
 // ---------------------------------------------------------------------------
@@ -391,8 +514,9 @@ struct DiagDev {
 // One thread per double2 of the flat n*ld factor; every thread of a row
 // recomputes the row's constraint scalars from the (read-only) m-vectors and
 // the row owner (first double2 of the row) writes ax_out and adds the m-dots.
+template <int NH>
 __global__ void __launch_bounds__(NT) diag_update_kernel(DiagDev a, double* ws, double* dots_out) {
-    constexpr int ND = 7 + 2 * CL_MAXIN;
+    constexpr int ND = 7 + 2 * NH;
     double acc[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) acc[d] = 0.0;
@@ -437,14 +561,15 @@ __global__ void __launch_bounds__(NT) diag_update_kernel(DiagDev a, double* ws, 
         acc[5] += dot2(y, y);
         acc[6] += dot2(g, y);
 #pragma unroll
-        for (int h = 0; h < CL_MAXIN; ++h)
+        for (int h = 0; h < NH; ++h)
             if (h < a.nh) {
                 const double2 hv = ld2cs(a.H[h] + off);
                 acc[7 + h] += dot2(g, hv);
-                acc[7 + CL_MAXIN + h] += dot2(y, hv);
+                acc[7 + NH + h] += dot2(y, hv);
             }
     }
-    reduce_and_finish<ND>(acc, ND, ws, dots_out);
+    // dots_out layout is fixed by the ABI (7 + 2*CL_MAXIN): the y-row lands at 7 + CL_MAXIN
+    reduce_and_finish<ND>(acc, ND, ws, dots_out, 7 + NH, CL_MAXIN - NH);
 }
 
 // ---------------------------------------------------------------------------
@@ -504,6 +629,302 @@ __global__ void __launch_bounds__(NT) basis_subtract_kernel(const double* __rest
         for (int t = 0; t < kc; ++t) s += hs[t] * __ldg(Q + (int64_t)t * ldq + k);
         v[k] -= s;
     }
+}
+
+// ---------------------------------------------------------------------------
+// tiled CSR SpMM: row segments staged in shared memory by the bulk-copy
+// (TMA) engine, one tile ahead, so the factor-row gathers are the only
+// global loads on the critical path (linops.py:122 spmm)
+// ---------------------------------------------------------------------------
+
+#define SP_SMAX 1024        // slots staged per tile (indices + values)
+#define SP_PTRMAX 264       // row pointers per tile: TR + 1 + alignment slack, TR <= 256
+#define SP_UNROLL 8         // gathers in flight per lane
+#define SP_NY 2             // epilogue limits of the tiled path (else the row-group kernel)
+#define SP_NZ 3
+#define SP_ND 4
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+struct SpDev {
+    int64_t nrows;
+    const int64_t* indptr;
+    const int32_t* indices;
+    const double* vals;
+    const double* X;
+    int ld;
+    double alpha;
+    double* out;
+    int tr;               // rows per tile (multiple of the group count)
+    int64_t ntiles;
+};
+
+struct SpTile {
+    int64_t ptr[SP_PTRMAX];
+    int32_t idx[SP_SMAX + 8];
+    double val[SP_SMAX + 4];
+};
+
+// Thread 0: stage tile `tile` (slot range [s0, s1)) into buffer `buf`.
+// Sources are read as 16-byte aligned supersets (the host pads every array).
+__device__ __forceinline__ void sp_issue(const SpDev& a, SpTile* T, int64_t (*meta)[4], uint64_t* bar, int buf,
+                                         int64_t tile, int64_t s0, int64_t s1) {
+    const int64_t r0 = tile * a.tr;
+    const int64_t r1 = min(r0 + (int64_t)a.tr, a.nrows);
+    const int64_t pb = r0 & ~1LL, pe = (r1 + 2) & ~1LL;
+    const bool heavy = (s1 - s0) > SP_SMAX;
+    const int64_t ib = s0 & ~3LL, ie = (s1 + 3) & ~3LL;
+    const int64_t vb = s0 & ~1LL, ve = (s1 + 1) & ~1LL;
+    const uint32_t pbytes = (uint32_t)((pe - pb) * 8);
+    const uint32_t ibytes = heavy ? 0u : (uint32_t)((ie - ib) * 4);
+    const uint32_t vbytes = heavy ? 0u : (uint32_t)((ve - vb) * 8);
+    meta[buf][0] = pb;
+    meta[buf][1] = ib;
+    meta[buf][2] = vb;
+    meta[buf][3] = heavy ? 1 : 0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_tx(&bar[buf], pbytes + ibytes + vbytes);
+    bulk_g2s(T[buf].ptr, a.indptr + pb, pbytes, &bar[buf]);
+    if (ibytes) bulk_g2s(T[buf].idx, a.indices + ib, ibytes, &bar[buf]);
+    if (vbytes) bulk_g2s(T[buf].val, a.vals + vb, vbytes, &bar[buf]);
+}
+
+template <int G, int VEC, int EPI>
+__global__ void __launch_bounds__(NT, EPI == 0 ? 5 : 3) spmm_tiled_kernel(SpDev a, EpiDev E, double* ws, double* dots_out) {
+    constexpr int NG = NT / G;
+    // epilogue operand set of the tiled path: Y0, Y1, out, Z0, Z1, Z2
+    constexpr int NOPS = SP_NY + 1 + SP_NZ;
+    __shared__ __align__(128) SpTile T[2];
+    __shared__ int64_t meta[2][4];
+    __shared__ __align__(8) uint64_t bar[2];
+    double dacc[SP_ND];
+#pragma unroll
+    for (int d = 0; d < SP_ND; ++d) dacc[d] = 0.0;
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int gl = lane % G;
+    const int grp = tid / G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - gl));
+    const int rpg = a.tr / NG;
+    const int ld = a.ld;
+    const double* __restrict__ X = a.X;
+
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    int64_t t = blockIdx.x;
+    const int64_t stride = gridDim.x;
+    int64_t nx0 = 0, nx1 = 0;        // slot bounds of tile t + stride (thread 0)
+    if (tid == 0 && t < a.ntiles) {
+        const int64_t r0 = t * a.tr, r1 = min(r0 + (int64_t)a.tr, a.nrows);
+        sp_issue(a, T, meta, bar, 0, t, __ldg(a.indptr + r0), __ldg(a.indptr + r1));
+        if (t + stride < a.ntiles) {
+            const int64_t q0 = (t + stride) * a.tr, q1 = min(q0 + (int64_t)a.tr, a.nrows);
+            nx0 = __ldg(a.indptr + q0);
+            nx1 = __ldg(a.indptr + q1);
+        }
+    }
+    uint32_t phase = 0;   // bit b: parity of buffer b's next completion
+    int buf = 0;
+    for (; t < a.ntiles; t += stride, buf ^= 1) {
+        if (tid == 0) {
+            const int64_t tn = t + stride;
+            if (tn < a.ntiles) {
+                sp_issue(a, T, meta, bar, buf ^ 1, tn, nx0, nx1);
+                const int64_t tnn = tn + stride;
+                if (tnn < a.ntiles) {
+                    const int64_t q0 = tnn * a.tr, q1 = min(q0 + (int64_t)a.tr, a.nrows);
+                    nx0 = __ldg(a.indptr + q0);
+                    nx1 = __ldg(a.indptr + q1);
+                }
+            }
+        }
+        mbar_wait(&bar[buf], (phase >> buf) & 1u);
+        phase ^= (1u << buf);
+        const SpTile& B = T[buf];
+        const int64_t pb = meta[buf][0], ib = meta[buf][1], vb = meta[buf][2];
+        const bool heavy = meta[buf][3] != 0;
+        const int64_t r0 = t * a.tr;
+        const int64_t nr = min((int64_t)a.tr, a.nrows - r0);
+        for (int k = 0; k < rpg; ++k) {
+            const int lr = grp * rpg + k;
+            if (lr >= nr) break;
+            const int64_t row = r0 + lr;
+            const int64_t s0 = B.ptr[row - pb], s1 = B.ptr[row + 1 - pb];
+            for (int c0 = 0; c0 < ld; c0 += G * VEC) {
+                const int col = c0 + gl * VEC;
+                const bool active = col < ld;
+                double2 acc = make_double2(0.0, 0.0);
+                if (!heavy) {
+                    for (int64_t s = s0; s < s1; s += SP_UNROLL) {
+                        int jv[SP_UNROLL];
+                        double cv[SP_UNROLL];
+                        double2 xv[SP_UNROLL];
+#pragma unroll
+                        for (int u = 0; u < SP_UNROLL; ++u) {
+                            const bool ok = s + u < s1;
+                            jv[u] = ok ? B.idx[s + u - ib] : 0;
+                            cv[u] = ok ? B.val[s + u - vb] : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < SP_UNROLL; ++u) {
+                            if (active && s + u < s1) {
+                                if (VEC == 2) xv[u] = ld2(X + (int64_t)jv[u] * ld + col);
+                                else xv[u] = make_double2(__ldg(X + (int64_t)jv[u] * ld + col), 0.0);
+                            } else {
+                                xv[u] = make_double2(0.0, 0.0);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < SP_UNROLL; ++u) {
+                            if (s + u < s1) {
+                                acc.x = fma(cv[u], xv[u].x, acc.x);
+                                acc.y = fma(cv[u], xv[u].y, acc.y);
+                            }
+                        }
+                    }
+                } else {
+                    // dense rows: slots straight from global, G at a time, broadcast by shuffles
+                    for (int64_t base = s0; base < s1; base += G) {
+                        const int64_t s = base + gl;
+                        int jj = 0;
+                        double cc = 0.0;
+                        if (s < s1) {
+                            jj = __ldg(a.indices + s);
+                            cc = __ldg(a.vals + s);
+                        }
+                        const int cnt = (int)min((int64_t)G, s1 - base);
+#pragma unroll 4
+                        for (int u = 0; u < cnt; ++u) {
+                            const int j = __shfl_sync(gmask, jj, (lane - gl) + u);
+                            const double c = __shfl_sync(gmask, cc, (lane - gl) + u);
+                            if (active) {
+                                if (VEC == 2) {
+                                    const double2 x = ld2(X + (int64_t)j * ld + col);
+                                    acc.x = fma(c, x.x, acc.x);
+                                    acc.y = fma(c, x.y, acc.y);
+                                } else {
+                                    acc.x = fma(c, __ldg(X + (int64_t)j * ld + col), acc.x);
+                                }
+                            }
+                        }
+                    }
+                }
+                if (!active) continue;
+                const int64_t off = row * (int64_t)ld + col;
+                double2 o = make_double2(a.alpha * acc.x, a.alpha * acc.y);
+                if (EPI == 0) {
+                    if (VEC == 2) st2(a.out + off, o);
+                    else a.out[off] = o.x;
+                } else {
+                    double2 ops[NOPS];
+#pragma unroll
+                    for (int j = 0; j < SP_NY; ++j) {
+                        if (j < E.ny) {
+                            const double2 y = VEC == 2 ? ld2cs(E.Y[j] + off) : make_double2(E.Y[j][off], 0.0);
+                            ops[j] = y;
+                            o = axpy2(E.ycoef[j], y, o);
+                        } else {
+                            ops[j] = make_double2(0.0, 0.0);
+                        }
+                    }
+                    if (VEC == 1) o.y = 0.0;
+                    ops[SP_NY] = o;
+#pragma unroll
+                    for (int j = 0; j < SP_NZ; ++j) {
+                        if (j < E.nz)
+                            ops[SP_NY + 1 + j] = VEC == 2 ? ld2cs(E.Z[j] + off) : make_double2(E.Z[j][off], 0.0);
+                        else
+                            ops[SP_NY + 1 + j] = make_double2(0.0, 0.0);
+                    }
+                    if (a.out != nullptr) {
+                        if (VEC == 2) st2(a.out + off, o);
+                        else a.out[off] = o.x;
+                    }
+#pragma unroll
+                    for (int d = 0; d < SP_ND; ++d)
+                        if (d < E.ndot) dacc[d] += dot2(select2(ops, E.da[d]), select2(ops, E.db[d]));
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (EPI == 1 && E.ndot > 0) reduce_and_finish<SP_ND>(dacc, E.ndot, ws, dots_out);
+}
+
+// Slot coefficients of a pattern with adjoint rows, assembled once per call
+// (linops.py:100 assemble) so the SpMM reads one value per slot.
+__global__ void __launch_bounds__(NT) assemble_kernel(PatDev P, int64_t nnz, double* vals) {
+    for (int64_t s = (int64_t)blockIdx.x * NT + threadIdx.x; s < nnz; s += (int64_t)gridDim.x * NT)
+        vals[s] = slot_coef(P, s);
+}
+
+template <int G, int VEC, int EPI>
+int sp_blocks_per_sm() {
+    static int cached = 0;
+    if (cached == 0) {
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, spmm_tiled_kernel<G, VEC, EPI>, NT, 0) != cudaSuccess ||
+            nb < 1)
+            nb = 1;
+        cached = nb;
+    }
+    return cached;
+}
+
+template <int G, int VEC, int EPI>
+void sp_launch(const SpDev& a0, const EpiDev& E, double* ws, double* dots, cudaStream_t st) {
+    SpDev a = a0;
+    a.ntiles = (a.nrows + a.tr - 1) / a.tr;
+    int grid = sp_blocks_per_sm<G, VEC, EPI>() * NSM;
+    if (grid > CL_RED_BLOCKS) grid = CL_RED_BLOCKS;
+    if ((int64_t)grid > a.ntiles) grid = (int)a.ntiles;
+    spmm_tiled_kernel<G, VEC, EPI><<<grid, NT, 0, st>>>(a, E, ws, dots);
+}
+
+template <int G, int VEC>
+void sp_dispatch_epi(const SpDev& a, const EpiDev& E, double* ws, double* dots, cudaStream_t st) {
+    const bool plain = E.ny == 0 && E.nz == 0 && E.ndot == 0 && a.out != nullptr;
+    if (plain) sp_launch<G, VEC, 0>(a, E, ws, dots, st);
+    else sp_launch<G, VEC, 1>(a, E, ws, dots, st);
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -592,13 +1013,67 @@ int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alp
         return CL_OK;
     }
     int G;
-    if (ld == 1) G = 1;
-    else if (ld <= 2) G = 1;
+    if (ld <= 2) G = 1;
     else if (ld <= 4) G = 2;
     else if (ld <= 8) G = 4;
     else if (ld <= 16) G = 8;
     else if (ld <= 32) G = 16;
     else G = 32;
+
+    // Tiled path: one value per slot -- the objective values (c_coeff folded
+    // into alpha) or the coefficients assembled into S->scratch.
+    const bool need_asm = P.at_ptr != nullptr && (P.w1 != nullptr || P.w2 != nullptr);
+    const bool tiled = (need_asm ? S->scratch != nullptr : P.cv != nullptr) && S->nnz >= 0 &&
+                       E.ny <= SP_NY && E.nz <= SP_NZ && E.ndot <= SP_ND &&
+                       aligned16(S->indptr) && aligned16(S->indices) &&
+                       (need_asm ? aligned16(S->scratch) : aligned16(P.cv));
+    if (tiled) {
+        // operand codes of the compact tiled epilogue: Y j -> j, out -> SP_NY, Z j -> SP_NY + 1 + j
+        for (int d = 0; d < E.ndot; ++d) {
+            uint8_t* c2[2] = {&E.da[d], &E.db[d]};
+            for (uint8_t* c : c2) {
+                if (*c == CL_OUT) *c = SP_NY;
+                else if (*c >= 16) *c = (uint8_t)(SP_NY + 1 + (*c - 16));
+            }
+        }
+        SpDev a;
+        a.nrows = P.nrows; a.indptr = P.indptr; a.indices = P.indices; a.X = X; a.ld = ld; a.out = out;
+        if (need_asm) {
+            if (S->nnz > 0) {
+                int64_t g = (S->nnz + NT - 1) / NT;
+                assemble_kernel<<<(int)(g > NSM * 16 ? NSM * 16 : g), NT, 0, st>>>(P, S->nnz, S->scratch);
+            }
+            a.vals = S->scratch;
+            a.alpha = alpha;
+        } else {
+            a.vals = P.cv;
+            a.alpha = alpha * P.c_coeff;
+        }
+        const int GG = (ld == 1) ? 1 : G;
+        const int NG = NT / GG;
+        const double avg = (double)S->nnz / (double)P.nrows;
+        int rpg = (int)((0.5 * SP_SMAX) / ((avg > 1.0 ? avg : 1.0) * NG));
+        const int rpg_max = (SP_PTRMAX - 4) / NG;
+        if (rpg > rpg_max) rpg = rpg_max;
+        if (rpg < 1) rpg = 1;
+        a.tr = rpg * NG;
+        a.ntiles = 0;
+        if (ld == 1) {
+            sp_dispatch_epi<1, 1>(a, E, ws, dots_out, st);
+        } else {
+            switch (G) {
+                case 1: sp_dispatch_epi<1, 2>(a, E, ws, dots_out, st); break;
+                case 2: sp_dispatch_epi<2, 2>(a, E, ws, dots_out, st); break;
+                case 4: sp_dispatch_epi<4, 2>(a, E, ws, dots_out, st); break;
+                case 8: sp_dispatch_epi<8, 2>(a, E, ws, dots_out, st); break;
+                case 16: sp_dispatch_epi<16, 2>(a, E, ws, dots_out, st); break;
+                default: sp_dispatch_epi<32, 2>(a, E, ws, dots_out, st); break;
+            }
+        }
+        return (int)cudaGetLastError();
+    }
+
+    // fused-coefficient path (no scratch given, or an all-zero matrix)
     const int64_t threads = P.nrows * G;
     const int grid = red_grid(threads);
     if (ld == 1) {
@@ -646,6 +1121,71 @@ int cl_constraint_eval(int64_t m, const int64_t* indptr, const int32_t* pi, cons
     return (int)cudaGetLastError();
 }
 
+int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const double* X1, const double* Y1,
+                            const double* X2, const double* Y2, double* out1, const double* X3, const double* Y3,
+                            double* out2, void* stream) {
+    if (n < 0 || ld < 1 || (ld > 1 && (ld & 1)) || aval == nullptr || X1 == nullptr || Y1 == nullptr ||
+        out1 == nullptr)
+        return CL_EARG;
+    if ((X2 == nullptr) != (Y2 == nullptr) || (X3 == nullptr) != (Y3 == nullptr)) return CL_EARG;
+    if (X3 != nullptr && out2 == nullptr) return CL_EARG;
+    if (n == 0) return CL_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    DiagCon d;
+    d.n = n; d.aval = aval; d.ld = ld; d.nop = 0;
+    d.nprod1 = X2 != nullptr ? 2 : 1;
+    d.out1 = out1; d.out2 = X3 != nullptr ? out2 : nullptr;
+    const double* want[6] = {X1, Y1, X2, Y2, X3, Y3};
+    for (int k = 0; k < 6; ++k) {
+        d.op[k] = nullptr;
+        d.pidx[k] = 0;
+    }
+    for (int k = 0; k < 6; ++k) {
+        if (want[k] == nullptr) continue;
+        int f = -1;
+        for (int q = 0; q < d.nop; ++q)
+            if (d.op[q] == want[k]) f = q;
+        if (f < 0) {
+            f = d.nop++;
+            d.op[f] = want[k];
+        }
+        d.pidx[k] = f;
+    }
+    if (ld >= 2 && ld / 2 <= NT * DC_U && aligned16(X1) && aligned16(Y1) && (X2 == nullptr || aligned16(X2)) &&
+        (Y2 == nullptr || aligned16(Y2)) && (X3 == nullptr || aligned16(X3)) && (Y3 == nullptr || aligned16(Y3))) {
+        const int rb = (NT * DC_U) / (ld / 2);
+        const int64_t nblk = (n + rb - 1) / rb;
+        const int grid = (int)(nblk > NSM * 8 ? NSM * 8 : nblk);
+        if (d.nop == 1) diag_constraint_flat_kernel<1><<<grid, NT, 0, st>>>(d);
+        else if (d.nop == 2) diag_constraint_flat_kernel<2><<<grid, NT, 0, st>>>(d);
+        else diag_constraint_flat_kernel<6><<<grid, NT, 0, st>>>(d);
+        return (int)cudaGetLastError();
+    }
+    const int G = ld <= 2 ? 1 : ld <= 4 ? 2 : ld <= 8 ? 4 : ld <= 16 ? 8 : ld <= 32 ? 16 : 32;
+    int64_t g = (n * G + 2 * NT - 1) / (2 * NT);
+    const int grid = (int)(g > NSM * 16 ? NSM * 16 : g);
+#define CL_DK(GG, VV)                                                                  \
+    do {                                                                               \
+        if (d.nop == 1) diag_constraint_kernel<GG, VV, 1><<<grid, NT, 0, st>>>(d);     \
+        else if (d.nop == 2) diag_constraint_kernel<GG, VV, 2><<<grid, NT, 0, st>>>(d); \
+        else diag_constraint_kernel<GG, VV, 6><<<grid, NT, 0, st>>>(d);                \
+    } while (0)
+    if (ld == 1) {
+        CL_DK(1, 1);
+    } else {
+        switch (G) {
+            case 1: CL_DK(1, 2); break;
+            case 2: CL_DK(2, 2); break;
+            case 4: CL_DK(4, 2); break;
+            case 8: CL_DK(8, 2); break;
+            case 16: CL_DK(16, 2); break;
+            default: CL_DK(32, 2); break;
+        }
+    }
+#undef CL_DK
+    return (int)cudaGetLastError();
+}
+
 int cl_sddmm(int64_t K, const int32_t* imap, const int32_t* jmap, int32_t ld, const double* X, const double* Y,
              double* x, void* stream) {
     if (K < 0 || ld < 1 || (ld > 1 && (ld & 1))) return CL_EARG;
@@ -678,7 +1218,11 @@ int cl_diag_alm_update(const cl_diag_update_args* a, double* dots_out, double* w
     for (int j = 0; j < CL_MAXIN; ++j) d.H[j] = j < a->nh ? a->H[j] : nullptr;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int64_t n2 = a->n * (a->ld / 2);
-    diag_update_kernel<<<red_grid(n2), NT, 0, st>>>(d, ws, dots_out);
+    const int grid = red_grid(n2);
+    if (a->nh == 0) diag_update_kernel<0><<<grid, NT, 0, st>>>(d, ws, dots_out);
+    else if (a->nh <= 4) diag_update_kernel<4><<<grid, NT, 0, st>>>(d, ws, dots_out);
+    else if (a->nh <= 10) diag_update_kernel<10><<<grid, NT, 0, st>>>(d, ws, dots_out);
+    else diag_update_kernel<CL_MAXIN><<<grid, NT, 0, st>>>(d, ws, dots_out);
     return (int)cudaGetLastError();
 }
 

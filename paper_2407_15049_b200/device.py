@@ -132,6 +132,13 @@ class Device:
         check(rc, "cl_pattern_spmm")
 
     def constraint_eval(self, con, ld, X1, Y1, out1, X2=None, Y2=None, X3=None, Y3=None, out2=None):
+        if con.diag_aval is not None:
+            rc = self.lib.cl_diag_constraint_eval(int(con.m), ptr(con.diag_aval), int(ld), ptr(X1), ptr(Y1),
+                                                  ptr(X2), ptr(Y2), ptr(out1), ptr(X3), ptr(Y3), ptr(out2),
+                                                  self.sp)
+            self.launches += 1
+            check(rc, "cl_diag_constraint_eval")
+            return
         rc = self.lib.cl_constraint_eval(int(con.m), ptr(con.indptr), ptr(con.pi), ptr(con.pj),
                                          ptr(con.val), int(ld), ptr(X1), ptr(Y1), ptr(X2), ptr(Y2),
                                          ptr(out1), ptr(X3), ptr(Y3), ptr(out2), self.sp)

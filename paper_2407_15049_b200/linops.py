@@ -46,6 +46,8 @@ class DevicePattern:
     at_con: torch.Tensor | None   # int32
     at_val: torch.Tensor | None   # fp64
 
+    scratch: torch.Tensor | None = None   # assembled slot coefficients (lazy)
+
     @property
     def nnz(self):
         return int(self.indices.numel())
@@ -53,6 +55,7 @@ class DevicePattern:
     def struct(self, c_coeff=None, w1=None, w2=None, use_cv=True, use_at=True):
         P = _lib.Pattern()
         P.nrows = self.nrows
+        P.nnz = self.nnz
         P.indptr = self.indptr.data_ptr()
         P.indices = self.indices.data_ptr()
         if use_cv and self.cv is not None and c_coeff is not None:
@@ -67,8 +70,12 @@ class DevicePattern:
             P.at_val = self.at_val.data_ptr()
             P.w1 = w1.data_ptr() if w1 is not None else None
             P.w2 = w2.data_ptr() if w2 is not None else None
+            if self.scratch is None:
+                self.scratch = padded(torch.empty(self.nnz, dtype=F64, device=self.indices.device))
+            P.scratch = self.scratch.data_ptr()
         else:
             P.at_ptr = P.at_con = P.at_val = P.w1 = P.w2 = None
+            P.scratch = None
         return P
 
     def bytes(self):
@@ -89,6 +96,18 @@ class ConstraintCSR:
     pi: torch.Tensor       # int32 row of the position
     pj: torch.Tensor       # int32 col of the position
     val: torch.Tensor      # fp64
+    diag_aval: torch.Tensor | None = None   # set when constraint c is a_c e_c e_c^T (row-local)
+
+
+PAD = 16   # elements readable past the logical end (bulk copies read 16-byte supersets)
+
+
+def padded(t):
+    """Copy of ``t`` in an allocation PAD elements longer (zero tail); returns the logical view."""
+    t = t.contiguous()
+    buf = torch.zeros(t.numel() + PAD, dtype=t.dtype, device=t.device)
+    buf[:t.numel()] = t
+    return buf[:t.numel()]
 
 
 # ---------------------------------------------------------------------------
@@ -343,10 +362,10 @@ def operator_stats(cop, adj):
 # ---------------------------------------------------------------------------
 
 def _csr_ptr(rows, nrows):
-    ptr = torch.zeros(nrows + 1, dtype=I64, device=rows.device)
+    ptr = torch.zeros(nrows + 1 + PAD, dtype=I64, device=rows.device)
     if rows.numel():
-        ptr[1:] = torch.cumsum(torch.bincount(rows, minlength=nrows), 0)
-    return ptr
+        ptr[1:nrows + 1] = torch.cumsum(torch.bincount(rows, minlength=nrows), 0)
+    return ptr[:nrows + 1]
 
 
 def _mirror(n, tag, r, c, v):
@@ -372,9 +391,9 @@ def build_operators(p: SdpProblem, dense_c=None, dev=None) -> OperatorBundle:
     # constraint CSR, rows sorted by compressed column (scipy canonical order)
     order = torch.argsort(cons * max(K, 1) + colidx)
     ccol = colidx[order]
-    con = ConstraintCSR(m=m, indptr=_csr_ptr(cons, m), colidx=ccol.to(I32),
+    con = ConstraintCSR(m=m, indptr=_csr_ptr(cons, m), colidx=padded(ccol.to(I32)),
                         pi=imap[ccol].to(I32).contiguous(), pj=jmap[ccol].to(I32).contiguous(),
-                        val=vals[order].contiguous())
+                        val=padded(vals[order]))
 
     c_r, c_c, c_v = T(p.C.rows, I64), T(p.C.cols, I64), T(p.C.vals, F64)
     ccodes, _, cvals = _mirror(n, torch.zeros_like(c_r), c_r, c_c, c_v)
@@ -382,7 +401,7 @@ def build_operators(p: SdpProblem, dense_c=None, dev=None) -> OperatorBundle:
     S = int(sup.numel())
     slot_a = torch.searchsorted(sup, uniq)
     slot_c = torch.searchsorted(sup, ccodes)
-    cv = torch.zeros(S, dtype=F64, device=dev.dev)
+    cv = padded(torch.zeros(S, dtype=F64, device=dev.dev))
     cv[slot_c] = cvals
     sup_i, sup_j = sup // n, sup % n
 
@@ -390,18 +409,18 @@ def build_operators(p: SdpProblem, dense_c=None, dev=None) -> OperatorBundle:
     s_of = slot_a[colidx]
     o2 = torch.argsort(s_of * max(m, 1) + cons)
     at_ptr = _csr_ptr(s_of, S)
-    omega = DevicePattern(n, _csr_ptr(sup_i, n), sup_j.to(I32), cv, at_ptr,
-                          cons[o2].to(I32), vals[o2].contiguous())
+    omega = DevicePattern(n, _csr_ptr(sup_i, n), padded(sup_j.to(I32)), cv, at_ptr,
+                          padded(cons[o2].to(I32)), padded(vals[o2]))
 
     # Omega_A: the K constraint positions only (same entry order, by column)
     o3 = torch.argsort(colidx * max(m, 1) + cons)
-    apat = DevicePattern(n, _csr_ptr(imap, n), jmap.to(I32), None, _csr_ptr(colidx, K),
-                         cons[o3].to(I32), vals[o3].contiguous())
+    apat = DevicePattern(n, _csr_ptr(imap, n), padded(jmap.to(I32)), None, _csr_ptr(colidx, K),
+                         padded(cons[o3].to(I32)), padded(vals[o3]))
 
     # objective's own CSR
     o4 = torch.argsort(ccodes)
     cs = ccodes[o4]
-    cpat = DevicePattern(n, _csr_ptr(cs // n, n), (cs % n).to(I32), cvals[o4].contiguous(),
+    cpat = DevicePattern(n, _csr_ptr(cs // n, n), padded((cs % n).to(I32)), padded(cvals[o4]),
                          None, None, None)
 
     cop = CompressedOperator(m, n, K, imap.to(I32), jmap.to(I32), slot_a, con, dev)
@@ -411,6 +430,7 @@ def build_operators(p: SdpProblem, dense_c=None, dev=None) -> OperatorBundle:
     if (m == n and p.a_val.size == m and np.array_equal(p.a_con, np.arange(m))
             and np.array_equal(p.a_row, p.a_con) and np.array_equal(p.a_col, p.a_con)):
         diag = a_val.contiguous()
+        con.diag_aval = diag
 
     if dense_c is None:
         dense_c = p.dense_c

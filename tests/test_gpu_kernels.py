@@ -1,0 +1,197 @@
+"""Edge cases of the sm_100a kernels against plain numpy/scipy references.
+
+Targets the paths the golden instances do not reach: tiles whose staged
+segment overflows shared memory (dense rows), empty rows, row counts that are
+not a multiple of the tile, every lane-group width (ld 1 .. 130, including
+ranks above 64 where a row is processed in column chunks), the assembled-
+coefficient SpMM, the diagonal-constraint fast path and every history-width
+bucket of the fused ALM update.
+"""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_2407_15049_b200 import _lib
+    from paper_2407_15049_b200.device import default_device
+    _lib.load(require_device=True)
+    return default_device()
+
+
+def _pattern(M, at=None):
+    """DevicePattern of a scipy CSR (values as cv); optional adjoint rows (at_ptr, at_con, at_val)."""
+    import torch
+    from paper_2407_15049_b200.linops import DevicePattern, padded
+    M = sp.csr_matrix(M)
+    M.sort_indices()
+    c = lambda a, dt: padded(torch.as_tensor(np.ascontiguousarray(a)).to("cuda", dt))  # noqa: E731
+    ptr = c(M.indptr.astype(np.int64), torch.int64)
+    idx = c(M.indices.astype(np.int32), torch.int32)
+    cv = c(M.data.astype(np.float64), torch.float64)
+    if at is None:
+        return DevicePattern(M.shape[0], ptr, idx, cv, None, None, None)
+    ap, ac, av = at
+    return DevicePattern(M.shape[0], ptr, idx, cv, c(ap, torch.int64), c(ac, torch.int32),
+                         c(av, torch.float64))
+
+
+def _rand_csr(rng, n, ncols, deg_fn):
+    rows, cols = [], []
+    for i in range(n):
+        d = deg_fn(i)
+        cs = np.unique(rng.integers(0, ncols, size=d)) if d else np.zeros(0, dtype=np.int64)
+        rows += [i] * len(cs)
+        cols += list(cs)
+    vals = rng.standard_normal(len(rows))
+    return sp.csr_matrix((vals, (rows, cols)), shape=(n, ncols))
+
+
+def _factor(rng, n, ld):
+    import torch
+    X = rng.standard_normal((n, ld))
+    return X, torch.as_tensor(X).cuda().contiguous()
+
+
+@pytest.mark.parametrize("ld", [1, 2, 4, 6, 16, 26, 30, 66, 130])
+@pytest.mark.parametrize("shape", ["sparse", "dense_rows", "empty_rows"])
+def test_tiled_spmm_matches_scipy(dev, ld, shape):
+    import torch
+    rng = np.random.default_rng(ld * 7 + len(shape))
+    n = 3001
+    if shape == "sparse":
+        M = _rand_csr(rng, n, n, lambda i: int(rng.integers(0, 12)))
+    elif shape == "dense_rows":       # rows far longer than one staged tile (> 1024 slots)
+        M = _rand_csr(rng, n, n, lambda i: 1500 if i % 97 == 0 else int(rng.integers(1, 8)))
+    else:
+        M = _rand_csr(rng, n, n, lambda i: 0 if i % 3 else int(rng.integers(1, 30)))
+    P = _pattern(M)
+    X, Xd = _factor(rng, n, ld)
+    out = torch.empty_like(Xd)
+    dev.spmm(P, Xd, ld, alpha=0.75, out=out, c_coeff=-1.5)
+    ref = 0.75 * (-1.5) * (M @ X)
+    err = np.abs(out.cpu().numpy() - ref).max() / (1 + np.abs(ref).max())
+    assert err <= 1e-13, err
+
+
+@pytest.mark.parametrize("ld", [1, 6, 26, 66])
+def test_tiled_spmm_epilogue_and_dots(dev, ld):
+    import torch
+    rng = np.random.default_rng(5 + ld)
+    n = 2000
+    M = _rand_csr(rng, n, n, lambda i: int(rng.integers(1, 9)))
+    P = _pattern(M)
+    X, Xd = _factor(rng, n, ld)
+    Y, Yd = _factor(rng, n, ld)
+    Z, Zd = _factor(rng, n, ld)
+    out = torch.empty_like(Xd)
+    dev.spmm(P, Xd, ld, alpha=2.0, out=out, Y=[Yd], ycoef=[-0.5], Z=[Zd],
+             dots=[("out", "out"), ("out", ("z", 0)), (("y", 0), ("z", 0))], at=10, c_coeff=1.0)
+    s = dev.fetch(13)[10:13]
+    o = 2.0 * (M @ X) - 0.5 * Y
+    assert np.abs(out.cpu().numpy() - o).max() <= 1e-12 * (1 + np.abs(o).max())
+    for got, want in zip(s, [np.sum(o * o), np.sum(o * Z), np.sum(Y * Z)]):
+        assert abs(got - want) <= 1e-11 * (1 + abs(want))
+
+
+def test_assembled_coefficient_spmm(dev):
+    """S = c*C + A*(w1) + A*(w2) assembled into scratch, then the tiled product."""
+    import torch
+    rng = np.random.default_rng(9)
+    n, m = 1500, 400
+    M = _rand_csr(rng, n, n, lambda i: int(rng.integers(1, 10)))
+    nnz = M.nnz
+    # each slot gets 0..3 adjoint entries
+    cnt = rng.integers(0, 4, size=nnz)
+    at_ptr = np.zeros(nnz + 1, dtype=np.int64)
+    at_ptr[1:] = np.cumsum(cnt)
+    at_con = rng.integers(0, m, size=at_ptr[-1]).astype(np.int32)
+    at_val = rng.standard_normal(at_ptr[-1])
+    P = _pattern(M, (at_ptr, at_con, at_val))
+    w1, w2 = rng.standard_normal(m), rng.standard_normal(m)
+    coef = np.array([np.dot(at_val[at_ptr[s]:at_ptr[s + 1]], w1[at_con[at_ptr[s]:at_ptr[s + 1]]])
+                     + np.dot(at_val[at_ptr[s]:at_ptr[s + 1]], w2[at_con[at_ptr[s]:at_ptr[s + 1]]])
+                     for s in range(nnz)]) + 0.3 * sp.csr_matrix(M).data
+    S = sp.csr_matrix((coef, M.indices, M.indptr), shape=M.shape)
+    X, Xd = _factor(rng, n, 26)
+    out = torch.empty_like(Xd)
+    dev.spmm(P, Xd, 26, out=out, c_coeff=0.3, w1=torch.as_tensor(w1).cuda(), w2=torch.as_tensor(w2).cuda())
+    ref = S @ X
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * (1 + np.abs(ref).max())
+
+
+@pytest.mark.parametrize("ld", [2, 26, 66, 130, 4098])
+def test_diag_constraint_fast_path_equals_generic(dev, ld):
+    """cl_diag_constraint_eval and cl_constraint_eval agree on diagonal constraints (summation order differs)."""
+    import torch
+    from paper_2407_15049_b200 import graphs, linops, problem
+    p = problem.build_maxcut(graphs.random_sparse(5000, deg=6.0, seed=ld))
+    ops = linops.build_operators(p)
+    con = ops.cop.con
+    assert con.diag_aval is not None
+    rng = np.random.default_rng(ld)
+    X = [torch.as_tensor(rng.standard_normal((p.n, ld))).cuda() for _ in range(6)]
+    o_fast = [torch.empty(p.m, dtype=torch.float64, device="cuda") for _ in range(2)]
+    o_gen = [torch.empty(p.m, dtype=torch.float64, device="cuda") for _ in range(2)]
+    dev.constraint_eval(con, ld, X[0], X[1], o_fast[0], X2=X[2], Y2=X[3], X3=X[4], Y3=X[5], out2=o_fast[1])
+    saved, con.diag_aval = con.diag_aval, None
+    try:
+        dev.constraint_eval(con, ld, X[0], X[1], o_gen[0], X2=X[2], Y2=X[3], X3=X[4], Y3=X[5], out2=o_gen[1])
+    finally:
+        con.diag_aval = saved
+    for a, b in zip(o_fast, o_gen):
+        a, b = a.cpu().numpy(), b.cpu().numpy()
+        assert np.abs(a - b).max() <= 1e-14 * (1 + np.abs(b).max())
+    Xh = [x.cpu().numpy() for x in X]
+    want = np.einsum("ij,ij->i", Xh[0], Xh[1]) + np.einsum("ij,ij->i", Xh[2], Xh[3])
+    assert np.abs(o_fast[0].cpu().numpy() - want).max() <= 1e-12 * (1 + np.abs(want).max())
+
+
+@pytest.mark.parametrize("nh", [0, 3, 9, 17])
+@pytest.mark.parametrize("refresh", [True, False])
+def test_diag_alm_update_buckets(dev, nh, refresh):
+    import torch
+    from paper_2407_15049_b200 import _lib
+    rng = np.random.default_rng(nh + 100 * refresh)
+    n, ld = 3000, 26
+    T = lambda *s: torch.as_tensor(rng.standard_normal(s)).cuda().contiguous()  # noqa: E731
+    R, D, CR, CD, gold = T(n, ld), T(n, ld), T(n, ld), T(n, ld), T(n, ld)
+    ax, q1, q2, lam, b, aval = T(n), T(n), T(n), T(n), T(n), T(n)
+    H = [T(n, ld) for _ in range(nh)]
+    gnew, y = torch.empty_like(R), torch.empty_like(R)
+    axo = torch.empty_like(ax)
+    tau, rho, scale = 0.37, 2.5, 0.8
+    Rh, Dh, CRh, CDh, goh = [t.cpu().numpy() for t in (R, D, CR, CD, gold)]
+    axh, q1h, q2h, lamh, bh, ah = [t.cpu().numpy() for t in (ax, q1, q2, lam, b, aval)]
+    Hh = [h.cpu().numpy() for h in H]
+    a = _lib.DiagUpdateArgs()
+    a.n, a.ld, a.aval = n, ld, aval.data_ptr()
+    a.tau, a.rho, a.scale = tau, rho, scale
+    a.R, a.D, a.CR, a.CD = R.data_ptr(), D.data_ptr(), CR.data_ptr(), CD.data_ptr()
+    a.ax, a.ax_out, a.q1, a.q2 = ax.data_ptr(), axo.data_ptr(), q1.data_ptr(), q2.data_ptr()
+    a.lam, a.b, a.g_old, a.g_new, a.y = lam.data_ptr(), b.data_ptr(), gold.data_ptr(), gnew.data_ptr(), y.data_ptr()
+    a.nh = nh
+    for j, h in enumerate(H):
+        a.H[j] = h.data_ptr()
+    a.refresh = 1 if refresh else 0
+    dev.diag_update(a, at=0)
+    s = dev.fetch(7 + 2 * _lib.CL_MAXIN)
+    if not refresh:
+        Rh = Rh + tau * Dh
+        CRh = CRh + tau * CDh
+        axh = axh + tau * q1h + tau * tau * q2h
+    res = axh - bh
+    w = lamh + rho * res
+    g = 2.0 * ((w * ah)[:, None] * Rh + scale * CRh)
+    yy = g - goh
+    close = lambda u, v: abs(u - v) <= 1e-10 * (1 + abs(v))  # noqa: E731
+    assert np.abs(gnew.cpu().numpy() - g).max() <= 1e-12 * (1 + np.abs(g).max())
+    assert close(s[0], np.sum(CRh * Rh)) and close(s[1], np.sum(g * g)) and close(s[2], np.sum(yy * Dh))
+    assert close(s[3], np.dot(lamh, res)) and close(s[4], np.dot(res, res))
+    for h in range(nh):
+        assert close(s[7 + h], np.sum(g * Hh[h]))
+        assert close(s[7 + _lib.CL_MAXIN + h], np.sum(yy * Hh[h]))

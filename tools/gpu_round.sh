@@ -6,6 +6,6 @@ TAG=${1:-r1}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -3 gpurun_out/bench_$TAG.err
 cat gpurun_out/bench_$TAG.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'constraint|pattern|diag|lincomb|sddmm' -c 60 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'pattern_spmm|constraint_kernel|diag_update' -s 3 -c 3 -o gpurun_out/prof_$TAG -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_$TAG.log 2>&1; tail -3 gpurun_out/ncu_$TAG.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'spmm|constraint|diag|lincomb|sddmm|assemble|basis' -c 60 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'spmm|constraint|diag_update' -s 3 -c 3 -o gpurun_out/prof_$TAG -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_$TAG.log 2>&1; tail -3 gpurun_out/ncu_$TAG.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
