@@ -331,6 +331,14 @@ def run_ours(args, rank, world, local_rank):
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     top = "pattern_spmm"
     achieved = kbytes[top] / (kms[top] * 1e-3) / 1e9
+    traffic, traffic_src = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        if n == int(1e7) and abs(args.deg - 6.0) < 1e-9 and ld == 26:
+            traffic, traffic_src = int(tj[top]), tj["source"]
+    except Exception:
+        pass
     kern = {nm: {"ms": kms[nm], "bytes": kbytes[nm],
                  "GB/s": kbytes[nm] / (kms[nm] * 1e-3) / 1e9,
                  "share": kms[nm] / sum(kms.values())} for nm in names}
@@ -352,7 +360,8 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": f"rows x{world}" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None},
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes": kbytes[top]},
         "kernels": kern,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -135,7 +135,7 @@ int cl_constraint_eval(int64_t m, const int64_t* indptr, const int32_t* pi, cons
                        void* stream);
 
 /* Diagonal-constraint form of cl_constraint_eval (constraint c is the single
- * entry a_c e_c e_c^T, m == n; MaxCut, problem.py:435 build_maxcut): the same
+ * entry a_c e_c e_c^T, m == n; MaxCut, problem.py:387 build_maxcut): the same
  * outputs from row dot products, out1[c] = a_c (X1[c].Y1[c] + X2[c].Y2[c]),
  * out2[c] = a_c X3[c].Y3[c], with no index traffic. */
 int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const double* X1, const double* Y1,
@@ -147,7 +147,7 @@ int cl_sddmm(int64_t K, const int32_t* imap, const int32_t* jmap, int32_t ld,
              const double* X, const double* Y, double* x, void* stream);
 
 /* Diagonal-constraint fast path for problems whose constraint c is the single
- * diagonal entry a_c * e_c e_c^T (m == n; MaxCut, problem.py:435): the ALM
+ * diagonal entry a_c * e_c e_c^T (m == n; MaxCut, problem.py:387): the ALM
  * step update and gradient (alm.py:306-318) become row-local and fuse into one pass.
  *   R  += tau*D;  CR += tau*CD;  ax_out[c] = ax[c] + tau*q1[c] + tau^2*q2[c]
  *   w[c] = lam[c] + rho*(ax[c]-b[c]);  g_new = 2*(w[row]*a*R + scale*CR)
