@@ -218,16 +218,30 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     n = int(args.n)
-    g = graphs.random_sparse(n, deg=args.deg, seed=args.seed + rank)
-    p = problem.build_maxcut(g)
     dev = device.default_device()
-    ops = linops.build_operators(p, dev=dev)
-    r = driver.initial_rank(p.m, p.n)
+    halo_bytes = 0
+    if world == 1:
+        g = graphs.random_sparse(n, deg=args.deg, seed=args.seed)
+        n_edges = int(g.edges_u.size)
+        p = problem.build_maxcut(g)
+        ops = linops.build_operators(p, dev=dev)
+        r = driver.initial_rank(p.m, p.n)
+    else:
+        # weak scaling: every rank owns n rows of one random graph on world*n vertices;
+        # remote factor rows arrive by the halo all-gather inside the SpMM (shard.py)
+        from paper_2407_15049_b200 import shard
+        dev.group, dev.world = None, world
+        ops = shard.sharded_maxcut_ops(world * n, args.deg, args.seed, rank, world, dev)
+        p = ops.problem
+        n_edges = ops.n_edges
+        r = driver.initial_rank(world * n, world * n)
     ld = device.padded_ld(r)
-    rng = np.random.default_rng(args.seed)
-    R_host = rng.standard_normal((n, r)) / math.sqrt(n * r)
+    rng = np.random.default_rng(args.seed + rank)
+    R_host = rng.standard_normal((n, r)) / math.sqrt(world * n * r)
     lam_host = 0.1 * rng.standard_normal(p.m)
-    rho = max(1.0, p.m / math.sqrt(max(p.nnz_a_full(), 1)))
+    rho = max(1.0, world * n / math.sqrt(world * n))
+    if world > 1:
+        halo_bytes = ops.plan.halo_bytes(ld)
     R = linops.to_factor(R_host, dev, ld)
     lam = linops.to_vec(lam_host, dev)
     core = alm.AlmCore(ops, n, ld)
@@ -248,6 +262,10 @@ def run_ours(args, rank, world, local_rank):
         if ev is not None:
             ev[2].record(st)
         core.grad_value(R, lam, rho, 1.0, zero, g_new, ybuf, [], refresh=True, fetch=False)
+        if world > 1:
+            # the Lagrangian value / gradient-norm scalars combine across ranks
+            red = dev.slab[alm.AlmCore.S_UPD:alm.AlmCore.S_UPD + 7].clone()
+            dist.all_reduce(red)
         if ev is not None:
             ev[3].record(st)
 
@@ -285,7 +303,7 @@ def run_ours(args, rank, world, local_rank):
 
     # end to end through the reference-facing API with host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and world == 1:
         R_pin = torch.from_numpy(R_host).pin_memory()
         lam_pin = torch.from_numpy(lam_host).pin_memory()
         out_pin = torch.empty((n, r), dtype=torch.float64).pin_memory()
@@ -353,7 +371,8 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded random graph, random factor/multiplier)",
-        "config": {"workload": workload_name(n, args.deg), "n": n, "edges": int(g.edges_u.size),
+        "config": {"workload": workload_name(world * n, args.deg), "n": world * n, "n_per_gpu": n,
+                   "edges": n_edges, "halo_bytes_per_spmm_per_rank": halo_bytes,
                    "rank": r, "ld": ld, "step": "BM gradient pass: SDDMM A(RR^T) + SpMM C R + fused 2 S R",
                    "bytes_per_step": step_bytes,
                    "l2": f"inputs larger than L2 (factor {n * ld * 8 / 1e9:.2f} GB >> 126 MB)",

@@ -90,6 +90,8 @@ typedef struct {
     const double* w2;
     int64_t nnz;            /* slots (indptr[nrows]); the host knows it, the launch needs it */
     double* scratch;        /* nnz+16 doubles for assembled coefficients, or NULL */
+    const double* ghost;    /* row-sharded solve: rows >= nown of X live here (halo), or NULL */
+    int64_t nown;           /* rows of X owned by this rank (column j >= nown reads ghost[j-nown]) */
 } cl_pattern;
 
 /* Pattern times factor with a fused epilogue (linops.py:122 spmm, and the
@@ -141,6 +143,10 @@ int cl_constraint_eval(int64_t m, const int64_t* indptr, const int32_t* pi, cons
 int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const double* X1, const double* Y1,
                             const double* X2, const double* Y2, double* out1, const double* X3, const double* Y3,
                             double* out2, void* stream);
+
+/* Halo packing of the row-sharded solve (rows published to the other ranks
+ * before an all-gather): out[i,:] = X[idx[i],:] for i < count, ld even. */
+int cl_gather_rows(const int32_t* idx, int64_t count, int32_t ld, const double* X, double* out, void* stream);
 
 /* Gathered outer product at K positions (linops.py:49), x[k] = X[imap[k]]·Y[jmap[k]]. */
 int cl_sddmm(int64_t K, const int32_t* imap, const int32_t* jmap, int32_t ld,

@@ -25,6 +25,7 @@ CL_DOT_PAIRS, CL_DOT_OUT_ALL, CL_DOT_FIRST_TWO = 0, 1, 2
 CL_EARG = 1001
 
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_diag_constraint_eval", "cl_sddmm",
+           "cl_gather_rows",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
            "cl_version", "cl_device_ok")
 
@@ -43,7 +44,7 @@ class LincombArgs(ctypes.Structure):
 class Pattern(ctypes.Structure):
     _fields_ = [("nrows", I64), ("indptr", P), ("indices", P), ("cv", P), ("c_coeff", D),
                 ("at_ptr", P), ("at_con", P), ("at_val", P), ("w1", P), ("w2", P),
-                ("nnz", I64), ("scratch", P)]
+                ("nnz", I64), ("scratch", P), ("ghost", P), ("nown", I64)]
 
 
 class Epilogue(ctypes.Structure):
@@ -74,6 +75,7 @@ def _declare(lib):
                                     P, P, P, P]
     lib.cl_constraint_eval.argtypes = [I64, P, P, P, P, I32, P, P, P, P, P, P, P, P, P]
     lib.cl_diag_constraint_eval.argtypes = [I64, P, I32, P, P, P, P, P, P, P, P, P]
+    lib.cl_gather_rows.argtypes = [P, I64, I32, P, P, P]
     lib.cl_sddmm.argtypes = [I64, P, P, I32, P, P, P, P]
     lib.cl_diag_alm_update.argtypes = [ctypes.POINTER(DiagUpdateArgs), P, P, P]
     lib.cl_basis_project.argtypes = [P, I64, I32, I64, P, P, P, P]

@@ -685,6 +685,8 @@ struct SpDev {
     const int32_t* indices;
     const double* vals;
     const double* X;
+    const double* Xg;     // ghost rows (row-sharded solve): column j >= nown reads Xg[j - nown]
+    int32_t nown;         // INT32_MAX when there is no ghost block
     int ld;
     double alpha;
     double* out;
@@ -722,8 +724,9 @@ __device__ __forceinline__ void sp_issue(const SpDev& a, SpTile* T, int64_t (*me
     if (vbytes) bulk_g2s(T[buf].val, a.vals + vb, vbytes, &bar[buf]);
 }
 
-template <int G, int VEC, int EPI>
-__global__ void __launch_bounds__(NT, EPI == 0 ? 5 : 3) spmm_tiled_kernel(SpDev a, EpiDev E, double* ws, double* dots_out) {
+template <int G, int VEC, int EPI, int GHOST>
+__global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : 5) : 3) spmm_tiled_kernel(SpDev a, EpiDev E, double* ws,
+                                                                                     double* dots_out) {
     constexpr int NG = NT / G;
     // epilogue operand set of the tiled path: Y0, Y1, out, Z0, Z1, Z2
     constexpr int NOPS = SP_NY + 1 + SP_NZ;
@@ -807,8 +810,10 @@ __global__ void __launch_bounds__(NT, EPI == 0 ? 5 : 3) spmm_tiled_kernel(SpDev 
 #pragma unroll
                         for (int u = 0; u < SP_UNROLL; ++u) {
                             if (active && s + u < s1) {
-                                if (VEC == 2) xv[u] = ld2(X + (int64_t)jv[u] * ld + col);
-                                else xv[u] = make_double2(__ldg(X + (int64_t)jv[u] * ld + col), 0.0);
+                                const double* src = (!GHOST || jv[u] < a.nown) ? X + (int64_t)jv[u] * ld
+                                                                               : a.Xg + (int64_t)(jv[u] - a.nown) * ld;
+                                if (VEC == 2) xv[u] = ld2(src + col);
+                                else xv[u] = make_double2(__ldg(src + col), 0.0);
                             } else {
                                 xv[u] = make_double2(0.0, 0.0);
                             }
@@ -838,11 +843,15 @@ __global__ void __launch_bounds__(NT, EPI == 0 ? 5 : 3) spmm_tiled_kernel(SpDev 
                             const double c = __shfl_sync(gmask, cc, (lane - gl) + u);
                             if (active) {
                                 if (VEC == 2) {
-                                    const double2 x = ld2(X + (int64_t)j * ld + col);
+                                    const double* src = (!GHOST || j < a.nown) ? X + (int64_t)j * ld
+                                                                               : a.Xg + (int64_t)(j - a.nown) * ld;
+                                    const double2 x = ld2(src + col);
                                     acc.x = fma(c, x.x, acc.x);
                                     acc.y = fma(c, x.y, acc.y);
                                 } else {
-                                    acc.x = fma(c, __ldg(X + (int64_t)j * ld + col), acc.x);
+                                    const double* src = (!GHOST || j < a.nown) ? X + (int64_t)j * ld
+                                                                               : a.Xg + (int64_t)(j - a.nown) * ld;
+                                    acc.x = fma(c, __ldg(src + col), acc.x);
                                 }
                             }
                         }
@@ -897,12 +906,13 @@ __global__ void __launch_bounds__(NT) assemble_kernel(PatDev P, int64_t nnz, dou
         vals[s] = slot_coef(P, s);
 }
 
-template <int G, int VEC, int EPI>
+template <int G, int VEC, int EPI, int GHOST>
 int sp_blocks_per_sm() {
     static int cached = 0;
     if (cached == 0) {
         int nb = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, spmm_tiled_kernel<G, VEC, EPI>, NT, 0) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, spmm_tiled_kernel<G, VEC, EPI, GHOST>, NT, 0) !=
+                cudaSuccess ||
             nb < 1)
             nb = 1;
         cached = nb;
@@ -910,21 +920,38 @@ int sp_blocks_per_sm() {
     return cached;
 }
 
-template <int G, int VEC, int EPI>
+template <int G, int VEC, int EPI, int GHOST>
 void sp_launch(const SpDev& a0, const EpiDev& E, double* ws, double* dots, cudaStream_t st) {
     SpDev a = a0;
     a.ntiles = (a.nrows + a.tr - 1) / a.tr;
-    int grid = sp_blocks_per_sm<G, VEC, EPI>() * NSM;
+    int grid = sp_blocks_per_sm<G, VEC, EPI, GHOST>() * NSM;
     if (grid > CL_RED_BLOCKS) grid = CL_RED_BLOCKS;
     if ((int64_t)grid > a.ntiles) grid = (int)a.ntiles;
-    spmm_tiled_kernel<G, VEC, EPI><<<grid, NT, 0, st>>>(a, E, ws, dots);
+    spmm_tiled_kernel<G, VEC, EPI, GHOST><<<grid, NT, 0, st>>>(a, E, ws, dots);
 }
 
 template <int G, int VEC>
 void sp_dispatch_epi(const SpDev& a, const EpiDev& E, double* ws, double* dots, cudaStream_t st) {
     const bool plain = E.ny == 0 && E.nz == 0 && E.ndot == 0 && a.out != nullptr;
-    if (plain) sp_launch<G, VEC, 0>(a, E, ws, dots, st);
-    else sp_launch<G, VEC, 1>(a, E, ws, dots, st);
+    const bool ghost = a.Xg != nullptr;
+    if (plain) {
+        if (ghost) sp_launch<G, VEC, 0, 1>(a, E, ws, dots, st);
+        else sp_launch<G, VEC, 0, 0>(a, E, ws, dots, st);
+    } else {
+        if (ghost) sp_launch<G, VEC, 1, 1>(a, E, ws, dots, st);
+        else sp_launch<G, VEC, 1, 0>(a, E, ws, dots, st);
+    }
+}
+
+// Halo packing for the row-sharded solve: out[i, :] = X[idx[i], :].
+__global__ void __launch_bounds__(NT) gather_rows_kernel(const int32_t* __restrict__ idx, int64_t count, int h2,
+                                                         const double* __restrict__ X, double* __restrict__ out) {
+    const int64_t total = count * h2;
+    for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < total; k += (int64_t)gridDim.x * NT) {
+        const int64_t i = k / h2;
+        const int q = (int)(k - i * h2);
+        st2(out + 2 * k, ld2(X + 2 * ((int64_t)__ldg(idx + i) * h2 + q)));
+    }
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -1038,6 +1065,8 @@ int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alp
         }
         SpDev a;
         a.nrows = P.nrows; a.indptr = P.indptr; a.indices = P.indices; a.X = X; a.ld = ld; a.out = out;
+        a.Xg = S->ghost;
+        a.nown = S->ghost != nullptr ? (int32_t)S->nown : INT32_MAX;
         if (need_asm) {
             if (S->nnz > 0) {
                 int64_t g = (S->nnz + NT - 1) / NT;
@@ -1073,7 +1102,8 @@ int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alp
         return (int)cudaGetLastError();
     }
 
-    // fused-coefficient path (no scratch given, or an all-zero matrix)
+    // fused-coefficient path (no scratch given, or an all-zero matrix); no ghost rows there
+    if (S->ghost != nullptr) return CL_EARG;
     const int64_t threads = P.nrows * G;
     const int grid = red_grid(threads);
     if (ld == 1) {
@@ -1183,6 +1213,18 @@ int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const dou
         }
     }
 #undef CL_DK
+    return (int)cudaGetLastError();
+}
+
+int cl_gather_rows(const int32_t* idx, int64_t count, int32_t ld, const double* X, double* out, void* stream) {
+    if (count < 0 || ld < 2 || (ld & 1) || (count > 0 && (idx == nullptr || X == nullptr || out == nullptr)))
+        return CL_EARG;
+    if (!aligned16(X) || !aligned16(out)) return CL_EARG;
+    if (count == 0) return CL_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t total = count * (ld / 2);
+    int64_t g = (total + NT - 1) / NT;
+    gather_rows_kernel<<<(int)(g > NSM * 16 ? NSM * 16 : g), NT, 0, st>>>(idx, count, ld / 2, X, out);
     return (int)cudaGetLastError();
 }
 

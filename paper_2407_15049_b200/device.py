@@ -48,6 +48,8 @@ class Device:
         self.slab = torch.zeros(SLAB, dtype=F64, device=self.dev)
         self.host = torch.zeros(SLAB, dtype=F64, pin_memory=True)
         self.launches = 0
+        self.group = None          # torch.distributed group of a row-sharded solve (shard.py)
+        self.world = 1
 
     # -- plumbing ---------------------------------------------------------
     @property
@@ -59,7 +61,17 @@ class Device:
         return ctypes.c_void_p(self.slab.data_ptr() + 8 * k)
 
     def fetch(self, count):
-        """Copy slab[:count] to the host (pinned) and wait; returns numpy view."""
+        """Copy slab[:count] to the host (pinned) and wait; returns numpy view.
+
+        In a row-sharded solve every slab entry is a per-rank partial sum: the
+        prefix is all-reduced (into a copy, the partials stay) first, so all
+        ranks read identical scalars."""
+        if self.world > 1:
+            from .shard import all_reduce_sum
+            red = all_reduce_sum(self.slab[:count].clone(), self.group)
+            self.host[:count].copy_(red, non_blocking=True)
+            self.stream.synchronize()
+            return self.host[:count].numpy()
         self.host[:count].copy_(self.slab[:count], non_blocking=True)
         self.stream.synchronize()
         return self.host[:count].numpy()
@@ -125,6 +137,11 @@ class Device:
                 e.db[d] = _op_code(y)
             nd = len(dots)
         e.ndot = nd
+        halo = getattr(pat, "halo", None)
+        if halo is not None:
+            ghost = halo.exchange(X, ld, self.gather_rows)
+            P.ghost = ghost.data_ptr()
+            P.nown = halo.nown
         rc = self.lib.cl_pattern_spmm(ctypes.byref(P), ptr(X), int(ld), float(alpha), ctypes.byref(e),
                                       ptr(out), self.slot(at) if nd else None,
                                       ptr(self.ws) if nd else None, self.sp)
@@ -144,6 +161,12 @@ class Device:
                                          ptr(out1), ptr(X3), ptr(Y3), ptr(out2), self.sp)
         self.launches += 1
         check(rc, "cl_constraint_eval")
+
+    def gather_rows(self, idx, X, out):
+        """out[i] = X[idx[i]] (halo packing, shard.py)."""
+        rc = self.lib.cl_gather_rows(ptr(idx), int(idx.numel()), int(X.shape[1]), ptr(X), ptr(out), self.sp)
+        self.launches += 1
+        check(rc, "cl_gather_rows")
 
     def sddmm(self, imap, jmap, ld, X, Y, out):
         rc = self.lib.cl_sddmm(int(imap.numel()), ptr(imap), ptr(jmap), int(ld), ptr(X), ptr(Y),

@@ -47,6 +47,7 @@ class DevicePattern:
     at_val: torch.Tensor | None   # fp64
 
     scratch: torch.Tensor | None = None   # assembled slot coefficients (lazy)
+    halo: object = None                   # shard.HaloPlan of a row-sharded pattern
 
     @property
     def nnz(self):

@@ -195,3 +195,44 @@ def test_diag_alm_update_buckets(dev, nh, refresh):
     for h in range(nh):
         assert close(s[7 + h], np.sum(g * Hh[h]))
         assert close(s[7 + _lib.CL_MAXIN + h], np.sum(yy * Hh[h]))
+
+
+class _FakeHalo:
+    """Stands in for shard.HaloPlan: columns >= nown read a fixed ghost block."""
+
+    def __init__(self, nown, ghost):
+        self.nown, self.ghost, self.calls = nown, ghost, 0
+
+    def exchange(self, X, ld, pack):
+        self.calls += 1
+        return self.ghost
+
+
+@pytest.mark.parametrize("ld", [2, 26, 66])
+def test_ghost_rows_in_tiled_spmm(dev, ld):
+    """Row-sharded SpMM: column j < nown reads the local factor, j >= nown the halo block."""
+    import torch
+    rng = np.random.default_rng(40 + ld)
+    nown, nghost = 2500, 1700
+    M = _rand_csr(rng, nown, nown + nghost, lambda i: int(rng.integers(0, 14)))
+    P = _pattern(M)
+    Xo, Xod = _factor(rng, nown, ld)
+    Xg, Xgd = _factor(rng, nghost, ld)
+    P.halo = _FakeHalo(nown, Xgd)
+    out = torch.empty_like(Xod)
+    dev.spmm(P, Xod, ld, out=out, c_coeff=1.0, Z=[Xod], dots=[("out", ("z", 0))], at=20)
+    ref = M @ np.vstack([Xo, Xg])
+    assert P.halo.calls == 1
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * (1 + np.abs(ref).max())
+    assert abs(dev.fetch(21)[20] - np.sum(ref * Xo)) <= 1e-10 * (1 + abs(np.sum(ref * Xo)))
+
+
+def test_gather_rows_kernel(dev):
+    import torch
+    rng = np.random.default_rng(3)
+    X, Xd = _factor(rng, 1000, 26)
+    idx = rng.choice(1000, size=321, replace=False).astype(np.int32)
+    out = torch.zeros((400, 26), dtype=torch.float64, device="cuda")
+    dev.gather_rows(torch.as_tensor(idx).cuda(), Xd, out)
+    got = out.cpu().numpy()
+    assert np.array_equal(got[:321], X[idx]) and not got[321:].any()
