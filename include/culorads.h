@@ -145,7 +145,8 @@ int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const dou
                             double* out2, void* stream);
 
 /* Halo packing of the row-sharded solve (rows published to the other ranks
- * before an all-gather): out[i,:] = X[idx[i],:] for i < count, ld even. */
+ * before an all-gather): out[i,:] = X[idx[i],:] for i < count (16-byte vector
+ * path for even ld and aligned rows, scalar otherwise). */
 int cl_gather_rows(const int32_t* idx, int64_t count, int32_t ld, const double* X, double* out, void* stream);
 
 /* Gathered outer product at K positions (linops.py:49), x[k] = X[imap[k]]·Y[jmap[k]]. */

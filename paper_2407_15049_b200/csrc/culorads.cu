@@ -954,6 +954,16 @@ __global__ void __launch_bounds__(NT) gather_rows_kernel(const int32_t* __restri
     }
 }
 
+__global__ void __launch_bounds__(NT) gather_rows_scalar_kernel(const int32_t* __restrict__ idx, int64_t count, int ld,
+                                                                const double* __restrict__ X, double* __restrict__ out) {
+    const int64_t total = count * ld;
+    for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < total; k += (int64_t)gridDim.x * NT) {
+        const int64_t i = k / ld;
+        const int q = (int)(k - i * ld);
+        out[k] = __ldg(X + (int64_t)__ldg(idx + i) * ld + q);
+    }
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace
@@ -1217,11 +1227,15 @@ int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const dou
 }
 
 int cl_gather_rows(const int32_t* idx, int64_t count, int32_t ld, const double* X, double* out, void* stream) {
-    if (count < 0 || ld < 2 || (ld & 1) || (count > 0 && (idx == nullptr || X == nullptr || out == nullptr)))
-        return CL_EARG;
-    if (!aligned16(X) || !aligned16(out)) return CL_EARG;
+    if (count < 0 || ld < 1 || (count > 0 && (idx == nullptr || X == nullptr || out == nullptr))) return CL_EARG;
     if (count == 0) return CL_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if ((ld & 1) || !aligned16(X) || !aligned16(out)) {
+        const int64_t total = count * ld;
+        int64_t g = (total + NT - 1) / NT;
+        gather_rows_scalar_kernel<<<(int)(g > NSM * 16 ? NSM * 16 : g), NT, 0, st>>>(idx, count, ld, X, out);
+        return (int)cudaGetLastError();
+    }
     const int64_t total = count * (ld / 2);
     int64_t g = (total + NT - 1) / NT;
     gather_rows_kernel<<<(int)(g > NSM * 16 ? NSM * 16 : g), NT, 0, st>>>(idx, count, ld / 2, X, out);

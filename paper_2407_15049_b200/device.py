@@ -164,7 +164,7 @@ class Device:
 
     def gather_rows(self, idx, X, out):
         """out[i] = X[idx[i]] (halo packing, shard.py)."""
-        rc = self.lib.cl_gather_rows(ptr(idx), int(idx.numel()), int(X.shape[1]), ptr(X), ptr(out), self.sp)
+        rc = self.lib.cl_gather_rows(ptr(idx), int(idx.numel()), int(out.shape[1]), ptr(X), ptr(out), self.sp)
         self.launches += 1
         check(rc, "cl_gather_rows")
 

@@ -136,7 +136,7 @@ class HaloPlan:
     def exchange(self, X, ld, pack):
         """Pack this rank's published rows of X and all-gather them; returns the halo buffer."""
         send, recv = self.buffers(ld, X)
-        pack(self.publish, X, send)
+        pack(self.publish, X.reshape(-1, ld), send)
         if self.world == 1:
             recv.copy_(send)
         elif recv.is_cuda and _nccl(self.group):
@@ -240,3 +240,104 @@ def sharded_maxcut_ops(n_global, deg, seed, rank, world, dev, group=None):
     problem = _NS(n=nown, m=nown, n_global=n_global, nnz_a_full=lambda: n_global)
     return _NS(problem=problem, cop=_NS(con=con), c_mat=_NS(cpat=cpat), b=ones.clone(),
                diag_aval=ones, is_diag=True, dev=dev, plan=plan, lo=lo, hi=hi, n_edges=n_edges)
+
+
+# ---------------------------------------------------------------------------
+# row-sharded solve of a diagonal-constraint problem (MaxCut family)
+# ---------------------------------------------------------------------------
+
+class ShardProblem:
+    """Local view of a global SdpProblem on one rank: local sizes, global norms.
+
+    ``n``/``m`` are the owned rows / constraints (buffer sizes of the solver
+    stages); every normalisation (b norms, ||vec C||_1, nnz(A)) stays global,
+    as do ``n_global``/``m_global`` for the rank rules (driver.py:130-135)."""
+
+    def __init__(self, p, lo, hi):
+        self.n = self.m = hi - lo
+        self.n_global, self.m_global = p.n, p.m
+        self.lo, self.hi = lo, hi
+        self.b_norm1, self.b_norminf, self.c_vec_norm1 = p.b_norm1, p.b_norminf, p.c_vec_norm1
+        self._nnz_a_full = p.nnz_a_full()
+        self.maximize = p.maximize
+
+    def nnz_a_full(self):
+        return self._nnz_a_full
+
+
+def slice_pattern(pat, lo, hi, bounds, rank, world, group, con_lo=None, halo=True):
+    """Rows [lo, hi) of a DevicePattern, columns remapped through a HaloPlan.
+
+    Adjoint rows keep their constraint coefficients; constraint ids are
+    shifted by ``con_lo`` (they must belong to this rank's constraints)."""
+    from .linops import DevicePattern, padded
+
+    ptr = pat.indptr
+    s0, s1 = int(ptr[lo]), int(ptr[hi])
+    indptr = ptr[lo:hi + 1] - s0
+    cols = pat.indices[s0:s1].to(I64)
+    plan = HaloPlan(lo, hi, indptr, cols, bounds, rank, world, group)
+    pad_ptr = torch.zeros(hi - lo + 1 + 16, dtype=I64, device=ptr.device)
+    pad_ptr[:hi - lo + 1] = indptr
+    cv = padded(pat.cv[s0:s1]) if pat.cv is not None else None
+    at_ptr = at_con = at_val = None
+    if pat.at_ptr is not None:
+        a0, a1 = int(pat.at_ptr[s0]), int(pat.at_ptr[s1])
+        ap = torch.zeros(s1 - s0 + 1 + 16, dtype=I64, device=ptr.device)
+        ap[:s1 - s0 + 1] = pat.at_ptr[s0:s1 + 1] - a0
+        at_ptr = ap[:s1 - s0 + 1]
+        con = pat.at_con[a0:a1].to(I64) - (con_lo if con_lo is not None else 0)
+        if con.numel() and (int(con.min()) < 0 or int(con.max()) >= hi - lo):
+            raise NotImplementedError("row-sharded solve needs each constraint owned by the rank "
+                                      "that owns its rows (diagonal constraints)")
+        at_con = padded(con.to(I32))
+        at_val = padded(pat.at_val[a0:a1])
+    out = DevicePattern(hi - lo, pad_ptr[:hi - lo + 1], padded(plan.local_indices), cv, at_ptr, at_con, at_val)
+    out.halo = plan if (halo and world > 1 and sum(plan.counts) > 0) else None
+    return out
+
+
+def build_sharded_operators(p, rank, world, dev, group=None):
+    """Rank-local OperatorBundle of a diagonal-constraint problem (constraint c is
+    a_c e_c e_c^T, e.g. MaxCut): factor rows, C/Omega/Omega_A pattern rows and
+    constraints [lo, hi), remote columns through halo plans. Built from the
+    single-device operators (linops.build_operators), then sliced."""
+    from .linops import (AdjointOperator, CompressedOperator, ConstraintCSR, ObjectiveMatrix,
+                         OperatorBundle, build_operators)
+
+    full = build_operators(p, dev=dev)
+    if not full.is_diag:
+        raise NotImplementedError("row-sharded solve supports diagonal constraints (MaxCut family)")
+    b = block_bounds(p.n, world)
+    lo, hi = b[rank], b[rank + 1]
+    cpat = slice_pattern(full.c_mat.cpat, lo, hi, b, rank, world, group)
+    omega = slice_pattern(full.adj.omega, lo, hi, b, rank, world, group, con_lo=lo)
+    apat = slice_pattern(full.adj.apat, lo, hi, b, rank, world, group, con_lo=lo)
+    aval = full.diag_aval[lo:hi].clone()      # clone: slices of m-vectors must start 16-byte aligned
+    fc = full.cop.con
+    con = ConstraintCSR(m=hi - lo, indptr=(fc.indptr[lo:hi + 1] - fc.indptr[lo]).contiguous(),
+                        colidx=fc.colidx[lo:hi], pi=fc.pi[lo:hi] - lo, pj=fc.pj[lo:hi] - lo,
+                        val=fc.val[lo:hi].clone(), diag_aval=aval)
+    sp = ShardProblem(p, lo, hi)
+    cop = CompressedOperator(hi - lo, hi - lo, full.cop.ncols, full.cop.imap, full.cop.jmap,
+                             full.cop.col_slot, con, dev)
+    adj = AdjointOperator(hi - lo, hi - lo, full.adj.sup_i_host, full.adj.sup_j_host, omega, apat,
+                          omega.cv, dev)
+    ops = OperatorBundle(problem=sp, cop=cop, adj=adj, c_mat=ObjectiveMatrix(adj, cpat), dev=dev,
+                         b=full.b[lo:hi].clone(), diag_aval=aval, omega_size_ref=full.omega_size_ref)
+    ops.row_range = (lo, hi)
+    del full
+    return ops
+
+
+def solve_sharded(p, cfg=None, *, group=None, dev=None):
+    """driver.solve on this rank's row block; every rank returns the same report."""
+    from . import driver
+    from .device import default_device
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = dev or default_device()
+    dev.world, dev.group = world, group
+    ops = build_sharded_operators(p, rank, world, dev, group)
+    return driver.solve(p, cfg, ops=ops)

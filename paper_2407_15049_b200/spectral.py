@@ -43,15 +43,20 @@ def _host_callback_op(apply_s, dev):
     return _DeviceOp(fn)
 
 
-def _lanczos_smallest(op, n, seed, max_basis, dev):
+def _lanczos_smallest(op, n, seed, max_basis, dev, rows=None):
+    """spectral.py:28. ``rows`` = (lo, hi, n_global): this rank's block of a
+    row-sharded vector; the Gram projections are all-reduced."""
     rng = np.random.default_rng(seed)
-    k_max = min(n, max_basis)
+    n_all = rows[2] if rows is not None else n
+    k_max = min(n_all, max_basis)
     npad = n + (n & 1)
     Q = dev.zeros(k_max, npad)
     alphas = np.zeros(k_max)
     betas = np.zeros(max(k_max - 1, 0))
-    q0 = rng.standard_normal(n)
+    q0 = rng.standard_normal(n_all)
     q0 /= np.linalg.norm(q0)
+    if rows is not None:
+        q0 = q0[rows[0]:rows[1]]
     Q[0, :n] = torch.as_tensor(q0).to(dev.dev)
     u = dev.zeros(npad)
     r = dev.zeros(npad)
@@ -69,6 +74,9 @@ def _lanczos_smallest(op, n, seed, max_basis, dev):
             dev.lincomb(r[:n], [u[:n], qk], [1.0, -alphas[k]])
         for _ in range(2):      # full reorthogonalisation, twice (spectral.py:55-56)
             dev.basis_project(Q, k + 1, n, r, h)
+            if dev.world > 1:
+                from .shard import all_reduce_sum
+                all_reduce_sum(h[:k + 1], dev.group)
             dev.basis_subtract(Q, k + 1, n, h, r)
         k += 1
         dev.lincomb(None, [r[:n]], [0.0], dots=[(0, 0)], at=A + 1)
@@ -94,7 +102,7 @@ def _lanczos_smallest(op, n, seed, max_basis, dev):
     return theta, residual, k
 
 
-def smallest_eigenvalue(apply_s, n, tol=1e-7, seed=0, max_basis=300, dev=None) -> EigEstimate:
+def smallest_eigenvalue(apply_s, n, tol=1e-7, seed=0, max_basis=300, dev=None, rows=None) -> EigEstimate:
     """Smallest eigenvalue of a self-adjoint operator (spectral.py:67).
 
     ``apply_s`` is a host callback v -> S v (numpy), or a device operator from
@@ -102,9 +110,9 @@ def smallest_eigenvalue(apply_s, n, tol=1e-7, seed=0, max_basis=300, dev=None) -
     """
     dev = dev or default_device()
     op = apply_s if isinstance(apply_s, _DeviceOp) else _host_callback_op(apply_s, dev)
-    theta, residual, k = _lanczos_smallest(op, n, seed, max_basis, dev)
+    theta, residual, k = _lanczos_smallest(op, n, seed, max_basis, dev, rows)
     if residual > tol * (1.0 + abs(theta)):
-        t2, r2, k2 = _lanczos_smallest(op, n, seed + 1, max_basis, dev)
+        t2, r2, k2 = _lanczos_smallest(op, n, seed + 1, max_basis, dev, rows)
         if r2 < residual:
             theta, residual, k = t2, r2, k2
     return EigEstimate(value=theta, residual=residual,
@@ -127,10 +135,13 @@ def dual_infeasibility(problem, ops, lam, tol=1e-7, seed=0):
     Returns (value, verified, sigma_min); lam may be host or device."""
     dev = ops.dev
     if isinstance(lam, torch.Tensor):
-        neg = dev.empty(problem.m)
+        neg = dev.empty(ops.problem.m)
         dev.lincomb(neg, [lam.to(dev.dev)], [-1.0])
     else:
         neg = torch.as_tensor(-np.asarray(lam, dtype=np.float64)).to(dev.dev)
-    est = smallest_eigenvalue(omega_operator(ops, neg, 1.0), problem.n, tol=tol, seed=seed, dev=dev)
+    rr = getattr(ops, "row_range", None)
+    rows = (rr[0], rr[1], problem.n) if rr is not None else None
+    n_loc = ops.problem.n
+    est = smallest_eigenvalue(omega_operator(ops, neg, 1.0), n_loc, tol=tol, seed=seed, dev=dev, rows=rows)
     value = abs(min(0.0, est.value)) / (1.0 + problem.c_vec_norm1)
     return value, est.verified, est.value

@@ -70,11 +70,70 @@ def test_sharded_gradient_pass_matches_global(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     n, deg, ld = 6000, 6.0, 26
-    mp.spawn(_worker, args=(world, _free_port(), n, deg, ld, q), nprocs=world, join=True)
-    res = [q.get() for _ in range(world)]
+    pc = mp.spawn(_worker, args=(world, _free_port(), n, deg, ld, q), nprocs=world, join=False)
+    res = [q.get(timeout=600) for _ in range(world)]
+    while not pc.join():
+        pass
     for rank, err, axe, gg, gg_ref, crr, crr_ref, counts in res:
         assert err <= 1e-13, (rank, err)
         assert axe <= 1e-12
         assert abs(gg - gg_ref) <= 1e-10 * gg_ref      # all-reduced scalars equal the global ones
         assert abs(crr - crr_ref) <= 1e-10 * (1 + abs(crr_ref))
         assert sum(counts) > 0                          # random graph: rows really cross blocks
+
+
+def _solve_worker(rank, world, port, case, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2407_15049_b200 import driver, shard
+        from paper_2407_15049_b200.device import Device
+        from tests._golden import cfg_of, load, problem_from
+        z = load(f"solve_{case}.npz")
+        p = problem_from(z)
+        try:
+            rep = shard.solve_sharded(p, driver.SolverConfig(**cfg_of(z)), dev=Device())
+        except Exception:
+            import traceback
+            q.put((rank, "error", traceback.format_exc(), None, None, None, None, None))
+            raise
+        tr = np.array([r[2:7] for r in rep.trace_rows], dtype=float).reshape(-1, 5)
+        q.put((rank, rep.status, rep.objective, rep.err1, rep.err3, rep.err2, tr, rep.rank_history))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,world", [("g1_like", 2), ("triangle_l2", 2), ("maxcut_2k_deg6", 3)])
+def test_sharded_solve_within_reference_envelope(case, world):
+    """A row-sharded solve (2-3 ranks) stays inside the reference's envelope, like the 1-GPU solve."""
+    from tests._golden import load
+    from tests.test_gpu_solve import first_dev
+    z = load(f"solve_{case}.npz")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    # read the queue before joining: a child blocks on exit until its queued payload is consumed
+    pc = mp.spawn(_solve_worker, args=(world, _free_port(), case, q), nprocs=world, join=False)
+    res = []
+    for _ in range(world):
+        res.append(q.get(timeout=600))
+        if res[-1][1] == "error":
+            pytest.fail(f"rank {res[-1][0]} raised:\n{res[-1][2]}")
+    res.sort(key=lambda t: t[0])
+    while not pc.join():
+        pass
+    # every rank took the same decisions and reports the same numbers
+    for r in res[1:]:
+        assert r[1] == res[0][1] and r[2] == res[0][2] and np.array_equal(r[6], res[0][6])
+    _, status, obj, err1, err3, err2, tr, ranks = res[0]
+    ref = z["trace"]
+    statuses = set(z["ulp_status"].tolist()) | {str(z["status"])}
+    objs = np.append(z["ulp_objective"], float(z["objective"]))
+    horizon = first_dev(tr, ref)
+    print(f"{case} x{world}: status {status} obj {obj!r} rows {len(tr)} (ref {len(ref)}) horizon {horizon} "
+          f"(ulp {int(z['ulp_horizon'].min())})")
+    assert status in statuses
+    assert horizon >= min(len(ref), len(tr), max(1, int(z["ulp_horizon"].min()) // 2))
+    pad = 1e-6 * max(1.0, abs(objs).max())
+    assert objs.min() - pad <= obj <= objs.max() + pad
