@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-solver", action="store_true", help="skip the solver-level rates and the G1 solve")
+    ap.add_argument("--n-g1", type=int, default=800)
     return ap.parse_args()
 
 
@@ -177,6 +179,66 @@ def cpu_measure(n, deg, seed, budget_s, warmup=1, max_steps=None):
     sec = sum(times) / len(times)
     return dict(value=nbytes / sec / 1e9, sec=sec, steps=len(times), threads=threads,
                 bytes=nbytes, n=n)
+
+
+def solver_rates(ops, dev, R, n, r, ld, n_g1):
+    """Solver-level numbers beside the operator bench (north_star: solve time and
+    iterations/s): ALM inner iterations and ADMM steps on the bench instance, and a
+    full solve of the G1-shaped instance (BASELINE configs[0]) on the device and,
+    for the CPU baseline, through the oracle on one host core, same stop rule."""
+    import torch
+
+    from paper_2407_15049_b200 import admm, alm, driver, graphs, problem
+
+    out = {}
+    rho = max(1.0, ops.problem.m / math.sqrt(max(ops.problem.nnz_a_full(), 1)))
+    dual = alm.DualVector(lam=dev.zeros(ops.problem.m), rho=rho)
+    core = alm.AlmCore(ops, n, ld)
+    Rw = R.clone()
+    rec = alm._RankRecorder(None, r)
+    alm._inner(core, Rw, dual.lam, rho, 1.0, 0.0, 3, None, 8, rec)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    res = alm._inner(core, Rw, dual.lam, rho, 1.0, 0.0, 20, None, 8, rec)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t
+    out["alm_inner_ms_per_iter"] = 1e3 * dt / max(res.iterations, 1)
+    out["alm_inner_iters_per_s"] = max(res.iterations, 1) / dt
+    st = admm.AdmmState(U=Rw.clone(), V=Rw.clone(), dual=dual, r=r)
+    hs, pool = admm.HalfStep(ops, n, ld), admm._Pool(dev, n, ld)
+    admm.admm_step(st, ops, hs=hs, pool=pool)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    cg = 0
+    for _ in range(3):
+        s_ = admm.admm_step(st, ops, hs=hs, pool=pool)
+        cg += s_.cg_iters_u + s_.cg_iters_v
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t
+    out["admm_ms_per_step"] = 1e3 * dt / 3
+    out["admm_cg_iters_per_step"] = cg / 3
+    del core, st, hs, pool, Rw
+    # full solve, G1-shaped instance (configs[0]): device vs the CPU oracle
+    p = problem.build_maxcut(graphs.random_sparse(n_g1, deg=48.0, seed=1))
+    driver.solve(p, driver.SolverConfig(time_limit=5.0))      # warm-up
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    rep = driver.solve(p, driver.SolverConfig())
+    gpu_s = time.perf_counter() - t
+    from oracle import lrsdp_oracle as O
+    t = time.perf_counter()
+    ref = O.solve(p)
+    cpu_s = time.perf_counter() - t
+    out["g1_solve"] = {
+        "instance": f"MaxCut random graph n={n_g1}, {p.C.nnz_stored - p.n} edges (BASELINE configs[0])",
+        "stop": "reopt_level 1, eps 1e-5 (SolverConfig defaults)",
+        "gpu_s": gpu_s, "cpu_s": cpu_s, "cpu_kind": "oracle port, 1 host core", "speedup": cpu_s / gpu_s,
+        "status": rep.status, "cpu_status": ref["status"], "objective": rep.objective,
+        "cpu_objective": ref["objective"],
+        "objective_rel_diff": abs(rep.objective - ref["objective"]) / max(1.0, abs(ref["objective"])),
+        "trace_rows": len(rep.trace_rows), "cpu_trace_rows": len(ref["trace"]),
+    }
+    return out
 
 
 def run_reference(args, rank):
@@ -360,6 +422,9 @@ def run_ours(args, rank, world, local_rank):
     kern = {nm: {"ms": kms[nm], "bytes": kbytes[nm],
                  "GB/s": kbytes[nm] / (kms[nm] * 1e-3) / 1e9,
                  "share": kms[nm] / sum(kms.values())} for nm in names}
+    solver = None
+    if world == 1 and not args.no_solver:
+        solver = solver_rates(ops, dev, R, n, r, ld, args.n_g1)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         n_s = int(min(n, 2e6))
@@ -386,6 +451,7 @@ def run_ours(args, rank, world, local_rank):
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
+        "solver": solver,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

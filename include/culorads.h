@@ -118,6 +118,9 @@ typedef struct {
     int32_t ndot;
     uint8_t da[8];
     uint8_t db[8];
+    const double* drow;     /* optional: out[i,:] += drow[i] * dmul[i] * Y[0][i,:] (dmul NULL = 1);
+                               the diagonal A*(v) term of a diagonal-constraint problem */
+    const double* dmul;
 } cl_epilogue;
 
 int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alpha,
@@ -148,6 +151,18 @@ int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const dou
  * before an all-gather): out[i,:] = X[idx[i],:] for i < count (16-byte vector
  * path for even ld and aligned rows, scalar otherwise). */
 int cl_gather_rows(const int32_t* idx, int64_t count, int32_t ld, const double* X, double* out, void* stream);
+
+/* ADMM half-step CG for diagonal constraints (admm.py:65 cg_solve with the
+ * operator of admm.py:45 subproblem_apply, A = diag(a)): one launch per
+ * operator application and one per update, each factor operand read once.
+ *   cl_diag_cg_apply: [p <- r + beta p if r != NULL]  y_c = a_c <p_c, Wf_c>,
+ *                     Q_c = rho (a_c y_c Wf_c + p_c),  dots_out[0] = <p, Q>
+ *   cl_cg_step:       x_out = x_in + alpha p,  r -= alpha Q,  dots_out[0] = <r, r>
+ * (N = n*ld doubles; x_out may alias x_in). */
+int cl_diag_cg_apply(int64_t n, int32_t ld, const double* aval, double rho, double beta, const double* r, double* p,
+                     const double* Wf, double* Q, double* dots_out, double* ws, void* stream);
+int cl_cg_step(int64_t N, double alpha, const double* x_in, double* x_out, const double* p, double* r,
+               const double* Q, double* dots_out, double* ws, void* stream);
 
 /* Gathered outer product at K positions (linops.py:49), x[k] = X[imap[k]]·Y[jmap[k]]. */
 int cl_sddmm(int64_t K, const int32_t* imap, const int32_t* jmap, int32_t ld,

@@ -25,7 +25,7 @@ CL_DOT_PAIRS, CL_DOT_OUT_ALL, CL_DOT_FIRST_TWO = 0, 1, 2
 CL_EARG = 1001
 
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_diag_constraint_eval", "cl_sddmm",
-           "cl_gather_rows",
+           "cl_gather_rows", "cl_diag_cg_apply", "cl_cg_step",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
            "cl_version", "cl_device_ok")
 
@@ -50,7 +50,8 @@ class Pattern(ctypes.Structure):
 class Epilogue(ctypes.Structure):
     _fields_ = [("ny", I32), ("Y", P * CL_MAXY), ("ycoef", D * CL_MAXY),
                 ("nz", I32), ("Z", P * CL_MAXY),
-                ("ndot", I32), ("da", ctypes.c_uint8 * 8), ("db", ctypes.c_uint8 * 8)]
+                ("ndot", I32), ("da", ctypes.c_uint8 * 8), ("db", ctypes.c_uint8 * 8),
+                ("drow", P), ("dmul", P)]
 
 
 class DiagUpdateArgs(ctypes.Structure):
@@ -75,6 +76,8 @@ def _declare(lib):
                                     P, P, P, P]
     lib.cl_constraint_eval.argtypes = [I64, P, P, P, P, I32, P, P, P, P, P, P, P, P, P]
     lib.cl_diag_constraint_eval.argtypes = [I64, P, I32, P, P, P, P, P, P, P, P, P]
+    lib.cl_diag_cg_apply.argtypes = [I64, I32, P, D, D, P, P, P, P, P, P, P]
+    lib.cl_cg_step.argtypes = [I64, D, P, P, P, P, P, P, P, P]
     lib.cl_gather_rows.argtypes = [P, I64, I32, P, P, P]
     lib.cl_sddmm.argtypes = [I64, P, P, I32, P, P, P, P]
     lib.cl_diag_alm_update.argtypes = [ctypes.POINTER(DiagUpdateArgs), P, P, P]

@@ -61,6 +61,10 @@ class HalfStep:
     def apply(self, W, Wf, rho, out, dot_with=None, at=None):
         """out = rho*(A*(A(W Wf^T)) Wf + W); optional <dot_with, out> -> slab[at]."""
         ops, dev = self.ops, self.dev
+        if ops.is_diag and (dot_with is None or dot_with is W):
+            # diagonal A: the whole operator is row-local, one streaming pass (cl_diag_cg_apply)
+            dev.diag_cg_apply(ops.diag_aval, self.ld, rho, W, Wf, out, at=at if at is not None else 0)
+            return out
         dev.constraint_eval(ops.cop.con, self.ld, W, Wf, self.y)
         dots = [(("y", 0), "out")] if dot_with is not None else None
         dev.spmm(ops.adj.apat, Wf, self.ld, alpha=rho, out=out, Y=[W], ycoef=[rho], w1=self.y,
@@ -70,15 +74,28 @@ class HalfStep:
     def rhs(self, Wf, lam, rho, scale, out, at):
         """out = S_b Wf + rho Wf with S_b = -scale C - A*(lam) + rho A*(b); ||out||^2 -> slab[at]."""
         ops, dev = self.ops, self.dev
+        if ops.is_diag:
+            # S_b = -scale C + diag(a (rho b - lam)): the C product plus a row-diagonal epilogue term
+            dev.lincomb(self.nlam, [ops.b, lam], [rho, -1.0])
+            dev.spmm(ops.c_mat.cpat, Wf, self.ld, alpha=-scale, out=out, Y=[Wf], ycoef=[rho], c_coeff=1.0,
+                     drow=self.nlam, dmul=ops.diag_aval, dots=[("out", "out")], at=at)
+            return out
         dev.lincomb(self.nlam, [lam], [-1.0])
         dev.lincomb(self.rhob, [ops.b], [rho])
         dev.spmm(ops.adj.omega, Wf, self.ld, alpha=1.0, out=out, Y=[Wf], ycoef=[rho],
                  c_coeff=-scale, w1=self.nlam, w2=self.rhob, dots=[("out", "out")], at=at)
         return out
 
-    def cg(self, x, Wf, rho, rhs, eps, max_iter):
-        """admm.py:65 in place on x (a device factor). Returns (iterations, residual)."""
+    def cg(self, x, Wf, rho, rhs, eps, max_iter, x0=None):
+        """admm.py:65 on device factors. Returns (iterations, residual).
+
+        The iterate starts at ``x0`` (read only) when given and is written to
+        ``x``; otherwise ``x`` is updated in place."""
+        if self.ops.is_diag:
+            return self._cg_diag(x, Wf, rho, rhs, eps, max_iter, x0)
         dev = self.dev
+        if x0 is not None:
+            dev.lincomb(x, [x0], [1.0])
         r, p, Q = self.r, self.p, self.Q
         A = self.S_CG
         self.apply(x, Wf, rho, Q)
@@ -106,6 +123,49 @@ class HalfStep:
                 break
             dev.lincomb(p, [r, p], [1.0, qn / qr])
             qr = qn
+        dev.lincomb(None, [x], [0.0], dots=[(0, 0)], at=A + 3)
+        if not math.isfinite(float(dev.fetch(A + 4)[A + 3])):
+            raise DivergedError("CG iterate diverged", last_iterate=x)
+        return its, rnorm
+
+
+    def _cg_diag(self, x, Wf, rho, rhs, eps, max_iter, x0):
+        """Same iteration as ``cg`` for diagonal A with fused launches: the direction
+        update p = r + beta p rides on the next operator application and the x/r
+        updates share one pass (cl_diag_cg_apply, cl_cg_step)."""
+        dev, ops = self.dev, self.ops
+        r, p, Q = self.r, self.p, self.Q
+        A = self.S_CG
+        xs = x if x0 is None else x0
+        dev.diag_cg_apply(ops.diag_aval, self.ld, rho, xs, Wf, Q, at=A)      # Q = apply(x0)
+        dev.lincomb(r, [rhs, Q], [1.0, -1.0], dots=[("out", "out")], at=A)
+        qr = float(dev.fetch(A + 1)[A])
+        rnorm = math.sqrt(qr)
+        if rnorm <= eps:
+            if x0 is not None:
+                dev.lincomb(x, [x0], [1.0])
+            return 0, rnorm
+        its = 0
+        beta = 0.0
+        for k in range(max_iter):
+            dev.diag_cg_apply(ops.diag_aval, self.ld, rho, p, Wf, Q, r=r, beta=beta, at=A + 1)
+            pq = float(dev.fetch(A + 2)[A + 1])
+            if not math.isfinite(pq):
+                raise DivergedError("CG produced non-finite curvature", last_iterate=xs)
+            if pq <= 0.0:
+                raise SpdViolationError(f"non-positive curvature {pq:.3e} in CG (operator not SPD)")
+            alpha = qr / pq
+            dev.cg_step(alpha, xs, x, p, r, Q, at=A + 2)
+            xs = x
+            qn = float(dev.fetch(A + 3)[A + 2])
+            rnorm = math.sqrt(qn)
+            its = k + 1
+            if rnorm <= eps:
+                break
+            beta = qn / qr
+            qr = qn
+        if x0 is not None and its == 0:
+            dev.lincomb(x, [x0], [1.0])
         dev.lincomb(None, [x], [0.0], dots=[(0, 0)], at=A + 3)
         if not math.isfinite(float(dev.fetch(A + 4)[A + 3])):
             raise DivergedError("CG iterate diverged", last_iterate=x)
@@ -255,15 +315,13 @@ def admm_step(state: AdmmState, ops, *, scale=1.0, cg_cap=200, cg_rel_floor=1e-1
     hs.rhs(state.V, lam, rho, scale, rhs, at=431)
     eps_u = max(rel * math.sqrt(float(dev.fetch(432)[431])), 1e-300)
     U = pool.get() if pool else dev.empty(n, ld)
-    dev.lincomb(U, [state.U], [1.0])
-    it_u, res_u = hs.cg(U, state.V, rho, rhs, eps_u, cg_cap)
+    it_u, res_u = hs.cg(U, state.V, rho, rhs, eps_u, cg_cap, x0=state.U)
     state.set_factors(U=U)
 
     hs.rhs(U, lam, rho, scale, rhs, at=432)
     eps_v = max(rel * math.sqrt(float(dev.fetch(433)[432])), 1e-300)
     V = pool.get() if pool else dev.empty(n, ld)
-    dev.lincomb(V, [state.V], [1.0])
-    it_v, res_v = hs.cg(V, U, rho, rhs, eps_v, cg_cap)
+    it_v, res_v = hs.cg(V, U, rho, rhs, eps_v, cg_cap, x0=state.V)
     state.set_factors(V=V)
     if pool:
         pool.put(rhs)

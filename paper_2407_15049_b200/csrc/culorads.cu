@@ -199,6 +199,8 @@ struct EpiDev {
     const double* Z[CL_MAXY];
     int ndot;
     uint8_t da[8], db[8];
+    const double* drow;   // optional per-row coefficient of Y[0] (diagonal term), times dmul[row]
+    const double* dmul;
 };
 
 __device__ __forceinline__ double slot_coef(const PatDev& P, int64_t s) {
@@ -875,6 +877,10 @@ __global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : 5) : 3) spmm_tiled
                             ops[j] = make_double2(0.0, 0.0);
                         }
                     }
+                    if (E.drow != nullptr) {
+                        const double dc = __ldg(E.drow + row) * (E.dmul != nullptr ? __ldg(E.dmul + row) : 1.0);
+                        o = axpy2(dc, ops[0], o);
+                    }
                     if (VEC == 1) o.y = 0.0;
                     ops[SP_NY] = o;
 #pragma unroll
@@ -932,7 +938,7 @@ void sp_launch(const SpDev& a0, const EpiDev& E, double* ws, double* dots, cudaS
 
 template <int G, int VEC>
 void sp_dispatch_epi(const SpDev& a, const EpiDev& E, double* ws, double* dots, cudaStream_t st) {
-    const bool plain = E.ny == 0 && E.nz == 0 && E.ndot == 0 && a.out != nullptr;
+    const bool plain = E.ny == 0 && E.nz == 0 && E.ndot == 0 && E.drow == nullptr && a.out != nullptr;
     const bool ghost = a.Xg != nullptr;
     if (plain) {
         if (ghost) sp_launch<G, VEC, 0, 1>(a, E, ws, dots, st);
@@ -952,6 +958,96 @@ __global__ void __launch_bounds__(NT) gather_rows_kernel(const int32_t* __restri
         const int q = (int)(k - i * h2);
         st2(out + 2 * k, ld2(X + 2 * ((int64_t)__ldg(idx + i) * h2 + q)));
     }
+}
+
+// ---------------------------------------------------------------------------
+// CG half-step of the ADMM stage for diagonal constraints (admm.py:65/45)
+// ---------------------------------------------------------------------------
+
+struct DiagCg {
+    int64_t n;
+    int ld;
+    const double* aval;
+    double rho, beta;
+    const double* r;      // p <- r + beta p first (NULL: p is read as is)
+    double* p;
+    const double* Wf;
+    double* Q;
+};
+
+// One operator application of the half-step system (admm.py:45):
+//   [p <- r + beta p]   y_c = a_c <p_c, Wf_c>   Q_c = rho (a_c y_c Wf_c + p_c)   dots[0] = <p, Q>
+// Rows stream through a block as one contiguous run of double2 units (as in
+// diag_constraint_flat_kernel); the row dot is folded in shared memory and
+// the units are finished from registers, so p and Wf are read once.
+__global__ void __launch_bounds__(NT) diag_cg_apply_kernel(DiagCg a, double* ws, double* dots_out) {
+    __shared__ double part[NT * DC_U];
+    __shared__ double coef[NT * DC_U];
+    const int h2 = a.ld >> 1;
+    const int rb = (NT * DC_U) / h2;
+    const int64_t nblk = (a.n + rb - 1) / rb;
+    double dacc[1] = {0.0};
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int64_t r0 = blk * rb;
+        const int nr = (int)min((int64_t)rb, a.n - r0);
+        const int units = nr * h2;
+        const int64_t base = r0 * (int64_t)h2;
+        double2 pv[DC_U], wv[DC_U];
+#pragma unroll
+        for (int u = 0; u < DC_U; ++u) {
+            const int e = threadIdx.x + u * NT;
+            if (e < units) {
+                const int64_t off = 2 * (base + e);
+                wv[u] = ld2(a.Wf + off);
+                if (a.r != nullptr) {
+                    const double2 rv = ld2cs(a.r + off);
+                    if (a.beta != 0.0) pv[u] = axpy2(a.beta, ld2cs(a.p + off), rv);
+                    else pv[u] = rv;
+                    st2(a.p + off, pv[u]);
+                } else {
+                    pv[u] = ld2cs(a.p + off);
+                }
+                part[e] = dot2(pv[u], wv[u]);
+            }
+        }
+        __syncthreads();
+        for (int rr = threadIdx.x; rr < nr; rr += NT) {
+            double sdot = 0.0;
+            for (int q = 0; q < h2; ++q) sdot += part[rr * h2 + q];
+            const double av = __ldg(a.aval + r0 + rr);
+            coef[rr] = a.rho * (av * (av * sdot));      // rho * a_c * y_c
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < DC_U; ++u) {
+            const int e = threadIdx.x + u * NT;
+            if (e < units) {
+                const double c = coef[e / h2];
+                double2 q;
+                q.x = fma(c, wv[u].x, a.rho * pv[u].x);
+                q.y = fma(c, wv[u].y, a.rho * pv[u].y);
+                st2(a.Q + 2 * (base + e), q);
+                dacc[0] += dot2(pv[u], q);
+            }
+        }
+        __syncthreads();
+    }
+    reduce_and_finish<1>(dacc, 1, ws, dots_out);
+}
+
+// CG update (admm.py:88-90): x_out = x_in + alpha p; r -= alpha Q; dots[0] = <r, r>.
+__global__ void __launch_bounds__(NT) cg_step_kernel(int64_t n2, double alpha, const double* x_in, double* x_out,
+                                                    const double* p, double* r, const double* Q, double* ws,
+                                                    double* dots_out) {
+    double dacc[1] = {0.0};
+    for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < n2; k += (int64_t)gridDim.x * NT) {
+        const int64_t off = 2 * k;
+        st2(x_out + off, axpy2(alpha, ld2cs(p + off), ld2cs(x_in + off)));
+        const double2 rv = axpy2(-alpha, ld2cs(Q + off), ld2cs(r + off));
+        st2(r + off, rv);
+        dacc[0] += dot2(rv, rv);
+    }
+    reduce_and_finish<1>(dacc, 1, ws, dots_out);
 }
 
 __global__ void __launch_bounds__(NT) gather_rows_scalar_kernel(const int32_t* __restrict__ idx, int64_t count, int ld,
@@ -1031,7 +1127,7 @@ int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alp
     P.nrows = S->nrows; P.indptr = S->indptr; P.indices = S->indices; P.cv = S->cv; P.c_coeff = S->c_coeff;
     P.at_ptr = S->at_ptr; P.at_con = S->at_con; P.at_val = S->at_val; P.w1 = S->w1; P.w2 = S->w2;
     EpiDev E;
-    E.ny = 0; E.nz = 0; E.ndot = 0;
+    E.ny = 0; E.nz = 0; E.ndot = 0; E.drow = nullptr; E.dmul = nullptr;
     for (int j = 0; j < CL_MAXY; ++j) { E.Y[j] = nullptr; E.Z[j] = nullptr; E.ycoef[j] = 0.0; }
     for (int j = 0; j < 8; ++j) { E.da[j] = 0; E.db[j] = 0; }
     if (epi != nullptr) {
@@ -1042,6 +1138,9 @@ int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alp
             if (ld > 1 && ((j < E.ny && !aligned16(E.Y[j])) || (j < E.nz && !aligned16(E.Z[j])))) return CL_EARG;
         }
         for (int j = 0; j < 8; ++j) { E.da[j] = epi->da[j]; E.db[j] = epi->db[j]; }
+        E.drow = epi->drow;
+        E.dmul = epi->dmul;
+        if (E.drow != nullptr && E.ny < 1) return CL_EARG;
     }
     if (ld > 1 && (!aligned16(X) || (out != nullptr && !aligned16(out)))) return CL_EARG;
     if (E.ndot > 0 && (dots_out == nullptr || ws == nullptr)) return CL_EARG;
@@ -1112,8 +1211,9 @@ int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alp
         return (int)cudaGetLastError();
     }
 
-    // fused-coefficient path (no scratch given, or an all-zero matrix); no ghost rows there
-    if (S->ghost != nullptr) return CL_EARG;
+    // fused-coefficient path (no scratch given, or an all-zero matrix); no ghost rows or
+    // diagonal epilogue term there
+    if (S->ghost != nullptr || E.drow != nullptr) return CL_EARG;
     const int64_t threads = P.nrows * G;
     const int grid = red_grid(threads);
     if (ld == 1) {
@@ -1239,6 +1339,35 @@ int cl_gather_rows(const int32_t* idx, int64_t count, int32_t ld, const double* 
     const int64_t total = count * (ld / 2);
     int64_t g = (total + NT - 1) / NT;
     gather_rows_kernel<<<(int)(g > NSM * 16 ? NSM * 16 : g), NT, 0, st>>>(idx, count, ld / 2, X, out);
+    return (int)cudaGetLastError();
+}
+
+int cl_diag_cg_apply(int64_t n, int32_t ld, const double* aval, double rho, double beta, const double* r, double* p,
+                     const double* Wf, double* Q, double* dots_out, double* ws, void* stream) {
+    if (n < 0 || ld < 2 || (ld & 1) || ld / 2 > NT * DC_U || aval == nullptr || p == nullptr || Wf == nullptr ||
+        Q == nullptr || dots_out == nullptr || ws == nullptr)
+        return CL_EARG;
+    if (!aligned16(p) || !aligned16(Wf) || !aligned16(Q) || (r != nullptr && !aligned16(r))) return CL_EARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (n == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double), st);
+    DiagCg d;
+    d.n = n; d.ld = ld; d.aval = aval; d.rho = rho; d.beta = beta; d.r = r; d.p = p; d.Wf = Wf; d.Q = Q;
+    const int rb = (NT * DC_U) / (ld / 2);
+    const int64_t nblk = (n + rb - 1) / rb;
+    const int grid = (int)(nblk > CL_RED_BLOCKS ? CL_RED_BLOCKS : nblk);
+    diag_cg_apply_kernel<<<grid, NT, 0, st>>>(d, ws, dots_out);
+    return (int)cudaGetLastError();
+}
+
+int cl_cg_step(int64_t N, double alpha, const double* x_in, double* x_out, const double* p, double* r,
+               const double* Q, double* dots_out, double* ws, void* stream) {
+    if (N < 0 || (N & 1) || x_in == nullptr || x_out == nullptr || p == nullptr || r == nullptr || Q == nullptr ||
+        dots_out == nullptr || ws == nullptr)
+        return CL_EARG;
+    if (!aligned16(x_in) || !aligned16(x_out) || !aligned16(p) || !aligned16(r) || !aligned16(Q)) return CL_EARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (N == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double), st);
+    cg_step_kernel<<<red_grid(N / 2), NT, 0, st>>>(N / 2, alpha, x_in, x_out, p, r, Q, ws, dots_out);
     return (int)cudaGetLastError();
 }
 

@@ -119,10 +119,13 @@ class Device:
         check(rc, "cl_lincomb")
 
     def spmm(self, pat, X, ld, alpha=1.0, out=None, Y=(), ycoef=(), Z=(), dots=None, at=0,
-             c_coeff=None, w1=None, w2=None, use_cv=True, use_at=True):
-        """out = alpha * S X + sum ycoef*Y over a device pattern (see linops.DevicePattern)."""
+             c_coeff=None, w1=None, w2=None, use_cv=True, use_at=True, drow=None, dmul=None):
+        """out = alpha * S X + sum ycoef*Y [+ diag(drow*dmul) Y[0]] over a device pattern
+        (see linops.DevicePattern)."""
         P = pat.struct(c_coeff=c_coeff, w1=w1, w2=w2, use_cv=use_cv, use_at=use_at)
         e = _lib.Epilogue()
+        e.drow = drow.data_ptr() if drow is not None else None
+        e.dmul = dmul.data_ptr() if dmul is not None else None
         e.ny = len(Y)
         for j, (t, c) in enumerate(zip(Y, ycoef)):
             e.Y[j] = t.data_ptr()
@@ -161,6 +164,20 @@ class Device:
                                          ptr(out1), ptr(X3), ptr(Y3), ptr(out2), self.sp)
         self.launches += 1
         check(rc, "cl_constraint_eval")
+
+    def diag_cg_apply(self, aval, ld, rho, p, Wf, Q, r=None, beta=0.0, at=0):
+        """[p <- r + beta p]; Q = rho (A*(A(p Wf^T)) Wf + p) for diagonal A; <p, Q> -> slab[at]."""
+        rc = self.lib.cl_diag_cg_apply(int(p.shape[0]), int(ld), ptr(aval), float(rho), float(beta), ptr(r),
+                                       ptr(p), ptr(Wf), ptr(Q), self.slot(at), ptr(self.ws), self.sp)
+        self.launches += 1
+        check(rc, "cl_diag_cg_apply")
+
+    def cg_step(self, alpha, x_in, x_out, p, r, Q, at=0):
+        """x_out = x_in + alpha p; r -= alpha Q; <r, r> -> slab[at]."""
+        rc = self.lib.cl_cg_step(int(r.numel()), float(alpha), ptr(x_in), ptr(x_out), ptr(p), ptr(r), ptr(Q),
+                                 self.slot(at), ptr(self.ws), self.sp)
+        self.launches += 1
+        check(rc, "cl_cg_step")
 
     def gather_rows(self, idx, X, out):
         """out[i] = X[idx[i]] (halo packing, shard.py)."""
