@@ -202,6 +202,59 @@ int cl_basis_project(const double* Q, int64_t ldq, int32_t k_cnt, int64_t n, con
 int cl_basis_subtract(const double* Q, int64_t ldq, int32_t k_cnt, int64_t n, const double* h,
                       double* v, void* stream);
 
+/* One ADMM step (admm.py:136 admm_step: U half-solve, V half-solve, dual
+ * ascent) for diagonal constraints, with every scalar decision of the
+ * reference (tolerance schedule, cg_solve's stop/curvature/finiteness
+ * tests, admm.py:65) taken in native host code between launches of the
+ * kernels above. Same launches in the same order as the Python host path,
+ * hence bit-identical iterates; values needed at the same decision point are
+ * read with one pinned copy + synchronize (3 per step when CG stops at once). */
+typedef struct {
+    int64_t n;                 /* rows = constraints */
+    int32_t ld;
+    const double* aval;        /* a_c */
+    const double* b;
+    const double* lam;         /* multiplier at the step start */
+    double* lam_new;           /* lam + rho (A(U_new V_new^T) - b) (dual ascent, out of place) */
+    double* ax;                /* A(U V^T): input when ax_valid, output A(U_new V_new^T) */
+    int32_t ax_valid;
+    double pnorm2_known;       /* ||A(UV^T)-b||^2 of the input state, or < 0 to recompute */
+    const double* U;
+    const double* V;
+    double* U_new;
+    double* V_new;
+    double* r;                 /* CG residual / direction / operator output, n x ld */
+    double* p;
+    double* Q;
+    double* rhs;               /* n x ld */
+    double* nlam;              /* m-vector scratch */
+    double* res;               /* m-vector scratch */
+    cl_pattern cpat;           /* C (cv values) */
+    double rho, scale, binf, rel_floor, primal_coeff;
+    int32_t cg_cap;
+    double* slab;              /* 16 device doubles for the step's reductions */
+    double* host;              /* 16 pinned host doubles */
+    double* ws;                /* reduction workspace (CL_WS_ALLOC doubles) */
+    void* stream;
+} cl_admm_diag_args;
+
+typedef struct {
+    int32_t it_u, it_v;
+    double res_u, res_v, eps_u, eps_v;
+    double pnorm2;             /* ||A(U_new V_new^T) - b||^2 */
+    int32_t hit_cap;
+    int32_t status;            /* 0 ok; 1 non-finite curvature; 2 non-positive curvature; 3 non-finite iterate */
+    int32_t bad_half;          /* 0: U half-solve, 1: V half-solve */
+    int32_t bad_is_new;        /* last iterate is U_new/V_new (1) or the input U/V (0) */
+    double pq_bad;
+    int32_t u_reused;          /* CG stopped at its start: the new U is the input U (U_new untouched) */
+    int32_t v_reused;
+    double objective;          /* <C, U V^T> of the new factors (admm.py:215) */
+    double lam_b;              /* lam_new . b */
+} cl_admm_step_stats;
+
+int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats* out);
+
 /* Library identity, for load checks. */
 const char* cl_version(void);
 int cl_device_ok(void);

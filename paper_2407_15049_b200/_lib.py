@@ -25,7 +25,7 @@ CL_DOT_PAIRS, CL_DOT_OUT_ALL, CL_DOT_FIRST_TWO = 0, 1, 2
 CL_EARG = 1001
 
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_diag_constraint_eval", "cl_sddmm",
-           "cl_gather_rows", "cl_diag_cg_apply", "cl_cg_step",
+           "cl_gather_rows", "cl_diag_cg_apply", "cl_cg_step", "cl_admm_step_diag",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
            "cl_version", "cl_device_ok")
 
@@ -62,6 +62,21 @@ class DiagUpdateArgs(ctypes.Structure):
                 ("nh", I32), ("H", P * CL_MAXIN), ("refresh", I32)]
 
 
+class AdmmDiagArgs(ctypes.Structure):
+    _fields_ = [("n", I64), ("ld", I32), ("aval", P), ("b", P), ("lam", P), ("lam_new", P), ("ax", P),
+                ("ax_valid", I32),
+                ("pnorm2_known", D), ("U", P), ("V", P), ("U_new", P), ("V_new", P),
+                ("r", P), ("p", P), ("Q", P), ("rhs", P), ("nlam", P), ("res", P),
+                ("cpat", Pattern), ("rho", D), ("scale", D), ("binf", D), ("rel_floor", D),
+                ("primal_coeff", D), ("cg_cap", I32), ("slab", P), ("host", P), ("ws", P), ("stream", P)]
+
+
+class AdmmStepStats(ctypes.Structure):
+    _fields_ = [("it_u", I32), ("it_v", I32), ("res_u", D), ("res_v", D), ("eps_u", D), ("eps_v", D),
+                ("pnorm2", D), ("hit_cap", I32), ("status", I32), ("bad_half", I32), ("bad_is_new", I32),
+                ("pq_bad", D), ("u_reused", I32), ("v_reused", I32), ("objective", D), ("lam_b", D)]
+
+
 _LIB = None
 _LOCK = threading.Lock()
 
@@ -78,6 +93,7 @@ def _declare(lib):
     lib.cl_diag_constraint_eval.argtypes = [I64, P, I32, P, P, P, P, P, P, P, P, P]
     lib.cl_diag_cg_apply.argtypes = [I64, I32, P, D, D, P, P, P, P, P, P, P]
     lib.cl_cg_step.argtypes = [I64, D, P, P, P, P, P, P, P, P]
+    lib.cl_admm_step_diag.argtypes = [ctypes.POINTER(AdmmDiagArgs), ctypes.POINTER(AdmmStepStats)]
     lib.cl_gather_rows.argtypes = [P, I64, I32, P, P, P]
     lib.cl_sddmm.argtypes = [I64, P, P, I32, P, P, P, P]
     lib.cl_diag_alm_update.argtypes = [ctypes.POINTER(DiagUpdateArgs), P, P, P]

@@ -12,6 +12,7 @@ assembles -scale*C - A*(lam) + rho*A*(b) inside the SpMM coefficients.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import time
 from collections import deque
@@ -296,10 +297,88 @@ def _resid(ops, ax, res, at):
     ops.dev.lincomb(res, [ax, ops.b], [1.0, -1.0], dots=[("out", "out")], at=at)
 
 
+NATIVE = True     # diagonal constraints, one device: run the step's control flow in C++
+
+
+def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, hs, pool):
+    """admm_step through cl_admm_step_diag: the same launches as the Python branch below,
+    with the scalar decisions taken in native code (bit-identical iterates)."""
+    from . import _lib
+    dev = ops.dev
+    p = ops.problem
+    n, ld = state.U.shape
+    a = _lib.AdmmDiagArgs()
+    a.n, a.ld = n, ld
+    a.aval, a.b, a.lam = ops.diag_aval.data_ptr(), ops.b.data_ptr(), state.dual.lam.data_ptr()
+    lam_new = hs.lam_spare if getattr(hs, "lam_spare", None) is not None else dev.empty(p.m)
+    a.lam_new = lam_new.data_ptr()
+    if state.ax is None:
+        ax = dev.empty(p.m)
+        a.ax_valid = 0
+    else:
+        ax = state.ax
+        a.ax_valid = 1
+    known = getattr(state, "pnorm2_ax", None) is state.ax and state.ax is not None
+    a.pnorm2_known = state.last_pnorm2 if known else -1.0
+    a.ax = ax.data_ptr()
+    U_new = pool.get() if pool else dev.empty(n, ld)
+    V_new = pool.get() if pool else dev.empty(n, ld)
+    rhs = pool.get() if pool else dev.empty(n, ld)
+    a.U, a.V, a.U_new, a.V_new = state.U.data_ptr(), state.V.data_ptr(), U_new.data_ptr(), V_new.data_ptr()
+    a.r, a.p, a.Q, a.rhs = hs.r.data_ptr(), hs.p.data_ptr(), hs.Q.data_ptr(), rhs.data_ptr()
+    nlam = hs.nlam
+    a.nlam, a.res = nlam.data_ptr(), hs.y.data_ptr()
+    a.cpat = ops.c_mat.cpat.struct(c_coeff=1.0)
+    a.rho, a.scale, a.binf = float(state.dual.rho), float(scale), float(p.b_norminf)
+    a.rel_floor, a.primal_coeff, a.cg_cap = float(cg_rel_floor), float(cg_primal_coeff), int(cg_cap)
+    a.slab = dev.slot(470).value
+    a.host = dev.host.data_ptr() + 8 * 470
+    a.ws = dev.ws.data_ptr()
+    a.stream = dev.stream.cuda_stream
+    st = _lib.AdmmStepStats()
+    rc = dev.lib.cl_admm_step_diag(ctypes.byref(a), ctypes.byref(st))
+    dev.launches += 8 + 3 * (st.it_u + st.it_v)
+    _lib.check(rc, "cl_admm_step_diag")
+    if st.status:
+        if st.bad_half == 0:
+            last = U_new if st.bad_is_new else state.U
+        else:
+            last = V_new if st.bad_is_new else state.V
+        if st.status == 2:
+            raise SpdViolationError(f"non-positive curvature {st.pq_bad:.3e} in CG (operator not SPD)")
+        raise DivergedError("CG iterate diverged" if st.status == 3 else "CG produced non-finite curvature",
+                            last_iterate=last)
+    if st.u_reused:                       # CG stopped at its start: the factor is unchanged
+        if pool:
+            pool.put(U_new)
+        U_new = state.U
+    if st.v_reused:
+        if pool:
+            pool.put(V_new)
+        V_new = state.V
+    state.set_factors(U=U_new)
+    state.set_factors(V=V_new)
+    state.ax = ax
+    state.last_pnorm2 = st.pnorm2
+    state.pnorm2_ax = ax
+    # the ascended multiplier was written out of place: swap buffers
+    old = state.dual.lam
+    state.dual.lam = lam_new
+    hs.lam_spare = old
+    state.step_obj = (st.objective, st.lam_b)
+    if pool:
+        pool.put(rhs)
+    return StepStats(st.it_u, st.it_v, st.res_u, st.res_v, bool(st.hit_cap))
+
+
 def admm_step(state: AdmmState, ops, *, scale=1.0, cg_cap=200, cg_rel_floor=1e-10,
               cg_primal_coeff=0.05, hs=None, pool=None) -> StepStats:
     """U half-solve, V half-solve, dual ascent (admm.py:136)."""
     dev = ops.dev
+    if NATIVE and ops.is_diag and dev.world == 1:
+        n, ld = state.U.shape
+        return _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff,
+                                 hs or HalfStep(ops, n, ld), pool)
     p = ops.problem
     dual = state.dual
     rho = dual.rho
@@ -406,6 +485,7 @@ def admm_run(state: AdmmState, ops, *, scale=1.0, eps=1e-5, gap_eps=None, min_st
             hit_deadline = True
             break
         U_prev, V_prev = state.U, state.V
+        state.step_obj = None
         stats = admm_step(state, ops, scale=scale, cg_cap=cg_cap, hs=hs, pool=pool)
         cg_total += stats.cg_iters_u + stats.cg_iters_v
         steps = step
@@ -413,7 +493,11 @@ def admm_run(state: AdmmState, ops, *, scale=1.0, eps=1e-5, gap_eps=None, min_st
         err1, p0 = pnorm / (1.0 + b1), pnorm / (1.0 + binf)
         obj = None
         if gap_eps is not None or recorder is not None:
-            obj, g3v = objective_and_gap()
+            if state.step_obj is not None:       # computed inside the native step (same kernels)
+                obj, lam_b = state.step_obj[0], -state.step_obj[1] / scale
+                g3v = abs(obj - lam_b) / (1.0 + abs(obj) + abs(lam_b))
+            else:
+                obj, g3v = objective_and_gap()
             g3 = g3v if gap_eps is not None else None
         if recorder is not None:
             recorder.record("admm", scale * obj, err1, max(stats.resid_u, stats.resid_v),
@@ -423,8 +507,10 @@ def admm_run(state: AdmmState, ops, *, scale=1.0, eps=1e-5, gap_eps=None, min_st
         if balance:
             dev.lincomb(None, [state.U, U_prev], [1.0, -1.0], dots=[("out", "out")], at=445)
             dev.lincomb(None, [state.V, V_prev], [1.0, -1.0], dots=[("out", "out")], at=446)
-        pool.put(U_prev)
-        pool.put(V_prev)
+        if U_prev is not state.U:
+            pool.put(U_prev)
+        if V_prev is not state.V:
+            pool.put(V_prev)
         if done:
             break
         if gap_eps is not None and p0 <= eps:
