@@ -251,9 +251,14 @@ typedef struct {
     int32_t v_reused;
     double objective;          /* <C, U V^T> of the new factors (admm.py:215) */
     double lam_b;              /* lam_new . b */
+    int32_t err_line;          /* diagnostics: admm_native.cu line of the first failing launch */
 } cl_admm_step_stats;
 
 int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats* out);
+
+/* L2 fetch granularity hint of the current device (cudaLimitMaxL2FetchGranularity, 0..128 bytes). */
+int cl_set_l2_fetch_granularity(int32_t bytes);
+int cl_get_l2_fetch_granularity(void);
 
 /* Library identity, for load checks. */
 const char* cl_version(void);

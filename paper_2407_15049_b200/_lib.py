@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libculorads.so")
+LIB_PATH = os.environ.get("CULORADS_LIB") or os.path.join(HERE, "libculorads.so")
 
 CL_MAXIN = 20
 CL_MAXDOT = 48
@@ -27,7 +27,7 @@ CL_EARG = 1001
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_diag_constraint_eval", "cl_sddmm",
            "cl_gather_rows", "cl_diag_cg_apply", "cl_cg_step", "cl_admm_step_diag",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
-           "cl_version", "cl_device_ok")
+           "cl_set_l2_fetch_granularity", "cl_get_l2_fetch_granularity", "cl_version", "cl_device_ok")
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64
@@ -74,7 +74,8 @@ class AdmmDiagArgs(ctypes.Structure):
 class AdmmStepStats(ctypes.Structure):
     _fields_ = [("it_u", I32), ("it_v", I32), ("res_u", D), ("res_v", D), ("eps_u", D), ("eps_v", D),
                 ("pnorm2", D), ("hit_cap", I32), ("status", I32), ("bad_half", I32), ("bad_is_new", I32),
-                ("pq_bad", D), ("u_reused", I32), ("v_reused", I32), ("objective", D), ("lam_b", D)]
+                ("pq_bad", D), ("u_reused", I32), ("v_reused", I32), ("objective", D), ("lam_b", D),
+                ("err_line", I32)]
 
 
 _LIB = None
@@ -99,6 +100,8 @@ def _declare(lib):
     lib.cl_diag_alm_update.argtypes = [ctypes.POINTER(DiagUpdateArgs), P, P, P]
     lib.cl_basis_project.argtypes = [P, I64, I32, I64, P, P, P, P]
     lib.cl_basis_subtract.argtypes = [P, I64, I32, I64, P, P, P]
+    lib.cl_set_l2_fetch_granularity.argtypes = [I32]
+    lib.cl_get_l2_fetch_granularity.argtypes = []
     lib.cl_version.restype = ctypes.c_char_p
     lib.cl_device_ok.restype = ctypes.c_int
     for name in EXPORTS:

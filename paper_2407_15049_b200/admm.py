@@ -338,7 +338,7 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
     st = _lib.AdmmStepStats()
     rc = dev.lib.cl_admm_step_diag(ctypes.byref(a), ctypes.byref(st))
     dev.launches += 8 + 3 * (st.it_u + st.it_v)
-    _lib.check(rc, "cl_admm_step_diag")
+    _lib.check(rc, f"cl_admm_step_diag (admm_native.cu:{st.err_line})")
     if st.status:
         if st.bad_half == 0:
             last = U_new if st.bad_is_new else state.U

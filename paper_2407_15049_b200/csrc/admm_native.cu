@@ -26,7 +26,16 @@ struct Ctx {
     cudaStream_t st;
     int rc;
     int64_t N;   // n * ld
+    int line;    // source line of the first failing call (diagnostics)
 };
+
+#define CL_TRY(c, expr)                 \
+    do {                                \
+        if (!(c).rc) {                  \
+            (c).rc = (expr);            \
+            if ((c).rc) (c).line = __LINE__; \
+        }                               \
+    } while (0)
 
 // Reduction slots inside the caller's slab. The values read together at one
 // decision point are contiguous, so each decision costs one synchronize.
@@ -40,6 +49,7 @@ bool fetch(Ctx& c, int lo, int cnt) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(c.st);
     if (e != cudaSuccess) {
         c.rc = (int)e;
+        c.line = __LINE__;
         return false;
     }
     return true;
@@ -64,7 +74,7 @@ void lincomb(Ctx& c, double* out, int nin, const double* const* in, const double
         L.da[0] = dot_out_out ? CL_OUT : 0;
         L.db[0] = dot_out_out ? CL_OUT : 0;
     }
-    c.rc = cl_lincomb(&L, N, dot_slot >= 0 ? c.a->slab + dot_slot : nullptr, c.a->ws, (void*)c.st);
+    CL_TRY(c, cl_lincomb(&L, N, dot_slot >= 0 ? c.a->slab + dot_slot : nullptr, c.a->ws, (void*)c.st));
 }
 
 void copy(Ctx& c, double* dst, const double* src) {
@@ -83,7 +93,7 @@ void selfdot(Ctx& c, const double* x, int slot) {
     L.in[0] = x;
     L.coef[0] = 0.0;
     L.ndot = 1;
-    c.rc = cl_lincomb(&L, c.N, c.a->slab + slot, c.a->ws, (void*)c.st);
+    CL_TRY(c, cl_lincomb(&L, c.N, c.a->slab + slot, c.a->ws, (void*)c.st));
 }
 
 // rhs = S_b Wf + rho Wf, S_b = -scale C + diag(a (rho b - lam))  (HalfStep.rhs, diagonal branch);
@@ -103,7 +113,7 @@ void rhs(Ctx& c, const double* Wf) {
     E.db[0] = CL_OUT;
     E.drow = a->nlam;
     E.dmul = a->aval;
-    c.rc = cl_pattern_spmm(&P, Wf, a->ld, -a->scale, &E, a->rhs, a->slab + S_RHS, a->ws, (void*)c.st);
+    CL_TRY(c, cl_pattern_spmm(&P, Wf, a->ld, -a->scale, &E, a->rhs, a->slab + S_RHS, a->ws, (void*)c.st));
 }
 
 // max(v, 1e-300) with Python semantics (v is kept unless 1e-300 > v; NaN stays NaN)
@@ -122,9 +132,8 @@ int half(Ctx& c, const double* x0, double* x, const double* Wf, double rel, int 
     *last_is_x = 0;
     *reused = 0;
     rhs(c, Wf);
-    if (!c.rc)
-        c.rc = cl_diag_cg_apply(a->n, a->ld, a->aval, a->rho, 0.0, nullptr, const_cast<double*>(x0), Wf, a->Q,
-                                a->slab + S_PQ, a->ws, (void*)c.st);
+    CL_TRY(c, cl_diag_cg_apply(a->n, a->ld, a->aval, a->rho, 0.0, nullptr, const_cast<double*>(x0), Wf, a->Q,
+                               a->slab + S_PQ, a->ws, (void*)c.st));
     {
         const double* in[2] = {a->rhs, a->Q};
         const double cf[2] = {1.0, -1.0};
@@ -145,9 +154,8 @@ int half(Ctx& c, const double* x0, double* x, const double* Wf, double rel, int 
     double beta = 0.0;
     const double* xs = x0;
     for (int k = 0; k < a->cg_cap; ++k) {
-        if (!c.rc)
-            c.rc = cl_diag_cg_apply(a->n, a->ld, a->aval, a->rho, beta, a->r, a->p, Wf, a->Q, a->slab + S_PQ, a->ws,
-                                    (void*)c.st);
+        CL_TRY(c, cl_diag_cg_apply(a->n, a->ld, a->aval, a->rho, beta, a->r, a->p, Wf, a->Q, a->slab + S_PQ,
+                                   a->ws, (void*)c.st));
         if (!fetch(c, S_PQ, 1)) return 0;
         const double pq = H(c, S_PQ);
         if (!isfinite(pq) || pq <= 0.0) {
@@ -157,7 +165,7 @@ int half(Ctx& c, const double* x0, double* x, const double* Wf, double rel, int 
             return isfinite(pq) ? 2 : 1;
         }
         const double alpha = qr / pq;
-        if (!c.rc) c.rc = cl_cg_step(c.N, alpha, xs, x, a->p, a->r, a->Q, a->slab + S_QN, a->ws, (void*)c.st);
+        CL_TRY(c, cl_cg_step(c.N, alpha, xs, x, a->p, a->r, a->Q, a->slab + S_QN, a->ws, (void*)c.st));
         xs = x;
         if (!fetch(c, S_QN, 1)) return 0;
         const double qn = H(c, S_QN);
@@ -181,19 +189,20 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
     c.a = a;
     c.st = reinterpret_cast<cudaStream_t>(a->stream);
     c.rc = 0;
+    c.line = 0;
     c.N = a->n * (int64_t)a->ld;
     memset(out, 0, sizeof(*out));
 
     // constraint values at the step start (AdmmState.constraint_values) and the primal measure
     if (!a->ax_valid)
-        c.rc = cl_diag_constraint_eval(a->n, a->aval, a->ld, a->U, a->V, nullptr, nullptr, a->ax, nullptr, nullptr,
-                                       nullptr, (void*)c.st);
+        CL_TRY(c, cl_diag_constraint_eval(a->n, a->aval, a->ld, a->U, a->V, nullptr, nullptr, a->ax, nullptr, nullptr,
+                                          nullptr, (void*)c.st));
     double pn2 = a->pnorm2_known;
     if (!(pn2 >= 0.0)) {
         const double* in[2] = {a->ax, a->b};
         const double cf[2] = {1.0, -1.0};
         lincomb(c, a->res, 2, in, cf, a->n, S_PM, true);
-        if (!fetch(c, S_PM, 1)) return c.rc;
+        if (!fetch(c, S_PM, 1)) { out->err_line = c.line; return c.rc; }
         pn2 = H(c, S_PM);
     }
     const double pmeas = sqrt(pn2) / (1.0 + a->binf);
@@ -211,7 +220,7 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
     int last_is_x = 0, reused = 0;
     double pqb = 0.0;
     int s = half(c, a->U, a->U_new, a->V, rel, -1, &out->eps_u, &out->it_u, &out->res_u, &last_is_x, &pqb, &reused);
-    if (c.rc) return c.rc;
+    if (c.rc) { out->err_line = c.line; return c.rc; }
     if (s) {
         out->status = s;
         out->bad_half = 0;
@@ -224,7 +233,7 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
     if (!reused) selfdot(c, a->U_new, S_XXU);
     s = half(c, a->V, a->V_new, Uc, rel, reused ? -1 : S_XXU, &out->eps_v, &out->it_v, &out->res_v, &last_is_x, &pqb,
              &reused);
-    if (c.rc) return c.rc;
+    if (c.rc) { out->err_line = c.line; return c.rc; }
     if (s == 4) {                      // U's iterate was not finite (checked one synchronize late)
         out->status = 3;
         out->bad_half = 0;
@@ -245,9 +254,8 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
     // dual ascent on the new constraint values (admm.py:165-166), written out of place into
     // lam_new so that a late-detected non-finite V leaves the multiplier untouched; then the
     // objective <C V, U> and lam_new . b that admm_run's gap test reads (admm.py:212-217)
-    if (!c.rc)
-        c.rc = cl_diag_constraint_eval(a->n, a->aval, a->ld, Uc, Vc, nullptr, nullptr, a->ax, nullptr, nullptr,
-                                       nullptr, (void*)c.st);
+    CL_TRY(c, cl_diag_constraint_eval(a->n, a->aval, a->ld, Uc, Vc, nullptr, nullptr, a->ax, nullptr, nullptr,
+                                      nullptr, (void*)c.st));
     {
         const double* in[2] = {a->ax, a->b};
         const double cf[2] = {1.0, -1.0};
@@ -268,7 +276,7 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
         E.ndot = 1;
         E.da[0] = CL_OUT;
         E.db[0] = 16;
-        c.rc = cl_pattern_spmm(&P, Vc, a->ld, 1.0, &E, nullptr, a->slab + S_OBJ, a->ws, (void*)c.st);
+        CL_TRY(c, cl_pattern_spmm(&P, Vc, a->ld, 1.0, &E, nullptr, a->slab + S_OBJ, a->ws, (void*)c.st));
     }
     if (!c.rc) {
         cl_lincomb_args L;
@@ -280,9 +288,9 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
         L.ndot = 1;
         L.da[0] = 0;
         L.db[0] = 1;
-        c.rc = cl_lincomb(&L, a->n, a->slab + S_LB, a->ws, (void*)c.st);
+        CL_TRY(c, cl_lincomb(&L, a->n, a->slab + S_LB, a->ws, (void*)c.st));
     }
-    if (!fetch(c, S_PN, 4)) return c.rc;
+    if (!fetch(c, S_PN, 4)) { out->err_line = c.line; return c.rc; }
     if (!out->v_reused && !isfinite(H(c, S_XXV))) {
         out->status = 3;
         out->bad_half = 1;
@@ -294,5 +302,6 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
     out->lam_b = H(c, S_LB);
     out->hit_cap = (out->it_u >= a->cg_cap && out->res_u > out->eps_u) ||
                    (out->it_v >= a->cg_cap && out->res_v > out->eps_v);
+    out->err_line = c.line;
     return c.rc;
 }

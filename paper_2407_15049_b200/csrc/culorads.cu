@@ -639,9 +639,16 @@ __global__ void __launch_bounds__(NT) basis_subtract_kernel(const double* __rest
 // global loads on the critical path (linops.py:122 spmm)
 // ---------------------------------------------------------------------------
 
+#ifndef SP_SMAX
 #define SP_SMAX 1024        // slots staged per tile (indices + values)
+#endif
 #define SP_PTRMAX 264       // row pointers per tile: TR + 1 + alignment slack, TR <= 256
+#ifndef SP_UNROLL
 #define SP_UNROLL 8         // gathers in flight per lane
+#endif
+#ifndef SP_MINB0
+#define SP_MINB0 4          // resident CTAs per SM the plain-epilogue variant is compiled for
+#endif
 #define SP_NY 2             // epilogue limits of the tiled path (else the row-group kernel)
 #define SP_NZ 3
 #define SP_ND 4
@@ -727,7 +734,7 @@ __device__ __forceinline__ void sp_issue(const SpDev& a, SpTile* T, int64_t (*me
 }
 
 template <int G, int VEC, int EPI, int GHOST>
-__global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : 5) : 3) spmm_tiled_kernel(SpDev a, EpiDev E, double* ws,
+__global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : 3) spmm_tiled_kernel(SpDev a, EpiDev E, double* ws,
                                                                                      double* dots_out) {
     constexpr int NG = NT / G;
     // epilogue operand set of the tiled path: Y0, Y1, out, Z0, Z1, Z2
@@ -1072,6 +1079,18 @@ extern "C" {
 
 const char* cl_version(void) { return "culorads-b200 0.1 sm_100a"; }
 
+int cl_set_l2_fetch_granularity(int32_t bytes) {
+    // L2 fetch granularity hint (0..128 bytes): random 208-byte factor-row gathers
+    // over-fetch with a coarse granularity
+    return (int)cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes);
+}
+
+int cl_get_l2_fetch_granularity(void) {
+    size_t v = 0;
+    if (cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity) != cudaSuccess) return -1;
+    return (int)v;
+}
+
 int cl_device_ok(void) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
@@ -1159,7 +1178,8 @@ int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alp
     // Tiled path: one value per slot -- the objective values (c_coeff folded
     // into alpha) or the coefficients assembled into S->scratch.
     const bool need_asm = P.at_ptr != nullptr && (P.w1 != nullptr || P.w2 != nullptr);
-    const bool tiled = (need_asm ? S->scratch != nullptr : P.cv != nullptr) && S->nnz >= 0 &&
+    // (an empty pattern needs no slot values: torch hands out NULL for 0-element tensors)
+    const bool tiled = ((need_asm ? S->scratch != nullptr : P.cv != nullptr) || S->nnz == 0) && S->nnz >= 0 &&
                        E.ny <= SP_NY && E.nz <= SP_NZ && E.ndot <= SP_ND &&
                        aligned16(S->indptr) && aligned16(S->indices) &&
                        (need_asm ? aligned16(S->scratch) : aligned16(P.cv));
