@@ -256,6 +256,60 @@ typedef struct {
 
 int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats* out);
 
+/* ALM inner solve (alm.py:268 alm_inner) for diagonal constraints: the
+ * iteration of the Python host path (vector-free L-BFGS over a host Gram
+ * matrix, exact quartic line search, fused step/gradient/Gram-row update)
+ * with its scalar algebra in native code; same launches and operands, hence
+ * bit-identical iterates. The caller provides nbuf >= 2*memory+4 factor
+ * buffers (the L-BFGS pool). Per-iteration trace records (L, err1, gnorm,
+ * CLOCK_MONOTONIC seconds) go to rec[4*k..], gradient norms to gnorms[]. */
+#define CL_ALM_MAXMEM 8
+#define CL_ALM_MAXBUF (2 * CL_ALM_MAXMEM + 4)
+#define CL_ALM_REFRESH 50      /* alm.py:29 _REFRESH_EVERY */
+typedef struct {
+    int64_t n;
+    int32_t ld;
+    int32_t memory;            /* L-BFGS pairs kept (<= CL_ALM_MAXMEM) */
+    int32_t max_iter;
+    double tol;
+    double reduce_factor;      /* < 0: none */
+    double rho, scale, b1;     /* b1 = ||b||_1 (trace err1) */
+    const double* aval;
+    const double* b;
+    const double* lam;
+    double* R;                 /* updated in place */
+    double* CR;
+    double* CD;
+    double* ax;                /* AlmCore.ax (current constraint values on return: see ax_is_ax2) */
+    double* ax2;
+    double* q1;
+    double* q2;
+    double* wv;
+    const double* zero_g;
+    int32_t nbuf;
+    double* bufs[CL_ALM_MAXBUF];
+    cl_pattern cpat;
+    double* slab;              /* >= 64 + 7 + 2*CL_MAXIN device doubles */
+    double* host;              /* same count, pinned */
+    double* ws;
+    void* stream;
+    int32_t rec_cap;
+    double* rec;               /* 4 * rec_cap host doubles */
+    double* gnorms;            /* rec_cap host doubles */
+} cl_alm_inner_args;
+
+typedef struct {
+    int32_t iterations;
+    int32_t n_records;
+    int32_t n_gnorms;
+    int32_t hit_cap;
+    int32_t status;            /* 0 ok; 1 non-finite Lagrangian at start; 2 diverged inside */
+    int32_t ax_is_ax2;
+    int32_t err_line;
+} cl_alm_inner_stats;
+
+int cl_alm_inner_diag(const cl_alm_inner_args* a, cl_alm_inner_stats* out);
+
 /* L2 fetch granularity hint of the current device (cudaLimitMaxL2FetchGranularity, 0..128 bytes). */
 int cl_set_l2_fetch_granularity(int32_t bytes);
 int cl_get_l2_fetch_granularity(void);

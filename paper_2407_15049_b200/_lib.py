@@ -25,7 +25,7 @@ CL_DOT_PAIRS, CL_DOT_OUT_ALL, CL_DOT_FIRST_TWO = 0, 1, 2
 CL_EARG = 1001
 
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_diag_constraint_eval", "cl_sddmm",
-           "cl_gather_rows", "cl_diag_cg_apply", "cl_cg_step", "cl_admm_step_diag",
+           "cl_gather_rows", "cl_diag_cg_apply", "cl_cg_step", "cl_admm_step_diag", "cl_alm_inner_diag",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
            "cl_set_l2_fetch_granularity", "cl_get_l2_fetch_granularity", "cl_version", "cl_device_ok")
 
@@ -78,6 +78,23 @@ class AdmmStepStats(ctypes.Structure):
                 ("err_line", I32)]
 
 
+CL_ALM_MAXMEM = 8
+CL_ALM_MAXBUF = 2 * CL_ALM_MAXMEM + 4
+
+
+class AlmInnerArgs(ctypes.Structure):
+    _fields_ = [("n", I64), ("ld", I32), ("memory", I32), ("max_iter", I32), ("tol", D), ("reduce_factor", D),
+                ("rho", D), ("scale", D), ("b1", D), ("aval", P), ("b", P), ("lam", P), ("R", P), ("CR", P),
+                ("CD", P), ("ax", P), ("ax2", P), ("q1", P), ("q2", P), ("wv", P), ("zero_g", P),
+                ("nbuf", I32), ("bufs", P * CL_ALM_MAXBUF), ("cpat", Pattern), ("slab", P), ("host", P),
+                ("ws", P), ("stream", P), ("rec_cap", I32), ("rec", P), ("gnorms", P)]
+
+
+class AlmInnerStats(ctypes.Structure):
+    _fields_ = [("iterations", I32), ("n_records", I32), ("n_gnorms", I32), ("hit_cap", I32), ("status", I32),
+                ("ax_is_ax2", I32), ("err_line", I32)]
+
+
 _LIB = None
 _LOCK = threading.Lock()
 
@@ -95,6 +112,7 @@ def _declare(lib):
     lib.cl_diag_cg_apply.argtypes = [I64, I32, P, D, D, P, P, P, P, P, P, P]
     lib.cl_cg_step.argtypes = [I64, D, P, P, P, P, P, P, P, P]
     lib.cl_admm_step_diag.argtypes = [ctypes.POINTER(AdmmDiagArgs), ctypes.POINTER(AdmmStepStats)]
+    lib.cl_alm_inner_diag.argtypes = [ctypes.POINTER(AlmInnerArgs), ctypes.POINTER(AlmInnerStats)]
     lib.cl_gather_rows.argtypes = [P, I64, I32, P, P, P]
     lib.cl_sddmm.argtypes = [I64, P, P, I32, P, P, P, P]
     lib.cl_diag_alm_update.argtypes = [ctypes.POINTER(DiagUpdateArgs), P, P, P]

@@ -115,8 +115,7 @@ class HalfStep:
             if pq <= 0.0:
                 raise SpdViolationError(f"non-positive curvature {pq:.3e} in CG (operator not SPD)")
             alpha = qr / pq
-            dev.lincomb(x, [x, p], [1.0, alpha])
-            dev.lincomb(r, [r, Q], [1.0, -alpha], dots=[("out", "out")], at=A + 2)
+            dev.cg_step(alpha, x, x, p, r, Q, at=A + 2)       # x += alpha p; r -= alpha Q; <r, r>
             qn = float(dev.fetch(A + 3)[A + 2])
             rnorm = math.sqrt(qn)
             its = k + 1

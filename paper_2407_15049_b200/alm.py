@@ -22,6 +22,7 @@ Host/device synchronisation: two small scalar reads per inner iteration.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import time
 from collections import deque
@@ -494,9 +495,66 @@ class InnerResult:
     ax: object
 
 
+NATIVE = True     # diagonal constraints, one device: run the inner loop's control flow in C++
+
+
+def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory, recorder):
+    """alm.py:268 through cl_alm_inner_diag: the launches of ``_inner`` below with the
+    host-side scalar algebra in native code (bit-identical iterates)."""
+    from . import _lib
+    dev, ops = core.dev, core.ops
+    n, ld = core.n, core.ld
+    nbuf = 2 * memory + 4
+    bufs = getattr(core, "native_bufs", None)
+    if bufs is None or len(bufs) < nbuf:
+        bufs = core.native_bufs = [dev.empty(n, ld) for _ in range(nbuf)]
+    if core.zero_g is None:
+        core.zero_g = dev.zeros(n, ld)
+    a = _lib.AlmInnerArgs()
+    a.n, a.ld, a.memory, a.max_iter = n, ld, memory, max_iter
+    a.tol = float(tol)
+    a.reduce_factor = float(reduce_factor) if reduce_factor is not None else -1.0
+    a.rho, a.scale, a.b1 = float(rho), float(scale), float(ops.problem.b_norm1)
+    a.aval, a.b, a.lam = ops.diag_aval.data_ptr(), ops.b.data_ptr(), lam.data_ptr()
+    a.R, a.CR, a.CD = R.data_ptr(), core.CR.data_ptr(), core.CD.data_ptr()
+    a.ax, a.ax2 = core.ax.data_ptr(), core.ax2.data_ptr()
+    a.q1, a.q2, a.wv = core.q1.data_ptr(), core.q2.data_ptr(), core.wv.data_ptr()
+    a.zero_g = core.zero_g.data_ptr()
+    a.nbuf = nbuf
+    for j in range(nbuf):
+        a.bufs[j] = bufs[j].data_ptr()
+    a.cpat = ops.c_mat.cpat.struct(c_coeff=1.0)
+    a.slab, a.host = dev.slab.data_ptr(), dev.host.data_ptr()
+    a.ws, a.stream = dev.ws.data_ptr(), dev.stream.cuda_stream
+    cap = max_iter + 1
+    rec = np.empty(4 * cap)
+    gn = np.empty(cap)
+    a.rec_cap = cap
+    a.rec = rec.ctypes.data
+    a.gnorms = gn.ctypes.data
+    st = _lib.AlmInnerStats()
+    rc = dev.lib.cl_alm_inner_diag(ctypes.byref(a), ctypes.byref(st))
+    dev.launches += 2 + 5 * st.iterations
+    _lib.check(rc, f"cl_alm_inner_diag (alm_native.cu:{st.err_line})")
+    if st.ax_is_ax2:
+        core.ax, core.ax2 = core.ax2, core.ax
+    if recorder:
+        for k in range(st.n_records):
+            recorder.record("alm", float(rec[4 * k]), float(rec[4 * k + 1]), float(rec[4 * k + 2]), rho,
+                            None, t=float(rec[4 * k + 3]))
+    if st.status == 1:
+        raise DivergedError("non-finite Lagrangian at inner start", last_iterate=R)
+    if st.status == 2:
+        raise DivergedError("inner iteration diverged", last_iterate=R)
+    return InnerResult(R, st.iterations, [float(x) for x in gn[:st.n_gnorms]], bool(st.hit_cap), core.ax)
+
+
 def _inner(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory, recorder):
     """alm.py:268 on device buffers. R is updated in place."""
     dev, ops = core.dev, core.ops
+    if (NATIVE and ops.is_diag and dev.world == 1 and memory <= 8 and core.ld >= 2
+            and getattr(ops, "row_range", None) is None):
+        return _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory, recorder)
     b1 = ops.problem.b_norm1
     pool = core.pool
     hist = LbfgsHistory(memory, pool)
@@ -604,9 +662,9 @@ class _RankRecorder:
     def __init__(self, rec, r):
         self.rec, self.r = rec, r
 
-    def record(self, stage, obj, err1, metric, rho, rank):
+    def record(self, stage, obj, err1, metric, rho, rank, t=None):
         if self.rec is not None:
-            self.rec.record(stage, obj, err1, metric, rho, self.r if rank is None else rank)
+            self.rec.record(stage, obj, err1, metric, rho, self.r if rank is None else rank, t=t)
 
     def __bool__(self):
         return self.rec is not None

@@ -49,3 +49,23 @@ def delaunay_like(n, seed=0):
 
 
 GENERATORS = {"random_sparse": random_sparse, "delaunay_like": delaunay_like}
+
+
+def random_completion(n2, n1, m, rank=2, seed=0):
+    """Seeded matrix-completion instance (BASELINE configs[3] family): m distinct
+    observed entries (i, j) of an n2 x n1 rank-`rank` matrix M = A B^T."""
+    from .problem import ObservationSet
+    rng = np.random.default_rng(seed)
+    draw = int(m * 1.1) + 16
+    code = np.unique(rng.integers(0, n2, size=draw, dtype=np.int64) * n1
+                     + rng.integers(0, n1, size=draw, dtype=np.int64))
+    if code.size > m:
+        code = np.sort(rng.choice(code, size=m, replace=False))
+    i, j = code // n1, code % n1
+    A = rng.standard_normal((n2, rank))
+    B = rng.standard_normal((n1, rank))
+    vals = np.einsum("kr,kr->k", A[i], B[j])
+    return ObservationSet(n2, n1, i, j, vals)
+
+
+GENERATORS["random_completion"] = random_completion
