@@ -92,6 +92,9 @@ typedef struct {
     double* scratch;        /* nnz+16 doubles for assembled coefficients, or NULL */
     const double* ghost;    /* row-sharded solve: rows >= nown of X live here (halo), or NULL */
     int64_t nown;           /* rows of X owned by this rank (column j >= nown reads ghost[j-nown]) */
+    const double* w1g;      /* row-sharded solve: multipliers of constraints owned by other ranks */
+    const double* w2g;      /* (adjoint entry con >= mown reads w?g[con-mown]), or NULL */
+    int64_t mown;
 } cl_pattern;
 
 /* Pattern times factor with a fused epilogue (linops.py:122 spmm, and the
@@ -163,6 +166,14 @@ int cl_diag_cg_apply(int64_t n, int32_t ld, const double* aval, double rho, doub
                      const double* Wf, double* Q, double* dots_out, double* ws, void* stream);
 int cl_cg_step(int64_t N, double alpha, const double* x_in, double* x_out, const double* p, double* r,
                const double* Q, double* dots_out, double* ws, void* stream);
+
+/* cl_constraint_eval for a row block of a row-sharded solve: factor row
+ * index >= nown of operand k (X1, Y1, X2, Y2, X3, Y3) reads ghosts[k][row-nown]
+ * (the halo rows gathered from the other ranks). */
+int cl_constraint_eval_halo(int64_t m, const int64_t* indptr, const int32_t* pi, const int32_t* pj,
+                            const double* val, int32_t ld, const double* X1, const double* Y1, const double* X2,
+                            const double* Y2, double* out1, const double* X3, const double* Y3, double* out2,
+                            const double* const* ghosts, int64_t nown, void* stream);
 
 /* Gathered outer product at K positions (linops.py:49), x[k] = X[imap[k]]·Y[jmap[k]]. */
 int cl_sddmm(int64_t K, const int32_t* imap, const int32_t* jmap, int32_t ld,

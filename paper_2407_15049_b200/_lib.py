@@ -24,7 +24,8 @@ CL_OUT = 255
 CL_DOT_PAIRS, CL_DOT_OUT_ALL, CL_DOT_FIRST_TWO = 0, 1, 2
 CL_EARG = 1001
 
-EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_diag_constraint_eval", "cl_sddmm",
+EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint_eval_halo",
+           "cl_diag_constraint_eval", "cl_sddmm",
            "cl_gather_rows", "cl_diag_cg_apply", "cl_cg_step", "cl_admm_step_diag", "cl_alm_inner_diag",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
            "cl_set_l2_fetch_granularity", "cl_get_l2_fetch_granularity", "cl_version", "cl_device_ok")
@@ -44,7 +45,8 @@ class LincombArgs(ctypes.Structure):
 class Pattern(ctypes.Structure):
     _fields_ = [("nrows", I64), ("indptr", P), ("indices", P), ("cv", P), ("c_coeff", D),
                 ("at_ptr", P), ("at_con", P), ("at_val", P), ("w1", P), ("w2", P),
-                ("nnz", I64), ("scratch", P), ("ghost", P), ("nown", I64)]
+                ("nnz", I64), ("scratch", P), ("ghost", P), ("nown", I64),
+                ("w1g", P), ("w2g", P), ("mown", I64)]
 
 
 class Epilogue(ctypes.Structure):
@@ -108,6 +110,7 @@ def _declare(lib):
     lib.cl_pattern_spmm.argtypes = [ctypes.POINTER(Pattern), P, I32, D, ctypes.POINTER(Epilogue),
                                     P, P, P, P]
     lib.cl_constraint_eval.argtypes = [I64, P, P, P, P, I32, P, P, P, P, P, P, P, P, P]
+    lib.cl_constraint_eval_halo.argtypes = [I64, P, P, P, P, I32, P, P, P, P, P, P, P, P, P, I64, P]
     lib.cl_diag_constraint_eval.argtypes = [I64, P, I32, P, P, P, P, P, P, P, P, P]
     lib.cl_diag_cg_apply.argtypes = [I64, I32, P, D, D, P, P, P, P, P, P, P]
     lib.cl_cg_step.argtypes = [I64, D, P, P, P, P, P, P, P, P]

@@ -189,7 +189,14 @@ struct PatDev {
     const double* at_val;
     const double* w1;
     const double* w2;
+    const double* w1g;    // row-sharded solve: multipliers of constraints owned elsewhere,
+    const double* w2g;    // at_con >= mown reads w?g[at_con - mown]
+    int64_t mown;
 };
+
+__device__ __forceinline__ double wval(const double* w, const double* wg, int64_t mown, int32_t c) {
+    return (wg == nullptr || c < mown) ? __ldg(w + c) : __ldg(wg + (c - mown));
+}
 
 struct EpiDev {
     int ny;
@@ -210,12 +217,12 @@ __device__ __forceinline__ double slot_coef(const PatDev& P, int64_t s) {
         const int64_t u0 = __ldg(P.at_ptr + s), u1 = __ldg(P.at_ptr + s + 1);
         if (P.w1 != nullptr) {
             double t = 0.0;
-            for (int64_t u = u0; u < u1; ++u) t += __ldg(P.at_val + u) * __ldg(P.w1 + __ldg(P.at_con + u));
+            for (int64_t u = u0; u < u1; ++u) t += __ldg(P.at_val + u) * wval(P.w1, P.w1g, P.mown, __ldg(P.at_con + u));
             data += t;
         }
         if (P.w2 != nullptr) {
             double t = 0.0;
-            for (int64_t u = u0; u < u1; ++u) t += __ldg(P.at_val + u) * __ldg(P.w2 + __ldg(P.at_con + u));
+            for (int64_t u = u0; u < u1; ++u) t += __ldg(P.at_val + u) * wval(P.w2, P.w2g, P.mown, __ldg(P.at_con + u));
             data += t;
         }
     }
@@ -325,6 +332,30 @@ __device__ __forceinline__ double group_dot(const double* __restrict__ X, const 
     return p;
 }
 
+// Ghost rows of the row-sharded solve for the six operands of constraint_kernel
+// (row index >= nown reads g[k][row - nown]); nown < 0: no ghost rows.
+struct ConGhost {
+    const double* g[6];
+    int64_t nown;
+};
+
+__device__ __forceinline__ const double* grow(const double* X, const double* Xg, int64_t i, int64_t nown, int ld) {
+    return (nown < 0 || i < nown) ? X + i * ld : Xg + (i - nown) * ld;
+}
+
+template <int G, int VEC>
+__device__ __forceinline__ double group_dot_rows(const double* __restrict__ x, const double* __restrict__ y, int ld,
+                                                 int gl, unsigned gmask) {
+    double p = 0.0;
+    for (int col = gl * VEC; col < ld; col += G * VEC) {
+        if (VEC == 2) p += dot2(ld2(x + col), ld2(y + col));
+        else p += __ldg(x + col) * __ldg(y + col);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) p += __shfl_xor_sync(gmask, p, o);
+    return p;
+}
+
 template <int G, int VEC>
 __global__ void __launch_bounds__(NT) constraint_kernel(int64_t m, const int64_t* __restrict__ indptr,
                                                         const int32_t* __restrict__ pi,
@@ -332,21 +363,28 @@ __global__ void __launch_bounds__(NT) constraint_kernel(int64_t m, const int64_t
                                                         const double* __restrict__ val, int ld,
                                                         const double* X1, const double* Y1,
                                                         const double* X2, const double* Y2, double* out1,
-                                                        const double* X3, const double* Y3, double* out2) {
+                                                        const double* X3, const double* Y3, double* out2,
+                                                        ConGhost gh) {
     const int lane = threadIdx.x & 31;
     const int gl = lane % G;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - gl));
     const int64_t groups_total = (int64_t)gridDim.x * (NT / G);
+    const int64_t nw = gh.nown;
     for (int64_t c = ((int64_t)blockIdx.x * NT + threadIdx.x) / G; c < m; c += groups_total) {
         const int64_t t0 = __ldg(indptr + c), t1 = __ldg(indptr + c + 1);
         double a1 = 0.0, a2 = 0.0;
         for (int64_t t = t0; t < t1; ++t) {
             const int64_t i = __ldg(pi + t), j = __ldg(pj + t);
             const double v = __ldg(val + t);
-            double x = group_dot<G, VEC>(X1, Y1, i, j, ld, gl, gmask);
-            if (X2 != nullptr) x += group_dot<G, VEC>(X2, Y2, i, j, ld, gl, gmask);
+            double x = group_dot_rows<G, VEC>(grow(X1, gh.g[0], i, nw, ld), grow(Y1, gh.g[1], j, nw, ld), ld, gl,
+                                              gmask);
+            if (X2 != nullptr)
+                x += group_dot_rows<G, VEC>(grow(X2, gh.g[2], i, nw, ld), grow(Y2, gh.g[3], j, nw, ld), ld, gl,
+                                            gmask);
             a1 += v * x;
-            if (X3 != nullptr) a2 += v * group_dot<G, VEC>(X3, Y3, i, j, ld, gl, gmask);
+            if (X3 != nullptr)
+                a2 += v * group_dot_rows<G, VEC>(grow(X3, gh.g[4], i, nw, ld), grow(Y3, gh.g[5], j, nw, ld), ld, gl,
+                                                 gmask);
         }
         if (gl == 0) {
             out1[c] = a1;
@@ -1101,6 +1139,16 @@ int cl_device_ok(void) {
 
 int cl_lincomb(const cl_lincomb_args* args, int64_t N, double* dots_out, double* ws, void* stream) {
     if (args == nullptr || N < 0 || args->nin < 0 || args->nin > CL_MAXIN) return CL_EARG;
+    if (N == 0) {
+        // empty operands (e.g. a rank that owns no constraints): dots are zero; torch
+        // hands out NULL for 0-element tensors, so no pointer checks apply
+        int nd = args->ndot;
+        if (args->mode == CL_DOT_OUT_ALL && nd > 0) nd = args->nin + 1;
+        if (args->mode == CL_DOT_FIRST_TWO && nd > 0) nd = 2 * CL_MAXIN - 1;
+        if (nd > 0 && dots_out != nullptr)
+            return (int)cudaMemsetAsync(dots_out, 0, sizeof(double) * nd, reinterpret_cast<cudaStream_t>(stream));
+        return CL_OK;
+    }
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     LcDev d;
     d.nin = args->nin;
@@ -1145,6 +1193,7 @@ int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alp
     PatDev P;
     P.nrows = S->nrows; P.indptr = S->indptr; P.indices = S->indices; P.cv = S->cv; P.c_coeff = S->c_coeff;
     P.at_ptr = S->at_ptr; P.at_con = S->at_con; P.at_val = S->at_val; P.w1 = S->w1; P.w2 = S->w2;
+    P.w1g = S->w1g; P.w2g = S->w2g; P.mown = S->mown;
     EpiDev E;
     E.ny = 0; E.nz = 0; E.ndot = 0; E.drow = nullptr; E.dmul = nullptr;
     for (int j = 0; j < CL_MAXY; ++j) { E.Y[j] = nullptr; E.Z[j] = nullptr; E.ycoef[j] = 0.0; }
@@ -1251,9 +1300,26 @@ int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alp
     return (int)cudaGetLastError();
 }
 
+int cl_constraint_eval_halo(int64_t m, const int64_t* indptr, const int32_t* pi, const int32_t* pj,
+                            const double* val, int32_t ld, const double* X1, const double* Y1, const double* X2,
+                            const double* Y2, double* out1, const double* X3, const double* Y3, double* out2,
+                            const double* const* ghosts, int64_t nown, void* stream);
+
 int cl_constraint_eval(int64_t m, const int64_t* indptr, const int32_t* pi, const int32_t* pj, const double* val,
                        int32_t ld, const double* X1, const double* Y1, const double* X2, const double* Y2,
                        double* out1, const double* X3, const double* Y3, double* out2, void* stream) {
+    return cl_constraint_eval_halo(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2, nullptr, -1,
+                                   stream);
+}
+
+int cl_constraint_eval_halo(int64_t m, const int64_t* indptr, const int32_t* pi, const int32_t* pj,
+                            const double* val, int32_t ld, const double* X1, const double* Y1, const double* X2,
+                            const double* Y2, double* out1, const double* X3, const double* Y3, double* out2,
+                            const double* const* ghosts, int64_t nown, void* stream) {
+    ConGhost gh;
+    for (int k = 0; k < 6; ++k) gh.g[k] = ghosts != nullptr ? ghosts[k] : nullptr;
+    gh.nown = ghosts != nullptr ? nown : -1;
+    if (m == 0) return CL_OK;
     if (m < 0 || ld < 1 || (ld > 1 && (ld & 1)) || X1 == nullptr || Y1 == nullptr || out1 == nullptr) return CL_EARG;
     if ((X2 == nullptr) != (Y2 == nullptr) || (X3 == nullptr) != (Y3 == nullptr)) return CL_EARG;
     if (X3 != nullptr && out2 == nullptr) return CL_EARG;
@@ -1264,9 +1330,9 @@ int cl_constraint_eval(int64_t m, const int64_t* indptr, const int32_t* pi, cons
     int64_t g = (threads + NT - 1) / NT;
     const int grid = (int)(g > 65535 * 8 ? 65535 * 8 : g);
 #define CL_CK(GG)                                                                                           \
-    constraint_kernel<GG, 2><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2)
+    constraint_kernel<GG, 2><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2, gh)
     if (ld == 1) {
-        constraint_kernel<1, 1><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2);
+        constraint_kernel<1, 1><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2, gh);
     } else {
         switch (G) {
             case 1: CL_CK(1); break;
@@ -1284,6 +1350,7 @@ int cl_constraint_eval(int64_t m, const int64_t* indptr, const int32_t* pi, cons
 int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const double* X1, const double* Y1,
                             const double* X2, const double* Y2, double* out1, const double* X3, const double* Y3,
                             double* out2, void* stream) {
+    if (n == 0) return CL_OK;
     if (n < 0 || ld < 1 || (ld > 1 && (ld & 1)) || aval == nullptr || X1 == nullptr || Y1 == nullptr ||
         out1 == nullptr)
         return CL_EARG;

@@ -145,6 +145,14 @@ class Device:
             ghost = halo.exchange(X, ld, self.gather_rows)
             P.ghost = ghost.data_ptr()
             P.nown = halo.nown
+        mhalo = getattr(pat, "mhalo", None)
+        if mhalo is not None and (w1 is not None or w2 is not None) and P.at_ptr:
+            # multipliers of constraints owned by other ranks (row-sharded solve)
+            if w1 is not None:
+                P.w1g = mhalo.exchange(w1, 1, self.gather_rows, slot=0).data_ptr()
+            if w2 is not None:
+                P.w2g = mhalo.exchange(w2, 1, self.gather_rows, slot=1).data_ptr()
+            P.mown = mhalo.nown
         rc = self.lib.cl_pattern_spmm(ctypes.byref(P), ptr(X), int(ld), float(alpha), ctypes.byref(e),
                                       ptr(out), self.slot(at) if nd else None,
                                       ptr(self.ws) if nd else None, self.sp)
@@ -158,6 +166,27 @@ class Device:
                                                   self.sp)
             self.launches += 1
             check(rc, "cl_diag_constraint_eval")
+            return
+        halo = getattr(con, "halo", None)
+        if halo is not None:
+            # remote factor rows of the owned constraints' positions, one halo per distinct operand
+            ops_ = [X1, Y1, X2, Y2, X3, Y3]
+            seen, ghosts = {}, []
+            for t in ops_:
+                if t is None:
+                    ghosts.append(None)
+                    continue
+                key = id(t)       # object identity: the same on every rank (data_ptr is 0 for empty tensors)
+                if key not in seen:
+                    seen[key] = halo.exchange(t, ld, self.gather_rows, slot=len(seen))
+                ghosts.append(seen[key])
+            garr = (ctypes.c_void_p * 6)(*[g.data_ptr() if g is not None else None for g in ghosts])
+            rc = self.lib.cl_constraint_eval_halo(int(con.m), ptr(con.indptr), ptr(con.pi), ptr(con.pj),
+                                                  ptr(con.val), int(ld), ptr(X1), ptr(Y1), ptr(X2), ptr(Y2),
+                                                  ptr(out1), ptr(X3), ptr(Y3), ptr(out2), garr, int(halo.nown),
+                                                  self.sp)
+            self.launches += 1
+            check(rc, "cl_constraint_eval_halo")
             return
         rc = self.lib.cl_constraint_eval(int(con.m), ptr(con.indptr), ptr(con.pi), ptr(con.pj),
                                          ptr(con.val), int(ld), ptr(X1), ptr(Y1), ptr(X2), ptr(Y2),

@@ -48,6 +48,7 @@ class DevicePattern:
 
     scratch: torch.Tensor | None = None   # assembled slot coefficients (lazy)
     halo: object = None                   # shard.HaloPlan of a row-sharded pattern
+    mhalo: object = None                  # shard.HaloPlan of the multipliers its adjoint rows read
 
     @property
     def nnz(self):
@@ -98,6 +99,7 @@ class ConstraintCSR:
     pj: torch.Tensor       # int32 col of the position
     val: torch.Tensor      # fp64
     diag_aval: torch.Tensor | None = None   # set when constraint c is a_c e_c e_c^T (row-local)
+    halo: object = None                      # shard.HaloPlan of the rows its positions reference
 
 
 PAD = 16   # elements readable past the logical end (bulk copies read 16-byte supersets)

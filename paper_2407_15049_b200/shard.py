@@ -64,68 +64,89 @@ def _all_gather_1d(t, world, group=None):
 
 
 def all_reduce_sum(t, group=None):
-    """In-place SUM all-reduce that also works for CUDA tensors on gloo."""
-    if t.is_cuda and not _nccl(group):
-        h = t.detach().cpu()
-        dist.all_reduce(h, group=group)
-        t.copy_(h)
-    else:
-        dist.all_reduce(t, group=group)
+    """In-place SUM over ranks, bit-identical on every rank and independent of the
+    collective algorithm: the per-rank partials are all-gathered and added in rank
+    order. (A backend's all-reduce may associate the sum differently on different
+    ranks for three or more ranks; the solver branches on these scalars, so every
+    rank must see the same bits.)"""
+    world = dist.get_world_size(group)
+    if world == 1:
+        return t
+    flat = t.reshape(-1)
+    parts = _all_gather_1d(flat, world, group)                 # (world, count)
+    acc = parts[0].clone()
+    for r in range(1, world):
+        acc += parts[r]
+    flat.copy_(acc)
     return t
 
 
 class HaloPlan:
-    """Publish/receive plan of one row-sharded symmetric pattern.
+    """Publish/receive plan of one contiguously partitioned index space (factor rows,
+    or renumbered constraints) of a row-sharded solve.
 
-    ``indptr`` (nown+1) and ``indices`` (global column ids) are the local CSR
-    rows [lo, hi) of a pattern; after construction ``local_indices`` holds
-    the remapped int32 column indices the kernels use.
+    Built from a symmetric pattern's local CSR rows (``indptr``, global
+    ``indices``): a row is published when it has a remote column. Or, with
+    ``publish`` given, from an explicit list of local indices to publish.
+    After construction ``local_indices`` holds the remapped int32 indices the
+    kernels use, and ``remap`` maps any other global ids the same way:
+    [0, nown) for owned ids, ``nown + r*maxb + t`` for the t-th published id
+    of rank r -- the position that id lands at in the halo buffer.
     """
 
-    def __init__(self, lo, hi, indptr, indices, bounds, rank, world, group=None):
+    def __init__(self, lo, hi, indptr, indices, bounds, rank, world, group=None, publish=None):
         self.lo, self.hi, self.rank, self.world, self.group = lo, hi, rank, world, group
         self.nown = nown = hi - lo
+        self.bounds = bounds
         dev = indices.device
         indices = indices.to(I64)
-        counts_row = (indptr[1:] - indptr[:-1]).to(I64)
-        rows = torch.repeat_interleave(torch.arange(nown, device=dev, dtype=I64), counts_row)
         own = (indices >= lo) & (indices < hi)
-        publish = torch.unique(rows[~own])                      # sorted local row ids
+        if publish is None:
+            counts_row = (indptr[1:] - indptr[:-1]).to(I64)      # symmetric-pattern rule
+            rows = torch.repeat_interleave(torch.arange(nown, device=dev, dtype=I64), counts_row)
+            publish = torch.unique(rows[~own])                  # sorted local row ids
+        else:
+            publish = torch.unique(publish.to(device=dev, dtype=I64))
         nb = torch.tensor([publish.numel()], dtype=I64, device=dev)
         counts = _all_gather_1d(nb, world, group).view(-1)
         self.counts = counts.cpu().tolist()
         self.maxb = maxb = max(1, max(self.counts))
         padded = torch.full((maxb,), -1, dtype=I64, device=dev)
         padded[:publish.numel()] = publish + lo
-        lists = _all_gather_1d(padded, world, group)             # (world, maxb) global ids, -1 padded
-        self.publish = publish.to(I32).contiguous()             # local rows this rank sends
-
-        remote = indices[~own]
-        bt = torch.tensor(bounds, dtype=I64, device=dev)
-        owner = torch.searchsorted(bt, remote, right=True) - 1
-        big = torch.iinfo(I64).max
-        keyed = torch.where(lists >= 0, lists, torch.full_like(lists, big))
-        # position of each remote column inside its owner's (sorted) publish list
-        pos = torch.empty_like(remote)
-        for r in range(world):
-            sel = owner == r
-            if bool(sel.any()):
-                pos[sel] = torch.searchsorted(keyed[r].contiguous(), remote[sel])
-        if remote.numel():
-            found = lists[owner, pos.clamp(max=maxb - 1)]
-            if not bool((found == remote).all()):
-                raise ValueError("pattern is not symmetric across the row blocks: a referenced "
-                                 "remote row is missing from its owner's publish list")
-        loc = indices - lo
-        loc[~own] = nown + owner * maxb + pos
+        self.lists = _all_gather_1d(padded, world, group)        # (world, maxb) global ids, -1 padded
+        self.publish = publish.to(I32).contiguous()             # local indices this rank sends
         if nown + world * maxb >= 2 ** 31:
-            raise ValueError("row block plus halo exceeds int32 column indices")
-        self.local_indices = loc.to(I32).contiguous()
+            raise ValueError("owned block plus halo exceeds int32 indices")
+        self.local_indices = self.remap(indices).to(I32).contiguous()
         self.halo_rows = world * maxb
         self._bufs = {}
 
-    def buffers(self, ld, like):
-        key = (ld, like.device)
+    def remap(self, ids):
+        """Global ids -> local/halo indices (int64); raises if a remote id is not published."""
+        ids = ids.to(I64)
+        lo, hi, maxb = self.lo, self.hi, self.maxb
+        own = (ids >= lo) & (ids < hi)
+        out = ids - lo
+        remote = ids[~own]
+        if remote.numel():
+            bt = torch.tensor(self.bounds, dtype=I64, device=ids.device)
+            owner = torch.searchsorted(bt, remote, right=True) - 1
+            lists = self.lists.to(ids.device)
+            keyed = torch.where(lists >= 0, lists, torch.full_like(lists, torch.iinfo(I64).max))
+            pos = torch.empty_like(remote)
+            for r in range(self.world):
+                sel = owner == r
+                if bool(sel.any()):
+                    pos[sel] = torch.searchsorted(keyed[r].contiguous(), remote[sel])
+            found = lists[owner, pos.clamp(max=maxb - 1)]
+            if not bool((found == remote).all()):
+                raise ValueError("a referenced remote index is missing from its owner's publish list "
+                                 "(pattern not symmetric across the blocks)")
+            out[~own] = self.nown + owner * maxb + pos
+        return out
+
+    def buffers(self, ld, like, slot=0):
+        key = (ld, like.device, slot)
         b = self._bufs.get(key)
         if b is None:
             send = torch.zeros((self.maxb, ld), dtype=like.dtype, device=like.device)
@@ -133,9 +154,10 @@ class HaloPlan:
             b = self._bufs[key] = (send, recv)
         return b
 
-    def exchange(self, X, ld, pack):
-        """Pack this rank's published rows of X and all-gather them; returns the halo buffer."""
-        send, recv = self.buffers(ld, X)
+    def exchange(self, X, ld, pack, slot=0):
+        """Pack this rank's published rows of X and all-gather them; returns the halo buffer
+        (one buffer per ``slot``, so several operands can be in flight at once)."""
+        send, recv = self.buffers(ld, X, slot)
         pack(self.publish, X.reshape(-1, ld), send)
         if self.world == 1:
             recv.copy_(send)
@@ -265,11 +287,11 @@ class ShardProblem:
         return self._nnz_a_full
 
 
-def slice_pattern(pat, lo, hi, bounds, rank, world, group, con_lo=None, halo=True):
+def slice_pattern(pat, lo, hi, bounds, rank, world, group, con_map=None, halo=True):
     """Rows [lo, hi) of a DevicePattern, columns remapped through a HaloPlan.
 
-    Adjoint rows keep their constraint coefficients; constraint ids are
-    shifted by ``con_lo`` (they must belong to this rank's constraints)."""
+    Adjoint rows keep their coefficients; constraint ids go through
+    ``con_map`` (global id -> local/halo multiplier index)."""
     from .linops import DevicePattern, padded
 
     ptr = pat.indptr
@@ -286,46 +308,105 @@ def slice_pattern(pat, lo, hi, bounds, rank, world, group, con_lo=None, halo=Tru
         ap = torch.zeros(s1 - s0 + 1 + 16, dtype=I64, device=ptr.device)
         ap[:s1 - s0 + 1] = pat.at_ptr[s0:s1 + 1] - a0
         at_ptr = ap[:s1 - s0 + 1]
-        con = pat.at_con[a0:a1].to(I64) - (con_lo if con_lo is not None else 0)
-        if con.numel() and (int(con.min()) < 0 or int(con.max()) >= hi - lo):
-            raise NotImplementedError("row-sharded solve needs each constraint owned by the rank "
-                                      "that owns its rows (diagonal constraints)")
-        at_con = padded(con.to(I32))
+        at_con = padded(con_map(pat.at_con[a0:a1].to(I64)).to(I32))
         at_val = padded(pat.at_val[a0:a1])
     out = DevicePattern(hi - lo, pad_ptr[:hi - lo + 1], padded(plan.local_indices), cv, at_ptr, at_con, at_val)
     out.halo = plan if (halo and world > 1 and sum(plan.counts) > 0) else None
-    return out
+    return out, plan
 
 
 def build_sharded_operators(p, rank, world, dev, group=None):
-    """Rank-local OperatorBundle of a diagonal-constraint problem (constraint c is
-    a_c e_c e_c^T, e.g. MaxCut): factor rows, C/Omega/Omega_A pattern rows and
-    constraints [lo, hi), remote columns through halo plans. Built from the
+    """Rank-local OperatorBundle of a row-sharded solve.
+
+    Rows [lo, hi) of the factors and of the C/Omega/Omega_A patterns live on
+    this rank. A constraint is owned by the rank of the smallest row among its
+    positions, and every position must touch an owned row (diagonal
+    constraints, matrix completion's symmetric pairs). Constraints are
+    renumbered so that each rank's owned constraints form a contiguous block.
+    Remote factor rows come through the Omega halo (constraint evaluation,
+    SpMM), and the multipliers of constraints owned elsewhere come through a
+    multiplier halo before each coefficient assembly. Built from the
     single-device operators (linops.build_operators), then sliced."""
     from .linops import (AdjointOperator, CompressedOperator, ConstraintCSR, ObjectiveMatrix,
-                         OperatorBundle, build_operators)
+                         OperatorBundle, build_operators, padded)
 
     full = build_operators(p, dev=dev)
-    if not full.is_diag:
-        raise NotImplementedError("row-sharded solve supports diagonal constraints (MaxCut family)")
+    tdev = full.b.device
     b = block_bounds(p.n, world)
     lo, hi = b[rank], b[rank + 1]
-    cpat = slice_pattern(full.c_mat.cpat, lo, hi, b, rank, world, group)
-    omega = slice_pattern(full.adj.omega, lo, hi, b, rank, world, group, con_lo=lo)
-    apat = slice_pattern(full.adj.apat, lo, hi, b, rank, world, group, con_lo=lo)
-    aval = full.diag_aval[lo:hi].clone()      # clone: slices of m-vectors must start 16-byte aligned
     fc = full.cop.con
-    con = ConstraintCSR(m=hi - lo, indptr=(fc.indptr[lo:hi + 1] - fc.indptr[lo]).contiguous(),
-                        colidx=fc.colidx[lo:hi], pi=fc.pi[lo:hi] - lo, pj=fc.pj[lo:hi] - lo,
-                        val=fc.val[lo:hi].clone(), diag_aval=aval)
+    m = p.m
+    bt = torch.tensor(b, dtype=I64, device=tdev)
+
+    # constraint ownership: the rank of one of its rows, alternating over the constraint's
+    # positions (c mod nnz) so that e.g. completion's (j, n1+i) pairs spread over both blocks
+    nnz_c = (fc.indptr[1:] - fc.indptr[:-1]).to(I64)
+    cid = torch.repeat_interleave(torch.arange(m, device=tdev, dtype=I64), nnz_c)
+    ar = torch.arange(m, device=tdev, dtype=I64)
+    pick = fc.indptr[:-1].to(I64) + torch.remainder(ar, nnz_c.clamp(min=1))
+    prow = fc.pi.to(I64)[pick.clamp(max=max(int(fc.pi.numel()) - 1, 0))] if fc.pi.numel() else ar
+    owner = torch.where(nnz_c > 0, torch.searchsorted(bt, prow, right=True) - 1, ar * world // max(m, 1))
+    counts = torch.bincount(owner, minlength=world)
+    bm = [0] + torch.cumsum(counts, 0).cpu().tolist()
+    # renumbering: owner-major, original order within an owner
+    order = torch.argsort(owner * m + torch.arange(m, device=tdev, dtype=I64))
+    new_id = torch.empty(m, dtype=I64, device=tdev)
+    new_id[order] = torch.arange(m, device=tdev, dtype=I64)
+    lo_m, hi_m = bm[rank], bm[rank + 1]
+    owned = order[lo_m:hi_m]                                   # global ids, increasing
+
+    # positions of owned constraints must touch an owned row
+    sel = owner[cid] == rank
+    pi_o, pj_o = fc.pi[sel].to(I64), fc.pj[sel].to(I64)
+    touch = ((pi_o >= lo) & (pi_o < hi)) | ((pj_o >= lo) & (pj_o < hi))
+    bad = torch.tensor([0 if bool(touch.all()) else 1], dtype=I64, device=tdev)
+    if int(_all_gather_1d(bad, world, group).sum()) > 0:        # every rank raises together (no hang)
+        raise NotImplementedError("row-sharded solve needs every position of a constraint to touch a row "
+                                  "of the owning rank")
+    # multiplier halo: owned constraints referenced from rows of other ranks
+    outside = ~(((pi_o >= lo) & (pi_o < hi)) & ((pj_o >= lo) & (pj_o < hi)))
+    pub = torch.unique(new_id[cid[sel][outside]] - lo_m)
+    om = full.adj.omega
+    s0, s1 = int(om.indptr[lo]), int(om.indptr[hi])
+    a0, a1 = int(om.at_ptr[s0]), int(om.at_ptr[s1])
+    ref = new_id[om.at_con[a0:a1].to(I64)]
+    mplan = HaloPlan(lo_m, hi_m, None, ref, bm, rank, world, group, publish=pub)
+
+    def con_map(c):
+        return mplan.remap(new_id[c])
+
+    cpat, _ = slice_pattern(full.c_mat.cpat, lo, hi, b, rank, world, group)
+    omega, oplan = slice_pattern(om, lo, hi, b, rank, world, group, con_map=con_map)
+    apat, _ = slice_pattern(full.adj.apat, lo, hi, b, rank, world, group, con_map=con_map)
+    for pat in (omega, apat):
+        pat.mhalo = mplan if (world > 1 and sum(mplan.counts) > 0) else None
+
+    if full.is_diag:
+        aval = full.diag_aval[owned].clone()       # clone: m-vector slices must start 16-byte aligned
+    else:
+        aval = None
+    # owned constraint rows, positions remapped through the Omega row halo
+    starts = fc.indptr[owned]
+    lens = nnz_c[owned]
+    ptr = torch.zeros(hi_m - lo_m + 1, dtype=I64, device=tdev)
+    ptr[1:] = torch.cumsum(lens, 0)
+    gather = torch.repeat_interleave(starts - ptr[:-1], lens) + torch.arange(int(ptr[-1]), device=tdev,
+                                                                            dtype=I64)
+    con = ConstraintCSR(m=hi_m - lo_m, indptr=ptr, colidx=padded(fc.colidx[gather]),
+                        pi=oplan.remap(fc.pi[gather]).to(I32).contiguous(),
+                        pj=oplan.remap(fc.pj[gather]).to(I32).contiguous(),
+                        val=padded(fc.val[gather]), diag_aval=aval)
+    con.halo = oplan if world > 1 and not full.is_diag else None
     sp = ShardProblem(p, lo, hi)
-    cop = CompressedOperator(hi - lo, hi - lo, full.cop.ncols, full.cop.imap, full.cop.jmap,
+    sp.m = hi_m - lo_m
+    cop = CompressedOperator(hi_m - lo_m, hi - lo, full.cop.ncols, full.cop.imap, full.cop.jmap,
                              full.cop.col_slot, con, dev)
-    adj = AdjointOperator(hi - lo, hi - lo, full.adj.sup_i_host, full.adj.sup_j_host, omega, apat,
+    adj = AdjointOperator(hi_m - lo_m, hi - lo, full.adj.sup_i_host, full.adj.sup_j_host, omega, apat,
                           omega.cv, dev)
     ops = OperatorBundle(problem=sp, cop=cop, adj=adj, c_mat=ObjectiveMatrix(adj, cpat), dev=dev,
-                         b=full.b[lo:hi].clone(), diag_aval=aval, omega_size_ref=full.omega_size_ref)
+                         b=full.b[owned].clone(), diag_aval=aval, omega_size_ref=full.omega_size_ref)
     ops.row_range = (lo, hi)
+    ops.con_range = (lo_m, hi_m)
     del full
     return ops
 
