@@ -155,6 +155,22 @@ int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const dou
  * path for even ld and aligned rows, scalar otherwise). */
 int cl_gather_rows(const int32_t* idx, int64_t count, int32_t ld, const double* X, double* out, void* stream);
 
+/* Fused SpMM passes of the ADMM step for diagonal constraints (ld <= 64):
+ *   cl_diag_admm_cg_init: rhs = -scale C Wf + rho Wf + diag(a nlam) Wf (admm.py:52,
+ *     nlam = rho b - lam) and the initial CG residual r = rhs - Q(x0) with
+ *     Q(x0) = rho (a y Wf + x0), y = a <x0, Wf>  (admm.py:45/72) -- rhs and Q are
+ *     never stored; dots_out[0] = ||rhs||^2, dots_out[1] = ||r||^2.
+ *   cl_diag_admm_step_end: <C V, U> (admm.py:215), ax = A(U V^T), the residual
+ *     ax - b and the dual ascent lam_new = lam + rho (ax - b) (admm.py:165-166);
+ *     dots_out[0] = <C V, U>, [1] = ||ax - b||^2, [2] = lam_new . b.
+ * C carries cv values (and ghost rows in a row-sharded solve). */
+int cl_diag_admm_cg_init(const cl_pattern* C, const double* Wf, const double* x0, int32_t ld, double scale, double rho,
+                         const double* nlam, const double* aval, double* r, double* dots_out, double* ws,
+                         void* stream);
+int cl_diag_admm_step_end(const cl_pattern* C, const double* U, const double* V, int32_t ld, const double* aval,
+                          const double* b, const double* lam, double rho, double* ax, double* lam_new, double* dots_out,
+                          double* ws, void* stream);
+
 /* ADMM half-step CG for diagonal constraints (admm.py:65 cg_solve with the
  * operator of admm.py:45 subproblem_apply, A = diag(a)): one launch per
  * operator application and one per update, each factor operand read once.

@@ -370,14 +370,148 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
     return StepStats(st.it_u, st.it_v, st.res_u, st.res_v, bool(st.hit_cap))
 
 
+_FUSED_LD = 64     # admm_native.cu FUSED_LD: fused rhs/initial-residual and step-end passes
+
+
+def _admm_step_diag_py(state, ops, scale, cg_cap, rel_floor, coeff, hs, pool):
+    """Python-driven twin of cl_admm_step_diag (admm_native.cu): the same launches in the
+    same order with the same scalar decisions, so the iterates are bit-identical. Used for
+    row-sharded solves (the halo exchanges and scalar reductions live in Python) and as the
+    reference the native step is tested against."""
+    dev = ops.dev
+    p = ops.problem
+    n, ld = state.U.shape
+    rho = float(state.dual.rho)
+    lam = state.dual.lam
+    base = 470
+    S = lambda k: base + k  # noqa: E731  (slots of admm_native.cu)
+    fused = ld <= _FUSED_LD
+    cpat = ops.c_mat.cpat
+
+    def fetch(hi):
+        return dev.fetch(S(hi))
+
+    if state.ax is None:
+        ax = dev.empty(p.m)
+        dev.constraint_eval(ops.cop.con, ld, state.U, state.V, ax)
+    else:
+        ax = state.ax
+    known = getattr(state, "pnorm2_ax", None) is state.ax and state.ax is not None
+    if known:
+        pn2 = state.last_pnorm2
+    else:
+        dev.lincomb(hs.y, [ax, ops.b], [1.0, -1.0], dots=[("out", "out")], at=S(0))
+        pn2 = float(fetch(1)[S(0)])
+    pmeas = math.sqrt(pn2) / (1.0 + p.b_norminf)
+    y = coeff * pmeas
+    mn = y if y < 1e-2 else 1e-2
+    rel = mn if mn > rel_floor else rel_floor
+    dev.lincomb(hs.nlam, [ops.b, lam], [rho, -1.0])
+    rhs = pool.get() if pool else dev.empty(n, ld)
+
+    def half(x0, x, Wf, xx_prev):
+        """-> (status, eps, its, rnorm, last_is_x, pq, reused)"""
+        if fused:
+            dev.diag_admm_cg_init(cpat, Wf, x0, ld, scale, rho, hs.nlam, ops.diag_aval, hs.r, at=S(1))
+        else:
+            dev.spmm(cpat, Wf, ld, alpha=-scale, out=rhs, Y=[Wf], ycoef=[rho], c_coeff=1.0, drow=hs.nlam,
+                     dmul=ops.diag_aval, dots=[("out", "out")], at=S(1))
+            dev.diag_cg_apply(ops.diag_aval, ld, rho, x0, Wf, hs.Q, at=S(4))
+            dev.lincomb(hs.r, [rhs, hs.Q], [1.0, -1.0], dots=[("out", "out")], at=S(2))
+        h = fetch(4 if xx_prev else 3)
+        if xx_prev and not math.isfinite(float(h[S(3)])):
+            return 4, 0.0, 0, 0.0, 0, 0.0, 0
+        v = rel * math.sqrt(float(h[S(1)]))
+        eps = 1e-300 if 1e-300 > v else v
+        qr = float(h[S(2)])
+        rnorm = math.sqrt(qr)
+        if rnorm <= eps:
+            return 0, eps, 0, rnorm, 0, 0.0, 1
+        its, beta, xs = 0, 0.0, x0
+        for k in range(cg_cap):
+            dev.diag_cg_apply(ops.diag_aval, ld, rho, hs.p, Wf, hs.Q, r=hs.r, beta=beta, at=S(4))
+            pq = float(fetch(5)[S(4)])
+            if not math.isfinite(pq) or pq <= 0.0:
+                return (2 if math.isfinite(pq) else 1), eps, its, rnorm, int(xs is x), pq, 0
+            alpha = qr / pq
+            dev.cg_step(alpha, xs, x, hs.p, hs.r, hs.Q, at=S(5))
+            xs = x
+            qn = float(fetch(6)[S(5)])
+            rnorm = math.sqrt(qn)
+            its = k + 1
+            if rnorm <= eps:
+                break
+            beta = qn / qr
+            qr = qn
+        if its == 0:
+            dev.lincomb(x, [x0], [1.0])
+        return 0, eps, its, rnorm, 0, 0.0, 0
+
+    U_new = pool.get() if pool else dev.empty(n, ld)
+    V_new = pool.get() if pool else dev.empty(n, ld)
+    st_u = half(state.U, U_new, state.V, False)
+    if st_u[0]:
+        last = U_new if st_u[4] else state.U
+        if st_u[0] == 2:
+            raise SpdViolationError(f"non-positive curvature {st_u[5]:.3e} in CG (operator not SPD)")
+        raise DivergedError("CG produced non-finite curvature", last_iterate=last)
+    Uc = state.U if st_u[6] else U_new
+    if not st_u[6]:
+        dev.lincomb(None, [U_new], [0.0], dots=[(0, 0)], at=S(3))
+    st_v = half(state.V, V_new, Uc, not st_u[6])
+    if st_v[0] == 4:
+        raise DivergedError("CG iterate diverged", last_iterate=U_new)
+    if st_v[0]:
+        last = V_new if st_v[4] else state.V
+        if st_v[0] == 2:
+            raise SpdViolationError(f"non-positive curvature {st_v[5]:.3e} in CG (operator not SPD)")
+        raise DivergedError("CG produced non-finite curvature", last_iterate=last)
+    Vc = state.V if st_v[6] else V_new
+    if not st_v[6]:
+        dev.lincomb(None, [V_new], [0.0], dots=[(0, 0)], at=S(7))
+    lam_new = hs.lam_spare if getattr(hs, "lam_spare", None) is not None else dev.empty(p.m)
+    if fused:
+        dev.diag_admm_step_end(cpat, Uc, Vc, ld, ops.diag_aval, ops.b, lam, rho, ax, lam_new, at=S(10))
+        h = fetch(13)
+        vx, obj, pn2, lamb = h[S(7)], h[S(10)], h[S(11)], h[S(12)]
+    else:
+        dev.constraint_eval(ops.cop.con, ld, Uc, Vc, ax)
+        dev.lincomb(hs.y, [ax, ops.b], [1.0, -1.0], dots=[("out", "out")], at=S(6))
+        dev.lincomb(lam_new, [lam, hs.y], [1.0, rho])
+        dev.spmm(cpat, Vc, ld, out=None, Z=[Uc], dots=[("out", ("z", 0))], at=S(8), c_coeff=1.0)
+        dev.lincomb(None, [lam_new, ops.b], [0.0, 0.0], dots=[(0, 1)], at=S(9))
+        h = fetch(10)
+        vx, pn2, obj, lamb = h[S(7)], h[S(6)], h[S(8)], h[S(9)]
+    if not st_v[6] and not math.isfinite(float(vx)):
+        raise DivergedError("CG iterate diverged", last_iterate=V_new)
+    if st_u[6] and pool:
+        pool.put(U_new)
+    if st_v[6] and pool:
+        pool.put(V_new)
+    state.set_factors(U=Uc)
+    state.set_factors(V=Vc)
+    state.ax = ax
+    state.last_pnorm2 = float(pn2)
+    state.pnorm2_ax = ax
+    hs.lam_spare = lam
+    state.dual.lam = lam_new
+    state.step_obj = (float(obj), float(lamb))
+    if pool:
+        pool.put(rhs)
+    hit_cap = (st_u[2] >= cg_cap and st_u[3] > st_u[1]) or (st_v[2] >= cg_cap and st_v[3] > st_v[1])
+    return StepStats(st_u[2], st_v[2], st_u[3], st_v[3], bool(hit_cap))
+
+
 def admm_step(state: AdmmState, ops, *, scale=1.0, cg_cap=200, cg_rel_floor=1e-10,
               cg_primal_coeff=0.05, hs=None, pool=None) -> StepStats:
     """U half-solve, V half-solve, dual ascent (admm.py:136)."""
     dev = ops.dev
-    if NATIVE and ops.is_diag and dev.world == 1:
+    if ops.is_diag:
         n, ld = state.U.shape
-        return _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff,
-                                 hs or HalfStep(ops, n, ld), pool)
+        hs = hs or HalfStep(ops, n, ld)
+        if NATIVE and dev.world == 1:
+            return _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, hs, pool)
+        return _admm_step_diag_py(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, hs, pool)
     p = ops.problem
     dual = state.dual
     rho = dual.rho

@@ -39,7 +39,11 @@ struct Ctx {
 
 // Reduction slots inside the caller's slab. The values read together at one
 // decision point are contiguous, so each decision costs one synchronize.
-enum { S_PM = 0, S_RHS = 1, S_R0 = 2, S_XXU = 3, S_PQ = 4, S_QN = 5, S_PN = 6, S_XXV = 7, S_OBJ = 8, S_LB = 9 };
+enum { S_PM = 0, S_RHS = 1, S_R0 = 2, S_XXU = 3, S_PQ = 4, S_QN = 5, S_PN = 6, S_XXV = 7, S_OBJ = 8, S_LB = 9,
+       S_E0 = 10 };   // S_E0..S_E0+2: the fused step-end dots (objective, ||ax-b||^2, lam_new.b)
+
+// ld <= FUSED_LD: the rhs + initial residual and the step end run as single fused SpMM passes
+constexpr int FUSED_LD = 64;
 
 // Copy slab[lo, lo+cnt) to the pinned host buffer and wait.
 bool fetch(Ctx& c, int lo, int cnt) {
@@ -131,10 +135,16 @@ int half(Ctx& c, const double* x0, double* x, const double* Wf, double rel, int 
     *its_out = 0;
     *last_is_x = 0;
     *reused = 0;
-    rhs(c, Wf);
-    CL_TRY(c, cl_diag_cg_apply(a->n, a->ld, a->aval, a->rho, 0.0, nullptr, const_cast<double*>(x0), Wf, a->Q,
-                               a->slab + S_PQ, a->ws, (void*)c.st));
-    {
+    if (a->ld <= FUSED_LD) {
+        // rhs (never stored), Q(x0) and r = rhs - Q(x0) in one pass over C's rows
+        cl_pattern P = a->cpat;
+        P.c_coeff = 1.0;
+        CL_TRY(c, cl_diag_admm_cg_init(&P, Wf, x0, a->ld, a->scale, a->rho, a->nlam, a->aval, a->r, a->slab + S_RHS,
+                                       a->ws, (void*)c.st));
+    } else {
+        rhs(c, Wf);
+        CL_TRY(c, cl_diag_cg_apply(a->n, a->ld, a->aval, a->rho, 0.0, nullptr, const_cast<double*>(x0), Wf, a->Q,
+                                   a->slab + S_PQ, a->ws, (void*)c.st));
         const double* in[2] = {a->rhs, a->Q};
         const double cf[2] = {1.0, -1.0};
         lincomb(c, a->r, 2, in, cf, c.N, S_R0, true);
@@ -254,52 +264,69 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
     // dual ascent on the new constraint values (admm.py:165-166), written out of place into
     // lam_new so that a late-detected non-finite V leaves the multiplier untouched; then the
     // objective <C V, U> and lam_new . b that admm_run's gap test reads (admm.py:212-217)
-    CL_TRY(c, cl_diag_constraint_eval(a->n, a->aval, a->ld, Uc, Vc, nullptr, nullptr, a->ax, nullptr, nullptr,
-                                      nullptr, (void*)c.st));
-    {
-        const double* in[2] = {a->ax, a->b};
-        const double cf[2] = {1.0, -1.0};
-        lincomb(c, a->res, 2, in, cf, a->n, S_PN, true);
-    }
-    {
-        const double* in[2] = {a->lam, a->res};
-        const double cf[2] = {1.0, a->rho};
-        lincomb(c, a->lam_new, 2, in, cf, a->n, -1, false);
-    }
-    if (!c.rc) {
+    if (a->ld <= FUSED_LD) {
         cl_pattern P = a->cpat;
         P.c_coeff = 1.0;
-        cl_epilogue E;
-        memset(&E, 0, sizeof(E));
-        E.nz = 1;
-        E.Z[0] = Uc;
-        E.ndot = 1;
-        E.da[0] = CL_OUT;
-        E.db[0] = 16;
-        CL_TRY(c, cl_pattern_spmm(&P, Vc, a->ld, 1.0, &E, nullptr, a->slab + S_OBJ, a->ws, (void*)c.st));
+        CL_TRY(c, cl_diag_admm_step_end(&P, Uc, Vc, a->ld, a->aval, a->b, a->lam, a->rho, a->ax, a->lam_new,
+                                        a->slab + S_E0, a->ws, (void*)c.st));
+        if (!fetch(c, S_XXV, S_E0 + 3 - S_XXV)) { out->err_line = c.line; return c.rc; }
+        if (!out->v_reused && !isfinite(H(c, S_XXV))) {
+            out->status = 3;
+            out->bad_half = 1;
+            out->bad_is_new = 1;
+            return CL_OK;
+        }
+        out->objective = H(c, S_E0);
+        out->pnorm2 = H(c, S_E0 + 1);
+        out->lam_b = H(c, S_E0 + 2);
+    } else {
+        CL_TRY(c, cl_diag_constraint_eval(a->n, a->aval, a->ld, Uc, Vc, nullptr, nullptr, a->ax, nullptr, nullptr,
+                                          nullptr, (void*)c.st));
+        {
+            const double* in[2] = {a->ax, a->b};
+            const double cf[2] = {1.0, -1.0};
+            lincomb(c, a->res, 2, in, cf, a->n, S_PN, true);
+        }
+        {
+            const double* in[2] = {a->lam, a->res};
+            const double cf[2] = {1.0, a->rho};
+            lincomb(c, a->lam_new, 2, in, cf, a->n, -1, false);
+        }
+        if (!c.rc) {
+            cl_pattern P = a->cpat;
+            P.c_coeff = 1.0;
+            cl_epilogue E;
+            memset(&E, 0, sizeof(E));
+            E.nz = 1;
+            E.Z[0] = Uc;
+            E.ndot = 1;
+            E.da[0] = CL_OUT;
+            E.db[0] = 16;
+            CL_TRY(c, cl_pattern_spmm(&P, Vc, a->ld, 1.0, &E, nullptr, a->slab + S_OBJ, a->ws, (void*)c.st));
+        }
+        if (!c.rc) {
+            cl_lincomb_args L;
+            memset(&L, 0, sizeof(L));
+            L.nin = 2;
+            L.mode = CL_DOT_PAIRS;
+            L.in[0] = a->lam_new;
+            L.in[1] = a->b;
+            L.ndot = 1;
+            L.da[0] = 0;
+            L.db[0] = 1;
+            CL_TRY(c, cl_lincomb(&L, a->n, a->slab + S_LB, a->ws, (void*)c.st));
+        }
+        if (!fetch(c, S_PN, 4)) { out->err_line = c.line; return c.rc; }
+        if (!out->v_reused && !isfinite(H(c, S_XXV))) {
+            out->status = 3;
+            out->bad_half = 1;
+            out->bad_is_new = 1;
+            return CL_OK;
+        }
+        out->pnorm2 = H(c, S_PN);
+        out->objective = H(c, S_OBJ);
+        out->lam_b = H(c, S_LB);
     }
-    if (!c.rc) {
-        cl_lincomb_args L;
-        memset(&L, 0, sizeof(L));
-        L.nin = 2;
-        L.mode = CL_DOT_PAIRS;
-        L.in[0] = a->lam_new;
-        L.in[1] = a->b;
-        L.ndot = 1;
-        L.da[0] = 0;
-        L.db[0] = 1;
-        CL_TRY(c, cl_lincomb(&L, a->n, a->slab + S_LB, a->ws, (void*)c.st));
-    }
-    if (!fetch(c, S_PN, 4)) { out->err_line = c.line; return c.rc; }
-    if (!out->v_reused && !isfinite(H(c, S_XXV))) {
-        out->status = 3;
-        out->bad_half = 1;
-        out->bad_is_new = 1;
-        return CL_OK;
-    }
-    out->pnorm2 = H(c, S_PN);
-    out->objective = H(c, S_OBJ);
-    out->lam_b = H(c, S_LB);
     out->hit_cap = (out->it_u >= a->cg_cap && out->res_u > out->eps_u) ||
                    (out->it_v >= a->cg_cap && out->res_v > out->eps_v);
     out->err_line = c.line;

@@ -11,6 +11,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include "culorads.h"
 
@@ -208,6 +209,13 @@ struct EpiDev {
     uint8_t da[8], db[8];
     const double* drow;   // optional per-row coefficient of Y[0] (diagonal term), times dmul[row]
     const double* dmul;
+    // diagonal-constraint ADMM epilogues (EPI 2: CG start, EPI 3: step end)
+    double rho;
+    double* rout;         // EPI 2: initial CG residual
+    const double* bvec;   // EPI 3: b
+    const double* lam;    // EPI 3: multiplier at the step start
+    double* axo;          // EPI 3: A(U V^T)
+    double* lamo;         // EPI 3: lam + rho (A(U V^T) - b)
 };
 
 __device__ __forceinline__ double slot_coef(const PatDev& P, int64_t s) {
@@ -904,6 +912,48 @@ __global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : 3) spm
                         }
                     }
                 }
+                if (EPI >= 2) {
+                    // Diagonal-constraint ADMM epilogues; the row is one column chunk (ld <= 2G),
+                    // every lane of the group takes part in the row dot <Z0_i, Y0_i>.
+                    const int64_t off = row * (int64_t)ld + col;
+                    const double2 zr = make_double2(0.0, 0.0);
+                    const double2 yv = active ? ld2cs(E.Y[0] + off) : zr;   // Wf (EPI 2) / V (EPI 3)
+                    const double2 zv = active ? ld2cs(E.Z[0] + off) : zr;   // x0 (EPI 2) / U (EPI 3)
+                    double pd = dot2(zv, yv);
+#pragma unroll
+                    for (int sh = G / 2; sh > 0; sh >>= 1) pd += __shfl_xor_sync(gmask, pd, sh);
+                    const double av = __ldg(E.dmul + row);
+                    double2 o = make_double2(a.alpha * acc.x, a.alpha * acc.y);
+                    if (EPI == 2) {
+                        // rhs = -scale C Wf + rho Wf + a (rho b - lam) Wf    (HalfStep.rhs, diagonal)
+                        o = axpy2(E.ycoef[0], yv, o);
+                        o = axpy2(__ldg(E.drow + row) * av, yv, o);
+                        // Q = rho (a y Wf + x0), y = a <x0, Wf>   (cl_diag_cg_apply);  r = rhs - Q
+                        const double cq = E.rho * (av * (av * pd));
+                        const double2 q = make_double2(fma(cq, yv.x, E.rho * zv.x), fma(cq, yv.y, E.rho * zv.y));
+                        double2 rr = axpy2(1.0, o, zr);
+                        rr = axpy2(-1.0, q, rr);
+                        if (active) {
+                            st2(E.rout + off, rr);
+                            dacc[0] += dot2(o, o);
+                            dacc[1] += dot2(rr, rr);
+                        }
+                    } else {
+                        // <C V, U> (objective), A(U V^T), residual, dual ascent, lam_new . b
+                        if (active) dacc[0] += dot2(o, zv);
+                        if (gl == 0) {
+                            const double ax = 0.0 + av * pd;
+                            const double bb = __ldg(E.bvec + row);
+                            const double res = fma(-1.0, bb, fma(1.0, ax, 0.0));
+                            const double ln = fma(E.rho, res, fma(1.0, __ldg(E.lam + row), 0.0));
+                            E.axo[row] = ax;
+                            E.lamo[row] = ln;
+                            dacc[1] += res * res;
+                            dacc[2] += ln * bb;
+                        }
+                    }
+                    continue;
+                }
                 if (!active) continue;
                 const int64_t off = row * (int64_t)ld + col;
                 double2 o = make_double2(a.alpha * acc.x, a.alpha * acc.y);
@@ -947,7 +997,7 @@ __global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : 3) spm
         }
         __syncthreads();
     }
-    if (EPI == 1 && E.ndot > 0) reduce_and_finish<SP_ND>(dacc, E.ndot, ws, dots_out);
+    if (EPI >= 1 && E.ndot > 0) reduce_and_finish<SP_ND>(dacc, E.ndot, ws, dots_out);
 }
 
 // Slot coefficients of a pattern with adjoint rows, assembled once per call
@@ -979,6 +1029,18 @@ void sp_launch(const SpDev& a0, const EpiDev& E, double* ws, double* dots, cudaS
     if (grid > CL_RED_BLOCKS) grid = CL_RED_BLOCKS;
     if ((int64_t)grid > a.ntiles) grid = (int)a.ntiles;
     spmm_tiled_kernel<G, VEC, EPI, GHOST><<<grid, NT, 0, st>>>(a, E, ws, dots);
+}
+
+template <int G, int VEC>
+void sp_dispatch_mode(int mode, const SpDev& a, const EpiDev& E, double* ws, double* dots, cudaStream_t st) {
+    const bool ghost = a.Xg != nullptr;
+    if (mode == 2) {
+        if (ghost) sp_launch<G, VEC, 2, 1>(a, E, ws, dots, st);
+        else sp_launch<G, VEC, 2, 0>(a, E, ws, dots, st);
+    } else {
+        if (ghost) sp_launch<G, VEC, 3, 1>(a, E, ws, dots, st);
+        else sp_launch<G, VEC, 3, 0>(a, E, ws, dots, st);
+    }
 }
 
 template <int G, int VEC>
@@ -1195,6 +1257,7 @@ int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alp
     P.at_ptr = S->at_ptr; P.at_con = S->at_con; P.at_val = S->at_val; P.w1 = S->w1; P.w2 = S->w2;
     P.w1g = S->w1g; P.w2g = S->w2g; P.mown = S->mown;
     EpiDev E;
+    memset(&E, 0, sizeof(E));
     E.ny = 0; E.nz = 0; E.ndot = 0; E.drow = nullptr; E.dmul = nullptr;
     for (int j = 0; j < CL_MAXY; ++j) { E.Y[j] = nullptr; E.Z[j] = nullptr; E.ycoef[j] = 0.0; }
     for (int j = 0; j < 8; ++j) { E.da[j] = 0; E.db[j] = 0; }
@@ -1456,6 +1519,70 @@ int cl_cg_step(int64_t N, double alpha, const double* x_in, double* x_out, const
     if (N == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double), st);
     cg_step_kernel<<<red_grid(N / 2), NT, 0, st>>>(N / 2, alpha, x_in, x_out, p, r, Q, ws, dots_out);
     return (int)cudaGetLastError();
+}
+
+// Shared setup of the fused diagonal-ADMM SpMM launches (C pattern with cv values).
+static int diag_admm_launch(int mode, const cl_pattern* S, const double* X, int32_t ld, double alpha, EpiDev& E,
+                            double* dots_out, double* ws, cudaStream_t st) {
+    if (S == nullptr || X == nullptr || ld < 2 || (ld & 1) || ld > 64 || dots_out == nullptr || ws == nullptr)
+        return CL_EARG;
+    if (S->at_ptr != nullptr && (S->w1 != nullptr || S->w2 != nullptr)) return CL_EARG;
+    if (!(S->cv != nullptr || S->nnz == 0) || !aligned16(S->indptr) || !aligned16(S->indices) || !aligned16(X))
+        return CL_EARG;
+    const int G = ld <= 2 ? 1 : ld <= 4 ? 2 : ld <= 8 ? 4 : ld <= 16 ? 8 : ld <= 32 ? 16 : 32;
+    SpDev a;
+    a.nrows = S->nrows; a.indptr = S->indptr; a.indices = S->indices; a.vals = S->cv; a.X = X; a.ld = ld;
+    a.out = nullptr; a.alpha = alpha * S->c_coeff;
+    a.Xg = S->ghost;
+    a.nown = S->ghost != nullptr ? (int32_t)S->nown : INT32_MAX;
+    const int NG = NT / G;
+    const double avg = S->nrows > 0 ? (double)S->nnz / (double)S->nrows : 1.0;
+    int rpg = (int)((0.5 * SP_SMAX) / ((avg > 1.0 ? avg : 1.0) * NG));
+    const int rpg_max = (SP_PTRMAX - 4) / NG;
+    if (rpg > rpg_max) rpg = rpg_max;
+    if (rpg < 1) rpg = 1;
+    a.tr = rpg * NG;
+    a.ntiles = 0;
+    if (S->nrows == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double) * E.ndot, st);
+    switch (G) {
+        case 1: sp_dispatch_mode<1, 2>(mode, a, E, ws, dots_out, st); break;
+        case 2: sp_dispatch_mode<2, 2>(mode, a, E, ws, dots_out, st); break;
+        case 4: sp_dispatch_mode<4, 2>(mode, a, E, ws, dots_out, st); break;
+        case 8: sp_dispatch_mode<8, 2>(mode, a, E, ws, dots_out, st); break;
+        case 16: sp_dispatch_mode<16, 2>(mode, a, E, ws, dots_out, st); break;
+        default: sp_dispatch_mode<32, 2>(mode, a, E, ws, dots_out, st); break;
+    }
+    return (int)cudaGetLastError();
+}
+
+int cl_diag_admm_cg_init(const cl_pattern* C, const double* Wf, const double* x0, int32_t ld, double scale, double rho,
+                         const double* nlam, const double* aval, double* r, double* dots_out, double* ws,
+                         void* stream) {
+    if (Wf == nullptr || x0 == nullptr || nlam == nullptr || aval == nullptr || r == nullptr) return CL_EARG;
+    if (!aligned16(Wf) || !aligned16(x0) || !aligned16(r)) return CL_EARG;
+    EpiDev E;
+    memset(&E, 0, sizeof(E));
+    E.ny = 1; E.Y[0] = Wf; E.ycoef[0] = rho;
+    E.nz = 1; E.Z[0] = x0;
+    E.ndot = 2;
+    E.drow = nlam; E.dmul = aval; E.rho = rho; E.rout = r;
+    return diag_admm_launch(2, C, Wf, ld, -scale, E, dots_out, ws, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cl_diag_admm_step_end(const cl_pattern* C, const double* U, const double* V, int32_t ld, const double* aval,
+                          const double* b, const double* lam, double rho, double* ax, double* lam_new, double* dots_out,
+                          double* ws, void* stream) {
+    if (U == nullptr || V == nullptr || aval == nullptr || b == nullptr || lam == nullptr || ax == nullptr ||
+        lam_new == nullptr)
+        return CL_EARG;
+    if (!aligned16(U) || !aligned16(V)) return CL_EARG;
+    EpiDev E;
+    memset(&E, 0, sizeof(E));
+    E.ny = 1; E.Y[0] = V; E.ycoef[0] = 0.0;
+    E.nz = 1; E.Z[0] = U;
+    E.ndot = 3;
+    E.dmul = aval; E.rho = rho; E.bvec = b; E.lam = lam; E.axo = ax; E.lamo = lam_new;
+    return diag_admm_launch(3, C, V, ld, 1.0, E, dots_out, ws, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int cl_sddmm(int64_t K, const int32_t* imap, const int32_t* jmap, int32_t ld, const double* X, const double* Y,

@@ -201,6 +201,30 @@ class Device:
         self.launches += 1
         check(rc, "cl_diag_cg_apply")
 
+    def _halo_struct(self, pat, X, ld):
+        P = pat.struct(c_coeff=1.0)
+        halo = getattr(pat, "halo", None)
+        if halo is not None:
+            P.ghost = halo.exchange(X, ld, self.gather_rows).data_ptr()
+            P.nown = halo.nown
+        return P
+
+    def diag_admm_cg_init(self, cpat, Wf, x0, ld, scale, rho, nlam, aval, r, at):
+        """Fused rhs + initial CG residual (cl_diag_admm_cg_init); ||rhs||^2, ||r||^2 -> slab[at:at+2]."""
+        P = self._halo_struct(cpat, Wf, ld)
+        rc = self.lib.cl_diag_admm_cg_init(ctypes.byref(P), ptr(Wf), ptr(x0), int(ld), float(scale), float(rho),
+                                           ptr(nlam), ptr(aval), ptr(r), self.slot(at), ptr(self.ws), self.sp)
+        self.launches += 1
+        check(rc, "cl_diag_admm_cg_init")
+
+    def diag_admm_step_end(self, cpat, U, V, ld, aval, b, lam, rho, ax, lam_new, at):
+        """Fused objective / A(UV^T) / residual / dual ascent (cl_diag_admm_step_end) -> slab[at:at+3]."""
+        P = self._halo_struct(cpat, V, ld)
+        rc = self.lib.cl_diag_admm_step_end(ctypes.byref(P), ptr(U), ptr(V), int(ld), ptr(aval), ptr(b), ptr(lam),
+                                            float(rho), ptr(ax), ptr(lam_new), self.slot(at), ptr(self.ws), self.sp)
+        self.launches += 1
+        check(rc, "cl_diag_admm_step_end")
+
     def cg_step(self, alpha, x_in, x_out, p, r, Q, at=0):
         """x_out = x_in + alpha p; r -= alpha Q; <r, r> -> slab[at]."""
         rc = self.lib.cl_cg_step(int(r.numel()), float(alpha), ptr(x_in), ptr(x_out), ptr(p), ptr(r), ptr(Q),
