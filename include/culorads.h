@@ -155,6 +155,17 @@ int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const dou
  * path for even ld and aligned rows, scalar otherwise). */
 int cl_gather_rows(const int32_t* idx, int64_t count, int32_t ld, const double* X, double* out, void* stream);
 
+/* Half-step operator (admm.py:45 subproblem_apply) for single-entry constraints
+ * (constraint c = a_c (e_i e_j^T + e_j e_i^T), or a_c e_i e_i^T; matrix completion,
+ * problem.py:410): one pass over Omega_A's rows,
+ *   out_i = rho (sum_{slots (i,j) of constraint c} a_c y_c Wf_j + W_i),
+ *   y_c = a_c (W_lo . Wf_hi + W_hi . Wf_lo),  (lo, hi) = (min, max)(i, j),
+ * i.e. A(W Wf^T) is recomputed per slot from the two gathered rows instead of a
+ * separate constraint pass + coefficient assembly; dots_out[0] = <W, out>. ld <= 64. */
+int cl_single_entry_apply(int64_t nrows, const int64_t* indptr, const int32_t* indices, const double* slot_a,
+                          int32_t ld, const double* W, const double* Wf, double rho, double* out, double* dots_out,
+                          double* ws, void* stream);
+
 /* Fused SpMM passes of the ADMM step for diagonal constraints (ld <= 64):
  *   cl_diag_admm_cg_init: rhs = -scale C Wf + rho Wf + diag(a nlam) Wf (admm.py:52,
  *     nlam = rho b - lam) and the initial CG residual r = rhs - Q(x0) with

@@ -27,7 +27,7 @@ CL_EARG = 1001
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint_eval_halo",
            "cl_diag_constraint_eval", "cl_sddmm",
            "cl_gather_rows", "cl_diag_cg_apply", "cl_cg_step", "cl_admm_step_diag", "cl_alm_inner_diag",
-           "cl_diag_admm_cg_init", "cl_diag_admm_step_end",
+           "cl_diag_admm_cg_init", "cl_diag_admm_step_end", "cl_single_entry_apply",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
            "cl_set_l2_fetch_granularity", "cl_get_l2_fetch_granularity", "cl_version", "cl_device_ok")
 
@@ -119,6 +119,7 @@ def _declare(lib):
     lib.cl_alm_inner_diag.argtypes = [ctypes.POINTER(AlmInnerArgs), ctypes.POINTER(AlmInnerStats)]
     lib.cl_diag_admm_cg_init.argtypes = [ctypes.POINTER(Pattern), P, P, I32, D, D, P, P, P, P, P, P]
     lib.cl_diag_admm_step_end.argtypes = [ctypes.POINTER(Pattern), P, P, I32, P, P, P, D, P, P, P, P, P]
+    lib.cl_single_entry_apply.argtypes = [I64, P, P, P, I32, P, P, D, P, P, P, P]
     lib.cl_gather_rows.argtypes = [P, I64, I32, P, P, P]
     lib.cl_sddmm.argtypes = [I64, P, P, I32, P, P, P, P]
     lib.cl_diag_alm_update.argtypes = [ctypes.POINTER(DiagUpdateArgs), P, P, P]

@@ -66,6 +66,12 @@ class HalfStep:
             # diagonal A: the whole operator is row-local, one streaming pass (cl_diag_cg_apply)
             dev.diag_cg_apply(ops.diag_aval, self.ld, rho, W, Wf, out, at=at if at is not None else 0)
             return out
+        apat = ops.adj.apat
+        if (apat.single_a is not None and apat.halo is None and self.ld <= 64
+                and (dot_with is None or dot_with is W)):
+            # single-entry constraints (matrix completion): A(W Wf^T) recomputed per slot, one pass
+            dev.single_entry_apply(apat, self.ld, W, Wf, rho, out, at=at if at is not None else 0)
+            return out
         dev.constraint_eval(ops.cop.con, self.ld, W, Wf, self.y)
         dots = [(("y", 0), "out")] if dot_with is not None else None
         dev.spmm(ops.adj.apat, Wf, self.ld, alpha=rho, out=out, Y=[W], ycoef=[rho], w1=self.y,

@@ -78,7 +78,9 @@ __device__ __forceinline__ void reduce_and_finish(const double (&acc)[ND], int n
 __device__ __forceinline__ double2 ld2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 __device__ __forceinline__ double2 ld2cs(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
-__device__ __forceinline__ double dot2(double2 a, double2 b) { return a.x * b.x + a.y * b.y; }
+// Explicit rounding (no compiler-chosen contraction): every kernel evaluates a 16-byte
+// dot the same way, so fused and unfused paths that read the same operands agree bit for bit.
+__device__ __forceinline__ double dot2(double2 a, double2 b) { return fma(a.y, b.y, __dmul_rn(a.x, b.x)); }
 __device__ __forceinline__ double2 axpy2(double a, double2 x, double2 y) {
     return make_double2(fma(a, x.x, y.x), fma(a, x.y, y.y));
 }
@@ -1056,6 +1058,75 @@ void sp_dispatch_epi(const SpDev& a, const EpiDev& E, double* ws, double* dots, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// single-entry constraints (constraint c = a_c (e_i e_j^T + e_j e_i^T), e.g. matrix
+// completion): the half-step operator of admm.py:45 in one pass over Omega_A
+// ---------------------------------------------------------------------------
+
+// out_i = rho (sum_{slots (i,j) of c} a_c y_c Wf_j + W_i),
+// y_c = a_c (W_lo . Wf_hi + W_hi . Wf_lo) with (lo, hi) = (min, max)(i, j) -- the same
+// association on both rows of c, so each constraint value is computed bit-identically
+// twice instead of being stored and re-read; dots[0] = <W, out>. One column chunk per
+// row (ld <= 2G): lanes share the slot indices by shuffles and reduce the dots.
+template <int G>
+__global__ void __launch_bounds__(NT) single_entry_apply_kernel(int64_t nrows, const int64_t* __restrict__ indptr,
+                                                                const int32_t* __restrict__ indices,
+                                                                const double* __restrict__ slot_a, int ld,
+                                                                const double* __restrict__ W,
+                                                                const double* __restrict__ Wf, double rho,
+                                                                double* __restrict__ out, double* ws,
+                                                                double* dots_out) {
+    double dacc[1] = {0.0};
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - gl));
+    const int64_t groups_total = (int64_t)gridDim.x * (NT / G);
+    const int col = gl * 2;
+    const bool active = col < ld;
+    const double2 zr = make_double2(0.0, 0.0);
+    for (int64_t row = ((int64_t)blockIdx.x * NT + threadIdx.x) / G; row < nrows; row += groups_total) {
+        const int64_t s0 = __ldg(indptr + row), s1 = __ldg(indptr + row + 1);
+        const double2 wi = active ? ld2(W + row * ld + col) : zr;
+        const double2 fi = active ? ld2(Wf + row * ld + col) : zr;
+        double2 acc = zr;
+        for (int64_t base = s0; base < s1; base += G) {
+            const int64_t s = base + gl;
+            int jj = 0;
+            double aa = 0.0;
+            if (s < s1) {
+                jj = __ldg(indices + s);
+                aa = __ldg(slot_a + s);
+            }
+            const int cnt = (int)min((int64_t)G, s1 - base);
+            for (int u = 0; u < cnt; ++u) {
+                const int j = __shfl_sync(gmask, jj, (lane - gl) + u);
+                const double av = __shfl_sync(gmask, aa, (lane - gl) + u);
+                const double2 wj = active ? ld2(W + (int64_t)j * ld + col) : zr;
+                const double2 fj = active ? ld2(Wf + (int64_t)j * ld + col) : zr;
+                const bool lo_is_i = row <= j;
+                double t1 = dot2(lo_is_i ? wi : wj, lo_is_i ? fj : fi);   // W_lo . Wf_hi
+                double t2 = dot2(lo_is_i ? wj : wi, lo_is_i ? fi : fj);   // W_hi . Wf_lo
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) {
+                    t1 += __shfl_xor_sync(gmask, t1, o);
+                    t2 += __shfl_xor_sync(gmask, t2, o);
+                }
+                const double y = 0.0 + av * (row == j ? t1 : t1 + t2);
+                const double coef = 0.0 + av * y;
+                acc.x = fma(coef, fj.x, acc.x);
+                acc.y = fma(coef, fj.y, acc.y);
+            }
+        }
+        if (active) {
+            double2 o = make_double2(rho * acc.x, rho * acc.y);
+            o = axpy2(rho, wi, o);
+            st2(out + row * ld + col, o);
+            dacc[0] += dot2(wi, o);
+        }
+    }
+    reduce_and_finish<1>(dacc, 1, ws, dots_out);
+}
+
 // Halo packing for the row-sharded solve: out[i, :] = X[idx[i], :].
 __global__ void __launch_bounds__(NT) gather_rows_kernel(const int32_t* __restrict__ idx, int64_t count, int h2,
                                                          const double* __restrict__ X, double* __restrict__ out) {
@@ -1583,6 +1654,28 @@ int cl_diag_admm_step_end(const cl_pattern* C, const double* U, const double* V,
     E.ndot = 3;
     E.dmul = aval; E.rho = rho; E.bvec = b; E.lam = lam; E.axo = ax; E.lamo = lam_new;
     return diag_admm_launch(3, C, V, ld, 1.0, E, dots_out, ws, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cl_single_entry_apply(int64_t nrows, const int64_t* indptr, const int32_t* indices, const double* slot_a,
+                          int32_t ld, const double* W, const double* Wf, double rho, double* out, double* dots_out,
+                          double* ws, void* stream) {
+    if (nrows < 0 || ld < 2 || (ld & 1) || ld > 64 || indptr == nullptr || W == nullptr || Wf == nullptr ||
+        out == nullptr || dots_out == nullptr || ws == nullptr)
+        return CL_EARG;
+    if (!aligned16(W) || !aligned16(Wf) || !aligned16(out)) return CL_EARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (nrows == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double), st);
+    const int G = ld <= 2 ? 1 : ld <= 4 ? 2 : ld <= 8 ? 4 : ld <= 16 ? 8 : ld <= 32 ? 16 : 32;
+    const int grid = red_grid(nrows * G);
+    switch (G) {
+        case 1: single_entry_apply_kernel<1><<<grid, NT, 0, st>>>(nrows, indptr, indices, slot_a, ld, W, Wf, rho, out, ws, dots_out); break;
+        case 2: single_entry_apply_kernel<2><<<grid, NT, 0, st>>>(nrows, indptr, indices, slot_a, ld, W, Wf, rho, out, ws, dots_out); break;
+        case 4: single_entry_apply_kernel<4><<<grid, NT, 0, st>>>(nrows, indptr, indices, slot_a, ld, W, Wf, rho, out, ws, dots_out); break;
+        case 8: single_entry_apply_kernel<8><<<grid, NT, 0, st>>>(nrows, indptr, indices, slot_a, ld, W, Wf, rho, out, ws, dots_out); break;
+        case 16: single_entry_apply_kernel<16><<<grid, NT, 0, st>>>(nrows, indptr, indices, slot_a, ld, W, Wf, rho, out, ws, dots_out); break;
+        default: single_entry_apply_kernel<32><<<grid, NT, 0, st>>>(nrows, indptr, indices, slot_a, ld, W, Wf, rho, out, ws, dots_out); break;
+    }
+    return (int)cudaGetLastError();
 }
 
 int cl_sddmm(int64_t K, const int32_t* imap, const int32_t* jmap, int32_t ld, const double* X, const double* Y,

@@ -225,6 +225,14 @@ class Device:
         self.launches += 1
         check(rc, "cl_diag_admm_step_end")
 
+    def single_entry_apply(self, apat, ld, W, Wf, rho, out, at=0):
+        """Fused half-step operator for single-entry constraints; <W, out> -> slab[at]."""
+        rc = self.lib.cl_single_entry_apply(int(apat.nrows), ptr(apat.indptr), ptr(apat.indices), ptr(apat.single_a),
+                                            int(ld), ptr(W), ptr(Wf), float(rho), ptr(out), self.slot(at),
+                                            ptr(self.ws), self.sp)
+        self.launches += 1
+        check(rc, "cl_single_entry_apply")
+
     def cg_step(self, alpha, x_in, x_out, p, r, Q, at=0):
         """x_out = x_in + alpha p; r -= alpha Q; <r, r> -> slab[at]."""
         rc = self.lib.cl_cg_step(int(r.numel()), float(alpha), ptr(x_in), ptr(x_out), ptr(p), ptr(r), ptr(Q),

@@ -49,6 +49,7 @@ class DevicePattern:
     scratch: torch.Tensor | None = None   # assembled slot coefficients (lazy)
     halo: object = None                   # shard.HaloPlan of a row-sharded pattern
     mhalo: object = None                  # shard.HaloPlan of the multipliers its adjoint rows read
+    single_a: torch.Tensor | None = None  # Omega_A of single-entry constraints: a_c per slot
 
     @property
     def nnz(self):
@@ -425,6 +426,24 @@ def build_operators(p: SdpProblem, dense_c=None, dev=None) -> OperatorBundle:
     cs = ccodes[o4]
     cpat = DevicePattern(n, _csr_ptr(cs // n, n), padded((cs % n).to(I32)), padded(cvals[o4]),
                          None, None, None)
+
+    # single-entry constraints (each A_c = a_c (e_i e_j^T + e_j e_i^T) or a_c e_i e_i^T, and no
+    # two constraints share a position): the ADMM operator fuses into one pass over Omega_A
+    # (cl_single_entry_apply). Matrix completion (problem.py:410) has this shape.
+    single = None
+    nnz_c = con.indptr[1:] - con.indptr[:-1]
+    apc = apat.at_ptr[1:] - apat.at_ptr[:-1]
+    if m and bool(((nnz_c == 1) | (nnz_c == 2)).all()) and bool((apc == 1).all()):
+        st = con.indptr[:-1]
+        pi0, pj0 = con.pi.to(I64)[st], con.pj.to(I64)[st]
+        two = nnz_c == 2
+        nxt = (st + 1).clamp(max=max(int(con.pi.numel()) - 1, 0))
+        pi1, pj1 = con.pi.to(I64)[nxt], con.pj.to(I64)[nxt]
+        ok1 = (~two) & (pi0 == pj0)
+        ok2 = two & (pi0 == pj1) & (pj0 == pi1) & (pi0 != pj0) & (con.val[st] == con.val[nxt])
+        if bool((ok1 | ok2).all()):
+            single = padded(apat.at_val[apat.at_ptr[:-1]].contiguous())
+    apat.single_a = single
 
     cop = CompressedOperator(m, n, K, imap.to(I32), jmap.to(I32), slot_a, con, dev)
     adj = AdjointOperator(m, n, sup_i.cpu().numpy(), sup_j.cpu().numpy(), omega, apat, cv, dev)
