@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-solver", action="store_true", help="skip the solver-level rates and the G1 solve")
     ap.add_argument("--n-g1", type=int, default=800)
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
+                    help="gloo: functional check of the N>1 path with ranks sharing one GPU (no timing value)")
     return ap.parse_args()
 
 
@@ -269,6 +271,15 @@ def run_reference(args, rank):
 # device arm
 # ---------------------------------------------------------------------------
 
+def _max_over_ranks(x):
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -276,9 +287,15 @@ def run_ours(args, rank, world, local_rank):
     from paper_2407_15049_b200 import alm, device, driver, graphs, linops, problem
     from paper_2407_15049_b200 import roofline as RL
 
+    if args.dist_backend == "gloo":
+        # functional check of the sharded path with several ranks sharing the visible GPU(s)
+        local_rank = local_rank % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     n = int(args.n)
     dev = device.default_device()
     halo_bytes = 0
@@ -327,7 +344,7 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             # the Lagrangian value / gradient-norm scalars combine across ranks
             red = dev.slab[alm.AlmCore.S_UPD:alm.AlmCore.S_UPD + 7].clone()
-            dist.all_reduce(red)
+            shard.all_reduce_sum(red)
         if ev is not None:
             ev[3].record(st)
 
@@ -358,9 +375,7 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         ms = t0.elapsed_time(t1) / K
     if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms = _max_over_ranks(ms)
     value = world * step_bytes / (ms * 1e-3) / 1e9
 
     # end to end through the reference-facing API with host buffers
@@ -389,9 +404,7 @@ def run_ours(args, rank, world, local_rank):
             torch.cuda.synchronize()
             e_ms = (time.perf_counter() - te) * 1e3 / K
         if world > 1:
-            tt = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e_ms = float(tt.item())
+            e_ms = _max_over_ranks(e_ms)
         e2e = {"value": world * step_bytes / (e_ms * 1e-3) / 1e9, "unit": UNIT,
                "ms_per_step": e_ms, "h2d_bytes_per_step": int(R_host.nbytes + lam_host.nbytes),
                "d2h_bytes_per_step": int(n * r * 8),
