@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--n", type=float, default=1e7)
+    ap.add_argument("--nrows", dest="n", type=float, default=1e7, help="rows (vertices) per GPU")
     ap.add_argument("--deg", type=float, default=6.0)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
