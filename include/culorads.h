@@ -348,6 +348,34 @@ typedef struct {
 
 int cl_alm_inner_diag(const cl_alm_inner_args* a, cl_alm_inner_stats* out);
 
+/* Slot values of a pattern (c_coeff cv + adjoint rows against w1/w2, linops.py:100
+ * assemble) written to vals[nnz] -- the pre-pass cl_pattern_spmm runs internally. */
+int cl_pattern_assemble(const cl_pattern* S, double* vals, void* stream);
+
+/* Lanczos loop of spectral.py:28 with native control flow. S is a pattern with
+ * assembled slot values (cv, no adjoint rows) applied to vectors (ld = 1); Q holds
+ * k_max basis rows of ldq doubles, Q[0] the start vector. Fills alphas[0..k) and
+ * betas[0..k-1) (host arrays) and returns k (the basis size) in *k_out. */
+typedef struct {
+    int64_t n;
+    int32_t k_max;
+    double breakdown;
+    double* Q;
+    int64_t ldq;
+    double* u;
+    double* r;
+    double* h;                 /* k_max device doubles (Gram projections) */
+    cl_pattern S;
+    double* slab;              /* 2 device doubles */
+    double* host;              /* 2 pinned host doubles */
+    double* ws;
+    void* stream;
+    double* alphas;
+    double* betas;
+} cl_lanczos_args;
+
+int cl_lanczos_loop(const cl_lanczos_args* a, int32_t* k_out);
+
 /* L2 fetch granularity hint of the current device (cudaLimitMaxL2FetchGranularity, 0..128 bytes). */
 int cl_set_l2_fetch_granularity(int32_t bytes);
 int cl_get_l2_fetch_granularity(void);

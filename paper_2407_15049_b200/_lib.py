@@ -27,7 +27,8 @@ CL_EARG = 1001
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint_eval_halo",
            "cl_diag_constraint_eval", "cl_sddmm",
            "cl_gather_rows", "cl_diag_cg_apply", "cl_cg_step", "cl_admm_step_diag", "cl_alm_inner_diag",
-           "cl_diag_admm_cg_init", "cl_diag_admm_step_end", "cl_single_entry_apply",
+           "cl_diag_admm_cg_init", "cl_diag_admm_step_end", "cl_single_entry_apply", "cl_lanczos_loop",
+           "cl_pattern_assemble",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
            "cl_set_l2_fetch_granularity", "cl_get_l2_fetch_granularity", "cl_version", "cl_device_ok")
 
@@ -98,6 +99,12 @@ class AlmInnerStats(ctypes.Structure):
                 ("ax_is_ax2", I32), ("err_line", I32)]
 
 
+class LanczosArgs(ctypes.Structure):
+    _fields_ = [("n", I64), ("k_max", I32), ("breakdown", D), ("Q", P), ("ldq", I64), ("u", P), ("r", P),
+                ("h", P), ("S", Pattern), ("slab", P), ("host", P), ("ws", P), ("stream", P),
+                ("alphas", P), ("betas", P)]
+
+
 _LIB = None
 _LOCK = threading.Lock()
 
@@ -120,6 +127,8 @@ def _declare(lib):
     lib.cl_diag_admm_cg_init.argtypes = [ctypes.POINTER(Pattern), P, P, I32, D, D, P, P, P, P, P, P]
     lib.cl_diag_admm_step_end.argtypes = [ctypes.POINTER(Pattern), P, P, I32, P, P, P, D, P, P, P, P, P]
     lib.cl_single_entry_apply.argtypes = [I64, P, P, P, I32, P, P, D, P, P, P, P]
+    lib.cl_pattern_assemble.argtypes = [ctypes.POINTER(Pattern), P, P]
+    lib.cl_lanczos_loop.argtypes = [ctypes.POINTER(LanczosArgs), ctypes.POINTER(I32)]
     lib.cl_gather_rows.argtypes = [P, I64, I32, P, P, P]
     lib.cl_sddmm.argtypes = [I64, P, P, I32, P, P, P, P]
     lib.cl_diag_alm_update.argtypes = [ctypes.POINTER(DiagUpdateArgs), P, P, P]

@@ -1678,6 +1678,20 @@ int cl_single_entry_apply(int64_t nrows, const int64_t* indptr, const int32_t* i
     return (int)cudaGetLastError();
 }
 
+int cl_pattern_assemble(const cl_pattern* S, double* vals, void* stream) {
+    if (S == nullptr || vals == nullptr || S->nnz < 0) return CL_EARG;
+    if (S->nnz == 0) return CL_OK;
+    PatDev P;
+    memset(&P, 0, sizeof(P));
+    P.nrows = S->nrows; P.indptr = S->indptr; P.indices = S->indices; P.cv = S->cv; P.c_coeff = S->c_coeff;
+    P.at_ptr = S->at_ptr; P.at_con = S->at_con; P.at_val = S->at_val; P.w1 = S->w1; P.w2 = S->w2;
+    P.w1g = S->w1g; P.w2g = S->w2g; P.mown = S->mown;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int64_t g = (S->nnz + NT - 1) / NT;
+    assemble_kernel<<<(int)(g > NSM * 16 ? NSM * 16 : g), NT, 0, st>>>(P, S->nnz, vals);
+    return (int)cudaGetLastError();
+}
+
 int cl_sddmm(int64_t K, const int32_t* imap, const int32_t* jmap, int32_t ld, const double* X, const double* Y,
              double* x, void* stream) {
     if (K < 0 || ld < 1 || (ld > 1 && (ld & 1))) return CL_EARG;

@@ -10,6 +10,7 @@ tridiagonal eigenproblem (size <= 300) is solved on the host with scipy.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -29,10 +30,13 @@ class EigEstimate:
 
 
 class _DeviceOp:
-    """Marks a device-native operator: op(v_dev, out_dev, dot_at) -> writes out, <out, v> at slab."""
+    """Marks a device-native operator: op(v_dev, out_dev, dot_at) -> writes out, <out, v> at slab.
+    ``assembled()`` (optional) returns a cl_pattern whose slot values are the operator's,
+    assembled once, for the native Lanczos loop."""
 
-    def __init__(self, fn):
+    def __init__(self, fn, assembled=None):
         self.fn = fn
+        self.assembled = assembled
 
 
 def _host_callback_op(apply_s, dev):
@@ -41,6 +45,27 @@ def _host_callback_op(apply_s, dev):
         out.copy_(torch.as_tensor(np.asarray(u, dtype=np.float64)).to(dev.dev))
         dev.lincomb(None, [out, v], [0.0, 0.0], dots=[(0, 1)], at=at, N=v.numel())
     return _DeviceOp(fn)
+
+
+NATIVE = True     # one device, assembled operator: run the Lanczos loop's control flow in C++
+
+
+def _lanczos_native(op, n, k_max, Q, u, r, h, dev, alphas, betas):
+    """The loop below through cl_lanczos_loop (same launches; bit-identical coefficients)."""
+    from . import _lib
+    a = _lib.LanczosArgs()
+    a.n, a.k_max, a.breakdown = n, k_max, 1e-14
+    a.Q, a.ldq = Q.data_ptr(), int(Q.shape[1])
+    a.u, a.r, a.h = u.data_ptr(), r.data_ptr(), h.data_ptr()
+    a.S = op.assembled()
+    a.slab, a.host = dev.slot(520).value, dev.host.data_ptr() + 8 * 520
+    a.ws, a.stream = dev.ws.data_ptr(), dev.stream.cuda_stream
+    a.alphas, a.betas = alphas.ctypes.data, betas.ctypes.data
+    k = _lib.I32(0)
+    rc = dev.lib.cl_lanczos_loop(ctypes.byref(a), ctypes.byref(k))
+    dev.launches += 9 * k.value
+    _lib.check(rc, "cl_lanczos_loop")
+    return k.value
 
 
 def _lanczos_smallest(op, n, seed, max_basis, dev, rows=None):
@@ -64,7 +89,10 @@ def _lanczos_smallest(op, n, seed, max_basis, dev, rows=None):
     A = 500
     k = 0
     breakdown = 1e-14
-    while k < k_max:
+    native = NATIVE and dev.world == 1 and getattr(op, "assembled", None) is not None
+    if native:
+        k = _lanczos_native(op, n, k_max, Q, u, r, h, dev, alphas, betas)
+    while not native and k < k_max:
         qk = Q[k, :n]
         op.fn(qk, u[:n], A)
         alphas[k] = float(dev.fetch(A + 1)[A])
@@ -126,7 +154,23 @@ def omega_operator(ops, lam_dev, c_coeff=1.0):
     def fn(v, out, at):
         dev.spmm(ops.adj.omega, v, 1, out=out, Z=[v], dots=[("out", ("z", 0))], at=at,
                  c_coeff=c_coeff, w1=lam_dev)
-    return _DeviceOp(fn)
+
+    def assembled():
+        """Slot values of c_coeff*C + A*(lam) assembled once (the pre-pass fn repeats per call)."""
+        from . import _lib
+        from .linops import padded
+        om = ops.adj.omega
+        P = om.struct(c_coeff=c_coeff, w1=lam_dev)
+        vals = padded(torch.empty(om.nnz, dtype=F64, device=dev.dev))
+        _lib.check(dev.lib.cl_pattern_assemble(ctypes.byref(P), vals.data_ptr() if om.nnz else None, dev.sp),
+                   "cl_pattern_assemble")
+        dev.launches += 1
+        S = om.struct(c_coeff=None)          # indices/pointers; values from `vals`
+        S.cv = vals.data_ptr() if om.nnz else None
+        S.c_coeff = 1.0
+        assembled.keep = vals                # keep the buffer alive while the loop runs
+        return S
+    return _DeviceOp(fn, assembled)
 
 
 def dual_infeasibility(problem, ops, lam, tol=1e-7, seed=0):

@@ -274,3 +274,24 @@ def test_single_entry_detection_rejects_general_constraints(dev):
     from tests._golden import load, problem_from
     ops = linops.build_operators(problem_from(load("solve_random_sdp.npz")))
     assert ops.adj.apat.single_a is None
+
+
+@pytest.mark.parametrize("case", ["maxcut", "completion"])
+def test_native_lanczos_bit_identical(dev, case):
+    """cl_lanczos_loop (operator assembled once) vs the Python-driven loop: same eigenvalue
+    estimate to the bit, and the same basis size."""
+    from paper_2407_15049_b200 import graphs, linops, problem, spectral
+    if case == "maxcut":
+        p = problem.build_maxcut(graphs.random_sparse(700, deg=8.0, seed=5))
+    else:
+        p = problem.build_matrix_completion(graphs.random_completion(60, 50, 900, seed=5))
+    ops = linops.build_operators(p)
+    lam = np.random.default_rng(7).standard_normal(p.m)
+    res = {}
+    for native in (True, False):
+        spectral.NATIVE = native
+        try:
+            res[native] = spectral.dual_infeasibility(p, ops, lam, tol=1e-7, seed=3)
+        finally:
+            spectral.NATIVE = True
+    assert res[True] == res[False]
