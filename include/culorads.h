@@ -166,7 +166,7 @@ int cl_single_entry_apply(int64_t nrows, const int64_t* indptr, const int32_t* i
                           int32_t ld, const double* W, const double* Wf, double rho, double* out, double* dots_out,
                           double* ws, void* stream);
 
-/* Fused SpMM passes of the ADMM step for diagonal constraints (ld <= 64):
+/* Fused SpMM passes of the ADMM step for diagonal constraints:
  *   cl_diag_admm_cg_init: rhs = -scale C Wf + rho Wf + diag(a nlam) Wf (admm.py:52,
  *     nlam = rho b - lam) and the initial CG residual r = rhs - Q(x0) with
  *     Q(x0) = rho (a y Wf + x0), y = a <x0, Wf>  (admm.py:45/72) -- rhs and Q are

@@ -376,7 +376,7 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
     return StepStats(st.it_u, st.it_v, st.res_u, st.res_v, bool(st.hit_cap))
 
 
-_FUSED_LD = 64     # admm_native.cu FUSED_LD: fused rhs/initial-residual and step-end passes
+_FUSED_LD = 1 << 30     # admm_native.cu FUSED_LD: fused rhs/initial-residual and step-end passes
 
 
 def _admm_step_diag_py(state, ops, scale, cg_cap, rel_floor, coeff, hs, pool):

@@ -43,7 +43,8 @@ enum { S_PM = 0, S_RHS = 1, S_R0 = 2, S_XXU = 3, S_PQ = 4, S_QN = 5, S_PN = 6, S
        S_E0 = 10 };   // S_E0..S_E0+2: the fused step-end dots (objective, ||ax-b||^2, lam_new.b)
 
 // ld <= FUSED_LD: the rhs + initial residual and the step end run as single fused SpMM passes
-constexpr int FUSED_LD = 64;
+// (any ld: the fused epilogues reduce the row dot over all column chunks)
+constexpr int FUSED_LD = 1 << 30;
 
 // Copy slab[lo, lo+cnt) to the pinned host buffer and wait.
 bool fetch(Ctx& c, int lo, int cnt) {

@@ -849,6 +849,13 @@ __global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : 3) spm
             if (lr >= nr) break;
             const int64_t row = r0 + lr;
             const int64_t s0 = B.ptr[row - pb], s1 = B.ptr[row + 1 - pb];
+            double pd_row = 0.0;     // EPI 2/3: the row dot <Z0_i, Y0_i> over all column chunks
+            if (EPI >= 2) {
+                for (int c = gl * VEC; c < ld; c += G * VEC)
+                    pd_row += dot2(ld2cs(E.Z[0] + row * (int64_t)ld + c), ld2cs(E.Y[0] + row * (int64_t)ld + c));
+#pragma unroll
+                for (int sh = G / 2; sh > 0; sh >>= 1) pd_row += __shfl_xor_sync(gmask, pd_row, sh);
+            }
             for (int c0 = 0; c0 < ld; c0 += G * VEC) {
                 const int col = c0 + gl * VEC;
                 const bool active = col < ld;
@@ -915,15 +922,13 @@ __global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : 3) spm
                     }
                 }
                 if (EPI >= 2) {
-                    // Diagonal-constraint ADMM epilogues; the row is one column chunk (ld <= 2G),
-                    // every lane of the group takes part in the row dot <Z0_i, Y0_i>.
+                    // Diagonal-constraint ADMM epilogues (per column chunk; the row dot was
+                    // reduced over the whole row above).
                     const int64_t off = row * (int64_t)ld + col;
                     const double2 zr = make_double2(0.0, 0.0);
                     const double2 yv = active ? ld2cs(E.Y[0] + off) : zr;   // Wf (EPI 2) / V (EPI 3)
                     const double2 zv = active ? ld2cs(E.Z[0] + off) : zr;   // x0 (EPI 2) / U (EPI 3)
-                    double pd = dot2(zv, yv);
-#pragma unroll
-                    for (int sh = G / 2; sh > 0; sh >>= 1) pd += __shfl_xor_sync(gmask, pd, sh);
+                    const double pd = pd_row;
                     const double av = __ldg(E.dmul + row);
                     double2 o = make_double2(a.alpha * acc.x, a.alpha * acc.y);
                     if (EPI == 2) {
@@ -943,7 +948,7 @@ __global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : 3) spm
                     } else {
                         // <C V, U> (objective), A(U V^T), residual, dual ascent, lam_new . b
                         if (active) dacc[0] += dot2(o, zv);
-                        if (gl == 0) {
+                        if (gl == 0 && c0 == 0) {
                             const double ax = 0.0 + av * pd;
                             const double bb = __ldg(E.bvec + row);
                             const double res = fma(-1.0, bb, fma(1.0, ax, 0.0));
@@ -1595,8 +1600,7 @@ int cl_cg_step(int64_t N, double alpha, const double* x_in, double* x_out, const
 // Shared setup of the fused diagonal-ADMM SpMM launches (C pattern with cv values).
 static int diag_admm_launch(int mode, const cl_pattern* S, const double* X, int32_t ld, double alpha, EpiDev& E,
                             double* dots_out, double* ws, cudaStream_t st) {
-    if (S == nullptr || X == nullptr || ld < 2 || (ld & 1) || ld > 64 || dots_out == nullptr || ws == nullptr)
-        return CL_EARG;
+    if (S == nullptr || X == nullptr || ld < 2 || (ld & 1) || dots_out == nullptr || ws == nullptr) return CL_EARG;
     if (S->at_ptr != nullptr && (S->w1 != nullptr || S->w2 != nullptr)) return CL_EARG;
     if (!(S->cv != nullptr || S->nnz == 0) || !aligned16(S->indptr) || !aligned16(S->indices) || !aligned16(X))
         return CL_EARG;

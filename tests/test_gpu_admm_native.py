@@ -11,7 +11,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _run_steps(native, p, steps, seed=0):
+def _run_steps(native, p, steps, seed=0, r=6):
     import torch
     from paper_2407_15049_b200 import admm, alm, linops
     from paper_2407_15049_b200.device import padded_ld
@@ -19,7 +19,6 @@ def _run_steps(native, p, steps, seed=0):
     try:
         ops = linops.build_operators(p)
         dev = ops.dev
-        r = 6
         ld = padded_ld(r)
         rng = np.random.default_rng(seed)
         R = linops.to_factor(rng.standard_normal((p.n, r)) / np.sqrt(p.n * r), dev, ld)
@@ -36,11 +35,12 @@ def _run_steps(native, p, steps, seed=0):
         admm.NATIVE = True
 
 
-def test_native_step_bit_identical_to_python_step():
+@pytest.mark.parametrize("r", [6, 70])
+def test_native_step_bit_identical_to_python_step(r):
     from paper_2407_15049_b200 import graphs, problem
     p = problem.build_maxcut(graphs.random_sparse(3000, deg=6.0, seed=4))
-    a = _run_steps(True, p, 12)
-    b = _run_steps(False, p, 12)
+    a = _run_steps(True, p, 12, r=r)
+    b = _run_steps(False, p, 12, r=r)
     assert sum(s[0] + s[1] for s in a[3]) > 0          # CG iterations actually ran
     for x, y in zip(a[:3], b[:3]):
         assert x.tobytes() == y.tobytes()

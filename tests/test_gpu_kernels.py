@@ -295,3 +295,43 @@ def test_native_lanczos_bit_identical(dev, case):
         finally:
             spectral.NATIVE = True
     assert res[True] == res[False]
+
+
+@pytest.mark.parametrize("ld", [2, 26, 66, 130])
+def test_fused_admm_passes_match_numpy(dev, ld):
+    """cl_diag_admm_cg_init / cl_diag_admm_step_end against dense numpy, including ranks
+    whose rows span several column chunks."""
+    import torch
+    from paper_2407_15049_b200 import graphs, linops, problem
+    p = problem.build_maxcut(graphs.random_sparse(1500, deg=7.0, seed=ld))
+    ops = linops.build_operators(p)
+    rng = np.random.default_rng(ld)
+    T = lambda *s: torch.as_tensor(rng.standard_normal(s)).cuda().contiguous()  # noqa: E731
+    Wf, x0, U, V = T(p.n, ld), T(p.n, ld), T(p.n, ld), T(p.n, ld)
+    nlam, lam = T(p.m), T(p.m)
+    aval = ops.diag_aval
+    r = torch.empty_like(Wf)
+    scale, rho = 0.7, 1.9
+    dev.diag_admm_cg_init(ops.c_mat.cpat, Wf, x0, ld, scale, rho, nlam, aval, r, at=60)
+    ax = torch.empty(p.m, dtype=torch.float64, device="cuda")
+    lam_new = torch.empty_like(ax)
+    dev.diag_admm_step_end(ops.c_mat.cpat, U, V, ld, aval, ops.b, lam, rho, ax, lam_new, at=62)
+    s = dev.fetch(65)
+    C = sp.csr_matrix((ops.c_mat.cpat.cv.cpu().numpy(), ops.c_mat.cpat.indices.cpu().numpy(),
+                       ops.c_mat.cpat.indptr.cpu().numpy()), shape=(p.n, p.n))
+    a = aval.cpu().numpy()
+    Wh, xh, Uh, Vh = [t.cpu().numpy() for t in (Wf, x0, U, V)]
+    rhs = -scale * (C @ Wh) + rho * Wh + (a * nlam.cpu().numpy())[:, None] * Wh
+    y = a * np.einsum("ij,ij->i", xh, Wh)
+    Q = rho * ((a * y)[:, None] * Wh + xh)
+    rr = rhs - Q
+    close = lambda u, v, t=1e-11: abs(u - v) <= t * (1 + abs(v))  # noqa: E731
+    assert np.abs(r.cpu().numpy() - rr).max() <= 1e-11 * (1 + np.abs(rr).max())
+    assert close(s[60], np.sum(rhs * rhs)) and close(s[61], np.sum(rr * rr))
+    axh = a * np.einsum("ij,ij->i", Uh, Vh)
+    res = axh - ops.b.cpu().numpy()
+    ln = lam.cpu().numpy() + rho * res
+    assert np.abs(ax.cpu().numpy() - axh).max() <= 1e-11 * (1 + np.abs(axh).max())
+    assert np.abs(lam_new.cpu().numpy() - ln).max() <= 1e-11 * (1 + np.abs(ln).max())
+    assert close(s[62], np.sum((C @ Vh) * Uh)) and close(s[63], res @ res)
+    assert close(s[64], ln @ ops.b.cpu().numpy())
