@@ -245,8 +245,10 @@ int cl_basis_subtract(const double* Q, int64_t ldq, int32_t k_cnt, int64_t n, co
  * reference (tolerance schedule, cg_solve's stop/curvature/finiteness
  * tests, admm.py:65) taken in native host code between launches of the
  * kernels above. Same launches in the same order as the Python host path,
- * hence bit-identical iterates; values needed at the same decision point are
- * read with one pinned copy + synchronize (3 per step when CG stops at once). */
+ * hence bit-identical iterates. The V half-step's start and the step end are
+ * launched speculatively (assuming the CGs stop at their start, the common case)
+ * so such a step costs ONE synchronize; a CG that iterates triggers the
+ * recomputation of the speculative work. */
 typedef struct {
     int64_t n;                 /* rows = constraints */
     int32_t ld;
@@ -261,10 +263,10 @@ typedef struct {
     const double* V;
     double* U_new;
     double* V_new;
-    double* r;                 /* CG residual / direction / operator output, n x ld */
-    double* p;
+    double* r;                 /* CG residual of the U half-step, n x ld */
+    double* r_v;               /* CG residual of the V half-step (started speculatively) */
+    double* p;                 /* CG direction / operator output, n x ld */
     double* Q;
-    double* rhs;               /* n x ld */
     double* nlam;              /* m-vector scratch */
     double* res;               /* m-vector scratch */
     cl_pattern cpat;           /* C (cv values) */

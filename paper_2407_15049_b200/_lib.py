@@ -70,7 +70,7 @@ class AdmmDiagArgs(ctypes.Structure):
     _fields_ = [("n", I64), ("ld", I32), ("aval", P), ("b", P), ("lam", P), ("lam_new", P), ("ax", P),
                 ("ax_valid", I32),
                 ("pnorm2_known", D), ("U", P), ("V", P), ("U_new", P), ("V_new", P),
-                ("r", P), ("p", P), ("Q", P), ("rhs", P), ("nlam", P), ("res", P),
+                ("r", P), ("r_v", P), ("p", P), ("Q", P), ("nlam", P), ("res", P),
                 ("cpat", Pattern), ("rho", D), ("scale", D), ("binf", D), ("rel_floor", D),
                 ("primal_coeff", D), ("cg_cap", I32), ("slab", P), ("host", P), ("ws", P), ("stream", P)]
 

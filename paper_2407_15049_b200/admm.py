@@ -328,9 +328,10 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
     a.ax = ax.data_ptr()
     U_new = pool.get() if pool else dev.empty(n, ld)
     V_new = pool.get() if pool else dev.empty(n, ld)
-    rhs = pool.get() if pool else dev.empty(n, ld)
+    if getattr(hs, "r_v", None) is None:
+        hs.r_v = dev.empty(n, ld)
     a.U, a.V, a.U_new, a.V_new = state.U.data_ptr(), state.V.data_ptr(), U_new.data_ptr(), V_new.data_ptr()
-    a.r, a.p, a.Q, a.rhs = hs.r.data_ptr(), hs.p.data_ptr(), hs.Q.data_ptr(), rhs.data_ptr()
+    a.r, a.r_v, a.p, a.Q = hs.r.data_ptr(), hs.r_v.data_ptr(), hs.p.data_ptr(), hs.Q.data_ptr()
     nlam = hs.nlam
     a.nlam, a.res = nlam.data_ptr(), hs.y.data_ptr()
     a.cpat = ops.c_mat.cpat.struct(c_coeff=1.0)
@@ -371,27 +372,21 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
     state.dual.lam = lam_new
     hs.lam_spare = old
     state.step_obj = (st.objective, st.lam_b)
-    if pool:
-        pool.put(rhs)
     return StepStats(st.it_u, st.it_v, st.res_u, st.res_v, bool(st.hit_cap))
 
 
-_FUSED_LD = 1 << 30     # admm_native.cu FUSED_LD: fused rhs/initial-residual and step-end passes
-
-
 def _admm_step_diag_py(state, ops, scale, cg_cap, rel_floor, coeff, hs, pool):
-    """Python-driven twin of cl_admm_step_diag (admm_native.cu): the same launches in the
-    same order with the same scalar decisions, so the iterates are bit-identical. Used for
-    row-sharded solves (the halo exchanges and scalar reductions live in Python) and as the
-    reference the native step is tested against."""
+    """Python-driven twin of cl_admm_step_diag (admm_native.cu) without its speculation:
+    every kernel that counts gets the same operands in the same order and the scalar
+    decisions are the same, so the iterates are bit-identical. Used for row-sharded solves
+    (halo exchanges and scalar reductions live in Python) and as the reference the native
+    step is tested against."""
     dev = ops.dev
     p = ops.problem
     n, ld = state.U.shape
     rho = float(state.dual.rho)
     lam = state.dual.lam
-    base = 470
-    S = lambda k: base + k  # noqa: E731  (slots of admm_native.cu)
-    fused = ld <= _FUSED_LD
+    S = lambda k: 470 + k  # noqa: E731  (slots of admm_native.cu)
     cpat = ops.c_mat.cpat
 
     def fetch(hi):
@@ -413,17 +408,10 @@ def _admm_step_diag_py(state, ops, scale, cg_cap, rel_floor, coeff, hs, pool):
     mn = y if y < 1e-2 else 1e-2
     rel = mn if mn > rel_floor else rel_floor
     dev.lincomb(hs.nlam, [ops.b, lam], [rho, -1.0])
-    rhs = pool.get() if pool else dev.empty(n, ld)
 
     def half(x0, x, Wf, xx_prev):
-        """-> (status, eps, its, rnorm, last_is_x, pq, reused)"""
-        if fused:
-            dev.diag_admm_cg_init(cpat, Wf, x0, ld, scale, rho, hs.nlam, ops.diag_aval, hs.r, at=S(1))
-        else:
-            dev.spmm(cpat, Wf, ld, alpha=-scale, out=rhs, Y=[Wf], ycoef=[rho], c_coeff=1.0, drow=hs.nlam,
-                     dmul=ops.diag_aval, dots=[("out", "out")], at=S(1))
-            dev.diag_cg_apply(ops.diag_aval, ld, rho, x0, Wf, hs.Q, at=S(4))
-            dev.lincomb(hs.r, [rhs, hs.Q], [1.0, -1.0], dots=[("out", "out")], at=S(2))
+        """-> (status, eps, its, rnorm, last_is_x, pq, kept); status 4: previous iterate not finite"""
+        dev.diag_admm_cg_init(cpat, Wf, x0, ld, scale, rho, hs.nlam, ops.diag_aval, hs.r, at=S(1))
         h = fetch(4 if xx_prev else 3)
         if xx_prev and not math.isfinite(float(h[S(3)])):
             return 4, 0.0, 0, 0.0, 0, 0.0, 0
@@ -453,14 +441,17 @@ def _admm_step_diag_py(state, ops, scale, cg_cap, rel_floor, coeff, hs, pool):
             dev.lincomb(x, [x0], [1.0])
         return 0, eps, its, rnorm, 0, 0.0, 0
 
+    def raise_for(st, half_new, half_old):
+        last = half_new if st[4] else half_old
+        if st[0] == 2:
+            raise SpdViolationError(f"non-positive curvature {st[5]:.3e} in CG (operator not SPD)")
+        raise DivergedError("CG produced non-finite curvature", last_iterate=last)
+
     U_new = pool.get() if pool else dev.empty(n, ld)
     V_new = pool.get() if pool else dev.empty(n, ld)
     st_u = half(state.U, U_new, state.V, False)
     if st_u[0]:
-        last = U_new if st_u[4] else state.U
-        if st_u[0] == 2:
-            raise SpdViolationError(f"non-positive curvature {st_u[5]:.3e} in CG (operator not SPD)")
-        raise DivergedError("CG produced non-finite curvature", last_iterate=last)
+        raise_for(st_u, U_new, state.U)
     Uc = state.U if st_u[6] else U_new
     if not st_u[6]:
         dev.lincomb(None, [U_new], [0.0], dots=[(0, 0)], at=S(3))
@@ -468,28 +459,16 @@ def _admm_step_diag_py(state, ops, scale, cg_cap, rel_floor, coeff, hs, pool):
     if st_v[0] == 4:
         raise DivergedError("CG iterate diverged", last_iterate=U_new)
     if st_v[0]:
-        last = V_new if st_v[4] else state.V
-        if st_v[0] == 2:
-            raise SpdViolationError(f"non-positive curvature {st_v[5]:.3e} in CG (operator not SPD)")
-        raise DivergedError("CG produced non-finite curvature", last_iterate=last)
+        raise_for(st_v, V_new, state.V)
     Vc = state.V if st_v[6] else V_new
     if not st_v[6]:
         dev.lincomb(None, [V_new], [0.0], dots=[(0, 0)], at=S(7))
     lam_new = hs.lam_spare if getattr(hs, "lam_spare", None) is not None else dev.empty(p.m)
-    if fused:
-        dev.diag_admm_step_end(cpat, Uc, Vc, ld, ops.diag_aval, ops.b, lam, rho, ax, lam_new, at=S(10))
-        h = fetch(13)
-        vx, obj, pn2, lamb = h[S(7)], h[S(10)], h[S(11)], h[S(12)]
-    else:
-        dev.constraint_eval(ops.cop.con, ld, Uc, Vc, ax)
-        dev.lincomb(hs.y, [ax, ops.b], [1.0, -1.0], dots=[("out", "out")], at=S(6))
-        dev.lincomb(lam_new, [lam, hs.y], [1.0, rho])
-        dev.spmm(cpat, Vc, ld, out=None, Z=[Uc], dots=[("out", ("z", 0))], at=S(8), c_coeff=1.0)
-        dev.lincomb(None, [lam_new, ops.b], [0.0, 0.0], dots=[(0, 1)], at=S(9))
-        h = fetch(10)
-        vx, pn2, obj, lamb = h[S(7)], h[S(6)], h[S(8)], h[S(9)]
-    if not st_v[6] and not math.isfinite(float(vx)):
+    dev.diag_admm_step_end(cpat, Uc, Vc, ld, ops.diag_aval, ops.b, lam, rho, ax, lam_new, at=S(10))
+    h = fetch(13)
+    if not st_v[6] and not math.isfinite(float(h[S(7)])):
         raise DivergedError("CG iterate diverged", last_iterate=V_new)
+    obj, pn2, lamb = h[S(10)], h[S(11)], h[S(12)]
     if st_u[6] and pool:
         pool.put(U_new)
     if st_v[6] and pool:
@@ -502,8 +481,6 @@ def _admm_step_diag_py(state, ops, scale, cg_cap, rel_floor, coeff, hs, pool):
     hs.lam_spare = lam
     state.dual.lam = lam_new
     state.step_obj = (float(obj), float(lamb))
-    if pool:
-        pool.put(rhs)
     hit_cap = (st_u[2] >= cg_cap and st_u[3] > st_u[1]) or (st_v[2] >= cg_cap and st_v[3] > st_v[1])
     return StepStats(st_u[2], st_v[2], st_u[3], st_v[3], bool(hit_cap))
 
