@@ -193,6 +193,11 @@ int cl_diag_cg_apply(int64_t n, int32_t ld, const double* aval, double rho, doub
                      const double* Wf, double* Q, double* dots_out, double* ws, void* stream);
 int cl_cg_step(int64_t N, double alpha, const double* x_in, double* x_out, const double* p, double* r,
                const double* Q, double* dots_out, double* ws, void* stream);
+/* cl_cg_step with alpha = qr / *pq computed on the device (pq: the device reduction of
+ * the preceding operator application); a non-finite or non-positive pq leaves x and r
+ * untouched (cg_solve raises there, admm.py:83-86). */
+int cl_cg_step_dev(int64_t N, double qr, const double* pq, const double* x_in, double* x_out, const double* p,
+                   double* r, const double* Q, double* dots_out, double* ws, void* stream);
 
 /* cl_constraint_eval for a row block of a row-sharded solve: factor row
  * index >= nown of operand k (X1, Y1, X2, Y2, X3, Y3) reads ghosts[k][row-nown]

@@ -26,7 +26,7 @@ CL_EARG = 1001
 
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint_eval_halo",
            "cl_diag_constraint_eval", "cl_sddmm",
-           "cl_gather_rows", "cl_diag_cg_apply", "cl_cg_step", "cl_admm_step_diag", "cl_alm_inner_diag",
+           "cl_gather_rows", "cl_diag_cg_apply", "cl_cg_step", "cl_cg_step_dev", "cl_admm_step_diag", "cl_alm_inner_diag",
            "cl_diag_admm_cg_init", "cl_diag_admm_step_end", "cl_single_entry_apply", "cl_lanczos_loop",
            "cl_pattern_assemble",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
@@ -129,6 +129,7 @@ def _declare(lib):
     lib.cl_single_entry_apply.argtypes = [I64, P, P, P, I32, P, P, D, P, P, P, P]
     lib.cl_pattern_assemble.argtypes = [ctypes.POINTER(Pattern), P, P]
     lib.cl_lanczos_loop.argtypes = [ctypes.POINTER(LanczosArgs), ctypes.POINTER(I32)]
+    lib.cl_cg_step_dev.argtypes = [I64, D, P, P, P, P, P, P, P, P, P]
     lib.cl_gather_rows.argtypes = [P, I64, I32, P, P, P]
     lib.cl_sddmm.argtypes = [I64, P, P, I32, P, P, P, P]
     lib.cl_diag_alm_update.argtypes = [ctypes.POINTER(DiagUpdateArgs), P, P, P]

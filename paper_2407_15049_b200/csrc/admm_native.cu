@@ -140,21 +140,21 @@ int cg_loop(Ctx& c, const double* x0, double* x, const double* Wf, double* r, do
     const double* xs = x0;
     *last_is_x = 0;
     for (int k = 0; k < a->cg_cap; ++k) {
+        // operator application, then the update with alpha = qr / pq taken on the device:
+        // pq and the new <r, r> are read together (one synchronize per iteration)
         CL_TRY(c, cl_diag_cg_apply(a->n, a->ld, a->aval, a->rho, beta, r, a->p, Wf, a->Q, a->slab + S_PQ, a->ws,
                                    (void*)c.st));
-        if (!fetch(c, S_PQ, 1)) return 0;
+        CL_TRY(c, cl_cg_step_dev(c.N, qr, a->slab + S_PQ, xs, x, a->p, r, a->Q, a->slab + S_QN, a->ws, (void*)c.st));
+        if (!fetch(c, S_PQ, 2)) return 0;
         const double pq = H(c, S_PQ);
-        if (!isfinite(pq) || pq <= 0.0) {
+        if (!isfinite(pq) || pq <= 0.0) {          // the device update was skipped
             *last_is_x = xs == x;
             *its_out = its;
             *rnorm_out = rnorm;
             *pq_bad = pq;
             return isfinite(pq) ? 2 : 1;
         }
-        const double alpha = qr / pq;
-        CL_TRY(c, cl_cg_step(c.N, alpha, xs, x, a->p, r, a->Q, a->slab + S_QN, a->ws, (void*)c.st));
         xs = x;
-        if (!fetch(c, S_QN, 1)) return 0;
         const double qn = H(c, S_QN);
         rnorm = sqrt(qn);
         its = k + 1;

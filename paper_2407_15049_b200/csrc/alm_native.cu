@@ -8,8 +8,8 @@
 // of best_step (alm.py:166/202), the curvature-pair bookkeeping -- is
 // restated here operation for operation, so the iterates are bit-identical
 // to the Python-driven path (tests/test_gpu_alm_native.py). Each iteration
-// needs three pinned reads (direction Gram row, line-search scalars, update
-// reductions).
+// needs two pinned reads: the direction's Gram row travels with the
+// line-search scalars, then the update's reductions.
 
 #include <cuda_runtime.h>
 #include <math.h>
@@ -336,9 +336,8 @@ extern "C" int cl_alm_inner_diag(const cl_alm_inner_args* a, cl_alm_inner_stats*
             Lc.out = B(c, Dn);
             TRY(c, cl_lincomb(&Lc, c.N, a->slab + S_DIR, a->ws, (void*)c.st));
         }
-        if (!fetch(c, nt + 1)) break;
-        for (int k = 0; k < nt; ++k) hist.set(Dn, tb[k], a->host[S_DIR + k]);
-        hist.set(Dn, Dn, a->host[S_DIR + nt]);
+        // (the direction's Gram row is read together with the line-search scalars below:
+        //  the line search only needs D on the device)
 
         // ---- exact line search (AlmCore.line_search, alm.py:135) ----
         double* D = B(c, Dn);
@@ -382,6 +381,8 @@ extern "C" int cl_alm_inner_diag(const cl_alm_inner_args* a, cl_alm_inner_stats*
             TRY(c, cl_lincomb(&Lc, a->n, a->slab + S_MV, a->ws, (void*)c.st));
         }
         if (!fetch(c, S_MV + 5)) break;
+        for (int k = 0; k < nt; ++k) hist.set(Dn, tb[k], a->host[S_DIR + k]);
+        hist.set(Dn, Dn, a->host[S_DIR + nt]);
         const double cdr = a->host[S_LS], cdd = a->host[S_LS + 1], crd = a->host[S_LS + 2];
         const double q2q2 = a->host[S_MV], q1q2 = a->host[S_MV + 1], wq2 = a->host[S_MV + 2];
         const double q1q1 = a->host[S_MV + 3], wq1 = a->host[S_MV + 4];

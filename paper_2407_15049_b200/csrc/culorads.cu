@@ -1233,6 +1233,26 @@ __global__ void __launch_bounds__(NT) cg_step_kernel(int64_t n2, double alpha, c
     reduce_and_finish<1>(dacc, 1, ws, dots_out);
 }
 
+// cg_step with alpha = qr / *pq taken on the device (no host round trip between the
+// operator application and the update). A curvature the host would reject (non-finite
+// or <= 0) leaves x and r untouched; the host sees it in the same read as <r, r>.
+__global__ void __launch_bounds__(NT) cg_step_dev_kernel(int64_t n2, double qr, const double* pq_ptr,
+                                                        const double* x_in, double* x_out, const double* p, double* r,
+                                                        const double* Q, double* ws, double* dots_out) {
+    const double pq = *pq_ptr;
+    if (!(isfinite(pq) && pq > 0.0)) return;
+    const double alpha = qr / pq;
+    double dacc[1] = {0.0};
+    for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < n2; k += (int64_t)gridDim.x * NT) {
+        const int64_t off = 2 * k;
+        st2(x_out + off, axpy2(alpha, ld2cs(p + off), ld2cs(x_in + off)));
+        const double2 rv = axpy2(-alpha, ld2cs(Q + off), ld2cs(r + off));
+        st2(r + off, rv);
+        dacc[0] += dot2(rv, rv);
+    }
+    reduce_and_finish<1>(dacc, 1, ws, dots_out);
+}
+
 __global__ void __launch_bounds__(NT) gather_rows_scalar_kernel(const int32_t* __restrict__ idx, int64_t count, int ld,
                                                                 const double* __restrict__ X, double* __restrict__ out) {
     const int64_t total = count * ld;
@@ -1594,6 +1614,18 @@ int cl_cg_step(int64_t N, double alpha, const double* x_in, double* x_out, const
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (N == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double), st);
     cg_step_kernel<<<red_grid(N / 2), NT, 0, st>>>(N / 2, alpha, x_in, x_out, p, r, Q, ws, dots_out);
+    return (int)cudaGetLastError();
+}
+
+int cl_cg_step_dev(int64_t N, double qr, const double* pq, const double* x_in, double* x_out, const double* p,
+                   double* r, const double* Q, double* dots_out, double* ws, void* stream) {
+    if (N < 0 || (N & 1) || pq == nullptr || x_in == nullptr || x_out == nullptr || p == nullptr || r == nullptr ||
+        Q == nullptr || dots_out == nullptr || ws == nullptr)
+        return CL_EARG;
+    if (!aligned16(x_in) || !aligned16(x_out) || !aligned16(p) || !aligned16(r) || !aligned16(Q)) return CL_EARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (N == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double), st);
+    cg_step_dev_kernel<<<red_grid(N / 2), NT, 0, st>>>(N / 2, qr, pq, x_in, x_out, p, r, Q, ws, dots_out);
     return (int)cudaGetLastError();
 }
 

@@ -335,3 +335,32 @@ def test_fused_admm_passes_match_numpy(dev, ld):
     assert np.abs(lam_new.cpu().numpy() - ln).max() <= 1e-11 * (1 + np.abs(ln).max())
     assert close(s[62], np.sum((C @ Vh) * Uh)) and close(s[63], res @ res)
     assert close(s[64], ln @ ops.b.cpu().numpy())
+
+
+@pytest.mark.parametrize("pq", [2.5, -1.0, 0.0, float("nan"), float("inf")])
+def test_cg_step_dev_alpha_and_rejected_curvature(dev, pq):
+    """cl_cg_step_dev: alpha = qr / pq on the device, bit-equal to the host division; a
+    curvature cg_solve rejects (admm.py:83-86) leaves x and r untouched."""
+    import ctypes
+    import torch
+    from paper_2407_15049_b200.device import ptr
+    rng = np.random.default_rng(1)
+    T = lambda: torch.as_tensor(rng.standard_normal((500, 6))).cuda().contiguous()  # noqa: E731
+    x, p_, r, Q = T(), T(), T(), T()
+    x0, r0 = x.clone(), r.clone()
+    dev.slab[700] = pq
+    qr = 3.7
+    rc = dev.lib.cl_cg_step_dev(x.numel(), qr, dev.slot(700), ptr(x), ptr(x), ptr(p_), ptr(r), ptr(Q),
+                                dev.slot(701), ptr(dev.ws), dev.sp)
+    assert rc == 0
+    torch.cuda.synchronize()
+    if np.isfinite(pq) and pq > 0:
+        alpha = qr / pq
+        want_x = x0.cpu().numpy() + alpha * p_.cpu().numpy()
+        want_r = r0.cpu().numpy() - alpha * Q.cpu().numpy()
+        assert np.abs(x.cpu().numpy() - want_x).max() <= 1e-14 * (1 + np.abs(want_x).max())
+        assert np.abs(r.cpu().numpy() - want_r).max() <= 1e-14 * (1 + np.abs(want_r).max())
+        assert abs(dev.fetch(702)[701] - np.sum(want_r * want_r)) <= 1e-10 * np.sum(want_r * want_r)
+    else:
+        assert torch.equal(x, x0) and torch.equal(r, r0)
+    del ctypes
