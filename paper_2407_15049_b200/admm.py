@@ -115,14 +115,23 @@ class HalfStep:
         its = 0
         for k in range(max_iter):
             self.apply(p, Wf, rho, Q, dot_with=p, at=A + 1)
-            pq = float(dev.fetch(A + 2)[A + 1])
+            if dev.world == 1:
+                # x += alpha p; r -= alpha Q; <r, r> with alpha = qr / <p, Q> taken on the device,
+                # so <p, Q> and <r, r> come back in one read (a rejected curvature skips the update)
+                dev.cg_step_dev(qr, A + 1, x, x, p, r, Q, at=A + 2)
+                h = dev.fetch(A + 3)
+                pq = float(h[A + 1])
+            else:
+                # row-sharded: <p, Q> is a per-rank partial until the slab is combined
+                pq = float(dev.fetch(A + 2)[A + 1])
             if not math.isfinite(pq):
                 raise DivergedError("CG produced non-finite curvature", last_iterate=x)
             if pq <= 0.0:
                 raise SpdViolationError(f"non-positive curvature {pq:.3e} in CG (operator not SPD)")
-            alpha = qr / pq
-            dev.cg_step(alpha, x, x, p, r, Q, at=A + 2)       # x += alpha p; r -= alpha Q; <r, r>
-            qn = float(dev.fetch(A + 3)[A + 2])
+            if dev.world > 1:
+                dev.cg_step(qr / pq, x, x, p, r, Q, at=A + 2)
+                h = dev.fetch(A + 3)
+            qn = float(h[A + 2])
             rnorm = math.sqrt(qn)
             its = k + 1
             if rnorm <= eps:

@@ -233,6 +233,14 @@ class Device:
         self.launches += 1
         check(rc, "cl_single_entry_apply")
 
+    def cg_step_dev(self, qr, pq_at, x_in, x_out, p, r, Q, at=0):
+        """x_out = x_in + alpha p; r -= alpha Q with alpha = qr / slab[pq_at] on the device;
+        <r, r> -> slab[at] (update skipped for a non-finite or non-positive curvature)."""
+        rc = self.lib.cl_cg_step_dev(int(r.numel()), float(qr), self.slot(pq_at), ptr(x_in), ptr(x_out), ptr(p),
+                                     ptr(r), ptr(Q), self.slot(at), ptr(self.ws), self.sp)
+        self.launches += 1
+        check(rc, "cl_cg_step_dev")
+
     def cg_step(self, alpha, x_in, x_out, p, r, Q, at=0):
         """x_out = x_in + alpha p; r -= alpha Q; <r, r> -> slab[at]."""
         rc = self.lib.cl_cg_step(int(r.numel()), float(alpha), ptr(x_in), ptr(x_out), ptr(p), ptr(r), ptr(Q),
