@@ -101,6 +101,34 @@ int red_grid(int64_t work_items) {
     return (int)g;
 }
 
+// Resident CTAs per SM of a kernel at NT threads (occupancy query, cached per kernel).
+int resident_blocks(const void* fn) {
+    static const void* keys[128];
+    static int vals[128];
+    static int cnt = 0;
+    for (int i = 0; i < cnt; ++i)
+        if (keys[i] == fn) return vals[i];
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, NT, 0) != cudaSuccess || nb < 1) nb = 1;
+    if (cnt < 128) {
+        keys[cnt] = fn;
+        vals[cnt] = nb;
+        ++cnt;
+    }
+    return nb;
+}
+
+// Grid of a grid-stride kernel: one full wave of resident CTAs (148 x CTAs/SM), fewer when
+// the work is smaller -- a partial second wave would idle part of the GPU at the end.
+int occ_grid(const void* fn, int64_t work_items, int64_t cap = CL_RED_BLOCKS) {
+    int64_t g = (work_items + NT - 1) / NT;
+    int64_t wave = (int64_t)resident_blocks(fn) * NSM;
+    if (wave > cap) wave = cap;
+    if (g > wave) g = wave;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
 // ---------------------------------------------------------------------------
 // streaming combination
 // ---------------------------------------------------------------------------
@@ -1331,15 +1359,23 @@ int cl_lincomb(const cl_lincomb_args* args, int64_t N, double* dots_out, double*
     if (d.ndot > 0 && (dots_out == nullptr || ws == nullptr)) return CL_EARG;
     const int64_t n2 = N / 2;
     const int tail = (int)(N & 1);
-    const int grid = red_grid(n2 + tail);
     if (N == 0) {
         if (d.ndot > 0) cudaMemsetAsync(dots_out, 0, sizeof(double) * d.ndot, st);
         return CL_OK;
     }
     switch (mode) {
-        case 0: lincomb_kernel<0><<<grid, NT, 0, st>>>(d, n2, tail, ws, dots_out); break;
-        case 1: lincomb_kernel<1><<<grid, NT, 0, st>>>(d, n2, tail, ws, dots_out); break;
-        default: lincomb_kernel<2><<<grid, NT, 0, st>>>(d, n2, tail, ws, dots_out); break;
+        case 0:
+            lincomb_kernel<0><<<occ_grid((const void*)lincomb_kernel<0>, n2 + tail), NT, 0, st>>>(d, n2, tail, ws,
+                                                                                                   dots_out);
+            break;
+        case 1:
+            lincomb_kernel<1><<<occ_grid((const void*)lincomb_kernel<1>, n2 + tail), NT, 0, st>>>(d, n2, tail, ws,
+                                                                                                   dots_out);
+            break;
+        default:
+            lincomb_kernel<2><<<occ_grid((const void*)lincomb_kernel<2>, n2 + tail), NT, 0, st>>>(d, n2, tail, ws,
+                                                                                                   dots_out);
+            break;
     }
     return (int)cudaGetLastError();
 }
@@ -1541,10 +1577,16 @@ int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const dou
         (Y2 == nullptr || aligned16(Y2)) && (X3 == nullptr || aligned16(X3)) && (Y3 == nullptr || aligned16(Y3))) {
         const int rb = (NT * DC_U) / (ld / 2);
         const int64_t nblk = (n + rb - 1) / rb;
-        const int grid = (int)(nblk > NSM * 8 ? NSM * 8 : nblk);
-        if (d.nop == 1) diag_constraint_flat_kernel<1><<<grid, NT, 0, st>>>(d);
-        else if (d.nop == 2) diag_constraint_flat_kernel<2><<<grid, NT, 0, st>>>(d);
-        else diag_constraint_flat_kernel<6><<<grid, NT, 0, st>>>(d);
+        // one full wave of resident CTAs (the shared-memory fold limits CTAs per SM)
+#define CL_DCF(NO)                                                                                  \
+    diag_constraint_flat_kernel<NO><<<(int)(nblk < (int64_t)resident_blocks((const void*)diag_constraint_flat_kernel<NO>) * NSM \
+                                                ? nblk                                            \
+                                                : (int64_t)resident_blocks((const void*)diag_constraint_flat_kernel<NO>) * NSM), \
+                                      NT, 0, st>>>(d)
+        if (d.nop == 1) CL_DCF(1);
+        else if (d.nop == 2) CL_DCF(2);
+        else CL_DCF(6);
+#undef CL_DCF
         return (int)cudaGetLastError();
     }
     const int G = ld <= 2 ? 1 : ld <= 4 ? 2 : ld <= 8 ? 4 : ld <= 16 ? 8 : ld <= 32 ? 16 : 32;
@@ -1600,7 +1642,9 @@ int cl_diag_cg_apply(int64_t n, int32_t ld, const double* aval, double rho, doub
     d.n = n; d.ld = ld; d.aval = aval; d.rho = rho; d.beta = beta; d.r = r; d.p = p; d.Wf = Wf; d.Q = Q;
     const int rb = (NT * DC_U) / (ld / 2);
     const int64_t nblk = (n + rb - 1) / rb;
-    const int grid = (int)(nblk > CL_RED_BLOCKS ? CL_RED_BLOCKS : nblk);
+    int64_t wave = (int64_t)resident_blocks((const void*)diag_cg_apply_kernel) * NSM;
+    if (wave > CL_RED_BLOCKS) wave = CL_RED_BLOCKS;
+    const int grid = (int)(nblk > wave ? wave : nblk);
     diag_cg_apply_kernel<<<grid, NT, 0, st>>>(d, ws, dots_out);
     return (int)cudaGetLastError();
 }
@@ -1613,7 +1657,8 @@ int cl_cg_step(int64_t N, double alpha, const double* x_in, double* x_out, const
     if (!aligned16(x_in) || !aligned16(x_out) || !aligned16(p) || !aligned16(r) || !aligned16(Q)) return CL_EARG;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (N == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double), st);
-    cg_step_kernel<<<red_grid(N / 2), NT, 0, st>>>(N / 2, alpha, x_in, x_out, p, r, Q, ws, dots_out);
+    cg_step_kernel<<<occ_grid((const void*)cg_step_kernel, N / 2), NT, 0, st>>>(N / 2, alpha, x_in, x_out, p, r, Q,
+                                                                                ws, dots_out);
     return (int)cudaGetLastError();
 }
 
@@ -1625,7 +1670,8 @@ int cl_cg_step_dev(int64_t N, double qr, const double* pq, const double* x_in, d
     if (!aligned16(x_in) || !aligned16(x_out) || !aligned16(p) || !aligned16(r) || !aligned16(Q)) return CL_EARG;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (N == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double), st);
-    cg_step_dev_kernel<<<red_grid(N / 2), NT, 0, st>>>(N / 2, qr, pq, x_in, x_out, p, r, Q, ws, dots_out);
+    cg_step_dev_kernel<<<occ_grid((const void*)cg_step_dev_kernel, N / 2), NT, 0, st>>>(N / 2, qr, pq, x_in, x_out,
+                                                                                        p, r, Q, ws, dots_out);
     return (int)cudaGetLastError();
 }
 
@@ -1760,11 +1806,12 @@ int cl_diag_alm_update(const cl_diag_update_args* a, double* dots_out, double* w
     for (int j = 0; j < CL_MAXIN; ++j) d.H[j] = j < a->nh ? a->H[j] : nullptr;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int64_t n2 = a->n * (a->ld / 2);
-    const int grid = red_grid(n2);
-    if (a->nh == 0) diag_update_kernel<0><<<grid, NT, 0, st>>>(d, ws, dots_out);
-    else if (a->nh <= 4) diag_update_kernel<4><<<grid, NT, 0, st>>>(d, ws, dots_out);
-    else if (a->nh <= 10) diag_update_kernel<10><<<grid, NT, 0, st>>>(d, ws, dots_out);
-    else diag_update_kernel<CL_MAXIN><<<grid, NT, 0, st>>>(d, ws, dots_out);
+#define CL_DU(NHH) diag_update_kernel<NHH><<<occ_grid((const void*)diag_update_kernel<NHH>, n2), NT, 0, st>>>(d, ws, dots_out)
+    if (a->nh == 0) CL_DU(0);
+    else if (a->nh <= 4) CL_DU(4);
+    else if (a->nh <= 10) CL_DU(10);
+    else CL_DU(CL_MAXIN);
+#undef CL_DU
     return (int)cudaGetLastError();
 }
 
