@@ -50,12 +50,18 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-solver", action="store_true", help="skip the solver-level rates and the G1 solve")
     ap.add_argument("--n-g1", type=int, default=800)
+    ap.add_argument("--graph", choices=("random", "delaunay"), default="random",
+                    help="random: BASELINE configs[2] (default); delaunay: mesh-like graph of degree 6")
+    ap.add_argument("--reorder", action="store_true", help="relabel rows by the solver's RCM locality order")
     ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
                     help="gloo: functional check of the N>1 path with ranks sharing one GPU (no timing value)")
     return ap.parse_args()
 
 
-def workload_name(n, deg):
+def workload_name(n, deg, graph="random", reorder=False):
+    if graph == "delaunay":
+        return (f"MaxCut Delaunay-like mesh n={n:.2e}, degree 6, scrambled labels"
+                + (", RCM locality order" if reorder else ""))
     return f"MaxCut synthetic random sparse graph n={n:.0e}, avg degree ~{deg:g} (BASELINE configs[2])"
 
 
@@ -300,9 +306,18 @@ def run_ours(args, rank, world, local_rank):
     dev = device.default_device()
     halo_bytes = 0
     if world == 1:
-        g = graphs.random_sparse(n, deg=args.deg, seed=args.seed)
+        if args.graph == "delaunay":
+            # the paper's 10^7-scale instances are Delaunay meshes: a triangulated lattice
+            # with scrambled labels, optionally relabelled by the solver's RCM order
+            g = graphs.delaunay_like(n, seed=args.seed)
+            n = g.n
+        else:
+            g = graphs.random_sparse(n, deg=args.deg, seed=args.seed)
         n_edges = int(g.edges_u.size)
         p = problem.build_maxcut(g)
+        if args.reorder:
+            from paper_2407_15049_b200 import reorder
+            p, _ = reorder.permute(p, reorder.locality_order(p))
         ops = linops.build_operators(p, dev=dev)
         r = driver.initial_rank(p.m, p.n)
     else:
@@ -445,7 +460,7 @@ def run_ours(args, rank, world, local_rank):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
-        if n == int(1e7) and abs(args.deg - 6.0) < 1e-9 and ld == 26:
+        if n == int(1e7) and abs(args.deg - 6.0) < 1e-9 and ld == 26 and args.graph == "random" and not args.reorder:
             traffic, traffic_src = int(tj[top]), tj["source"]
     except Exception:
         pass
@@ -466,7 +481,8 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded random graph, random factor/multiplier)",
-        "config": {"workload": workload_name(world * n, args.deg), "n": world * n, "n_per_gpu": n,
+        "config": {"workload": workload_name(world * n, args.deg, args.graph, args.reorder), "n": world * n,
+                   "n_per_gpu": n,
                    "edges": n_edges, "halo_bytes_per_spmm_per_rank": halo_bytes,
                    "rank": r, "ld": ld, "step": "BM gradient pass: SDDMM A(RR^T) + SpMM C R + fused 2 S R",
                    "bytes_per_step": step_bytes,

@@ -68,7 +68,7 @@ def _lanczos_native(op, n, k_max, Q, u, r, h, dev, alphas, betas):
     return k.value
 
 
-def _lanczos_smallest(op, n, seed, max_basis, dev, rows=None):
+def _lanczos_smallest(op, n, seed, max_basis, dev, rows=None, perm=None):
     """spectral.py:28. ``rows`` = (lo, hi, n_global): this rank's block of a
     row-sharded vector; the Gram projections are all-reduced."""
     rng = np.random.default_rng(seed)
@@ -82,6 +82,8 @@ def _lanczos_smallest(op, n, seed, max_basis, dev, rows=None):
     q0 /= np.linalg.norm(q0)
     if rows is not None:
         q0 = q0[rows[0]:rows[1]]
+    if perm is not None:
+        q0 = q0[perm]              # locality-ordered operator: the same start vector, relabelled
     Q[0, :n] = torch.as_tensor(q0).to(dev.dev)
     u = dev.zeros(npad)
     r = dev.zeros(npad)
@@ -130,7 +132,8 @@ def _lanczos_smallest(op, n, seed, max_basis, dev, rows=None):
     return theta, residual, k
 
 
-def smallest_eigenvalue(apply_s, n, tol=1e-7, seed=0, max_basis=300, dev=None, rows=None) -> EigEstimate:
+def smallest_eigenvalue(apply_s, n, tol=1e-7, seed=0, max_basis=300, dev=None, rows=None,
+                        perm=None) -> EigEstimate:
     """Smallest eigenvalue of a self-adjoint operator (spectral.py:67).
 
     ``apply_s`` is a host callback v -> S v (numpy), or a device operator from
@@ -138,9 +141,9 @@ def smallest_eigenvalue(apply_s, n, tol=1e-7, seed=0, max_basis=300, dev=None, r
     """
     dev = dev or default_device()
     op = apply_s if isinstance(apply_s, _DeviceOp) else _host_callback_op(apply_s, dev)
-    theta, residual, k = _lanczos_smallest(op, n, seed, max_basis, dev, rows)
+    theta, residual, k = _lanczos_smallest(op, n, seed, max_basis, dev, rows, perm)
     if residual > tol * (1.0 + abs(theta)):
-        t2, r2, k2 = _lanczos_smallest(op, n, seed + 1, max_basis, dev, rows)
+        t2, r2, k2 = _lanczos_smallest(op, n, seed + 1, max_basis, dev, rows, perm)
         if r2 < residual:
             theta, residual, k = t2, r2, k2
     return EigEstimate(value=theta, residual=residual,
@@ -186,6 +189,7 @@ def dual_infeasibility(problem, ops, lam, tol=1e-7, seed=0):
     rr = getattr(ops, "row_range", None)
     rows = (rr[0], rr[1], problem.n) if rr is not None else None
     n_loc = ops.problem.n
-    est = smallest_eigenvalue(omega_operator(ops, neg, 1.0), n_loc, tol=tol, seed=seed, dev=dev, rows=rows)
+    est = smallest_eigenvalue(omega_operator(ops, neg, 1.0), n_loc, tol=tol, seed=seed, dev=dev, rows=rows,
+                              perm=getattr(ops, "perm", None))
     value = abs(min(0.0, est.value)) / (1.0 + problem.c_vec_norm1)
     return value, est.verified, est.value

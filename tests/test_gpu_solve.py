@@ -97,3 +97,36 @@ def test_determinism_same_seed_bit_identical():
     b = driver.solve(p, driver.SolverConfig(deterministic=True))
     assert a.to_json_dict() == b.to_json_dict()
     assert trace_array(a.trace_rows).tobytes() == trace_array(b.trace_rows).tobytes()
+
+
+def test_locality_reordered_solve_in_envelope_and_unpermuted():
+    """SolverConfig(reorder=True) on the Delaunay-like instance (labels scrambled, RCM
+    order restores locality): same envelope as the plain solve, factors and multipliers
+    returned in the caller's labelling (errors recomputed by the oracle agree)."""
+    from oracle import lrsdp_oracle as O
+    from paper_2407_15049_b200 import driver, reorder
+    z = load("solve_delaunay_45.npz")
+    p = problem_from(z)
+    assert reorder.locality_gain(p, reorder.locality_order(p)) >= 2.0
+    cfg = dict(cfg_of(z))
+    rep = driver.solve(p, driver.SolverConfig(**cfg, reorder=True))
+    objs = np.append(z["ulp_objective"], float(z["objective"]))
+    statuses = set(z["ulp_status"].tolist()) | {str(z["status"])}
+    assert rep.status in statuses
+    lo, hi = objs.min(), objs.max()
+    if rep.status == "optimal":
+        assert lo - 1e-6 * hi <= rep.objective <= hi + 1e-6 * hi
+    r = rep.rank_final
+    e = O.errors(O.OracleOps(p), rep.U[:, :r].cpu().numpy(), rep.V[:, :r].cpu().numpy(), rep.lam.cpu().numpy())
+    assert abs(e["err1"] - rep.err1) <= 1e-12 + 1e-9 * rep.err1
+    assert abs(e["err3"] - rep.err3) <= 1e-12 + 1e-9 * rep.err3
+    assert abs(-e["obj"] - rep.objective) <= 1e-9 * abs(rep.objective)
+
+
+def test_reorder_skipped_for_random_graphs():
+    from paper_2407_15049_b200 import driver
+    z = load("solve_g1_like.npz")
+    p = problem_from(z)
+    a = driver.solve(p, driver.SolverConfig(deterministic=True))
+    b = driver.solve(p, driver.SolverConfig(deterministic=True, reorder=True))
+    assert trace_array(a.trace_rows).tobytes() == trace_array(b.trace_rows).tobytes()

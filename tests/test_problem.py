@@ -140,3 +140,25 @@ def test_problem_norms_match_oracle(case):
     b1, binf, cn = O.norms(p)
     assert (p.b_norm1, p.b_norminf, p.c_vec_norm1) == (b1, binf, cn)
     assert p.nnz_a_full() == O.nnz_a_full(p)
+
+
+def test_locality_permutation_is_a_relabelling():
+    """reorder.permute: objective and constraint values invariant under the relabelling."""
+    from paper_2407_15049_b200 import graphs, problem, reorder
+    from oracle import lrsdp_oracle as O
+    for p in (problem.build_maxcut(graphs.delaunay_like(400, seed=2)),
+              problem.build_matrix_completion(graphs.random_completion(20, 15, 120, seed=2))):
+        perm = reorder.locality_order(p)
+        q, inv = reorder.permute(p, perm)
+        assert np.array_equal(inv[perm], np.arange(p.n))
+        rng = np.random.default_rng(0)
+        U, V = rng.standard_normal((p.n, 3)), rng.standard_normal((p.n, 3))
+        oa, ob = O.OracleOps(p), O.OracleOps(q)
+        assert abs(oa.objective(U, V) - ob.objective(U[perm], V[perm])) <= 1e-10 * (1 + abs(oa.objective(U, V)))
+        ax, bx = oa.A(U, V), ob.A(U[perm], V[perm])
+        if reorder.is_diag(p):
+            bx = bx[inv]
+        assert np.abs(ax - bx).max() <= 1e-12 * (1 + np.abs(ax).max())
+        assert reorder.is_diag(q) == reorder.is_diag(p)
+    g = problem.build_maxcut(graphs.delaunay_like(900, seed=3))
+    assert reorder.locality_gain(g, reorder.locality_order(g)) > 2.0
