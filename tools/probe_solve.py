@@ -1,6 +1,6 @@
 """Time one device MaxCut solve on a synthetic graph (development probe, not the bench).
 
-    python tools/probe_solve.py N DEG [time_limit]
+    python tools/probe_solve.py N DEG [time_limit] [random|delaunay] [reorder]
 """
 import os
 import sys
@@ -14,19 +14,21 @@ from paper_2407_15049_b200 import driver, graphs, linops, problem  # noqa: E402
 n = int(float(sys.argv[1]))
 deg = float(sys.argv[2])
 tl = float(sys.argv[3]) if len(sys.argv) > 3 else 600.0
+kind = sys.argv[4] if len(sys.argv) > 4 else "random"
+reorder = len(sys.argv) > 5 and sys.argv[5] == "reorder"
 t = time.perf_counter()
-g = graphs.random_sparse(n, deg=deg, seed=0)
+g = graphs.delaunay_like(n, seed=0) if kind == "delaunay" else graphs.random_sparse(n, deg=deg, seed=0)
 t_g = time.perf_counter() - t
 t = time.perf_counter()
 p = problem.build_maxcut(g)
 t_p = time.perf_counter() - t
 t = time.perf_counter()
-ops = linops.build_operators(p)
+ops = None if reorder else linops.build_operators(p)
 torch.cuda.synchronize()
 t_o = time.perf_counter() - t
-print(f"n={n} edges={g.edges_u.size} gen {t_g:.2f}s build_maxcut {t_p:.2f}s build_operators {t_o:.2f}s", flush=True)
+print(f"{kind} reorder={reorder} n={n} edges={g.edges_u.size} gen {t_g:.2f}s build_maxcut {t_p:.2f}s build_operators {t_o:.2f}s", flush=True)
 t = time.perf_counter()
-rep = driver.solve(p, driver.SolverConfig(time_limit=tl), ops=ops)
+rep = driver.solve(p, driver.SolverConfig(time_limit=tl, reorder=reorder), ops=ops)
 torch.cuda.synchronize()
 dt = time.perf_counter() - t
 print(f"solve {dt:.2f}s status {rep.status} obj {rep.objective:.10g} err1 {rep.err1:.2e} err3 {rep.err3:.2e} "
