@@ -199,6 +199,18 @@ int cl_cg_step(int64_t N, double alpha, const double* x_in, double* x_out, const
 int cl_cg_step_dev(int64_t N, double qr, const double* pq, const double* x_in, double* x_out, const double* p,
                    double* r, const double* Q, double* dots_out, double* ws, void* stream);
 
+/* The same CG iteration with Q never stored: cl_diag_cg_apply_rows writes the
+ * per-row coefficient coef_c = rho a_c y_c (n doubles) instead of Q, and
+ * cl_diag_cg_step rebuilds Q_c = coef_c Wf_c + rho p_c with the same expression
+ * while it updates x and r, so the results are bit-identical to the stored-Q
+ * pair and the pass streams one n x ld operand less. alpha is taken as given,
+ * or as qr / *pq on the device when pq != NULL (semantics of cl_cg_step_dev). */
+int cl_diag_cg_apply_rows(int64_t n, int32_t ld, const double* aval, double rho, double beta, const double* r,
+                          double* p, const double* Wf, double* coef, double* dots_out, double* ws, void* stream);
+int cl_diag_cg_step(int64_t n, int32_t ld, double rho, const double* coef, const double* Wf, double alpha,
+                    double qr, const double* pq, const double* x_in, double* x_out, const double* p, double* r,
+                    double* dots_out, double* ws, void* stream);
+
 /* cl_constraint_eval for a row block of a row-sharded solve: factor row
  * index >= nown of operand k (X1, Y1, X2, Y2, X3, Y3) reads ghosts[k][row-nown]
  * (the halo rows gathered from the other ranks). */

@@ -56,6 +56,7 @@ class HalfStep:
         self.r = dev.empty(n, ld)
         self.p = dev.empty(n, ld)
         self.Q = dev.empty(n, ld)
+        self.coef = self.Q.view(-1)[:n]      # per-row CG coefficients (Q itself is not stored in the loop)
         self.nlam = dev.empty(m)
         self.rhob = dev.empty(m)
 
@@ -163,14 +164,14 @@ class HalfStep:
         its = 0
         beta = 0.0
         for k in range(max_iter):
-            dev.diag_cg_apply(ops.diag_aval, self.ld, rho, p, Wf, Q, r=r, beta=beta, at=A + 1)
+            dev.diag_cg_apply_rows(ops.diag_aval, self.ld, rho, p, Wf, self.coef, r=r, beta=beta, at=A + 1)
             pq = float(dev.fetch(A + 2)[A + 1])
             if not math.isfinite(pq):
                 raise DivergedError("CG produced non-finite curvature", last_iterate=xs)
             if pq <= 0.0:
                 raise SpdViolationError(f"non-positive curvature {pq:.3e} in CG (operator not SPD)")
             alpha = qr / pq
-            dev.cg_step(alpha, xs, x, p, r, Q, at=A + 2)
+            dev.diag_cg_step(self.ld, rho, self.coef, Wf, xs, x, p, r, alpha=alpha, at=A + 2)
             xs = x
             qn = float(dev.fetch(A + 3)[A + 2])
             rnorm = math.sqrt(qn)
@@ -432,12 +433,12 @@ def _admm_step_diag_py(state, ops, scale, cg_cap, rel_floor, coeff, hs, pool):
             return 0, eps, 0, rnorm, 0, 0.0, 1
         its, beta, xs = 0, 0.0, x0
         for k in range(cg_cap):
-            dev.diag_cg_apply(ops.diag_aval, ld, rho, hs.p, Wf, hs.Q, r=hs.r, beta=beta, at=S(4))
+            dev.diag_cg_apply_rows(ops.diag_aval, ld, rho, hs.p, Wf, hs.coef, r=hs.r, beta=beta, at=S(4))
             pq = float(fetch(5)[S(4)])
             if not math.isfinite(pq) or pq <= 0.0:
                 return (2 if math.isfinite(pq) else 1), eps, its, rnorm, int(xs is x), pq, 0
             alpha = qr / pq
-            dev.cg_step(alpha, xs, x, hs.p, hs.r, hs.Q, at=S(5))
+            dev.diag_cg_step(ld, rho, hs.coef, Wf, xs, x, hs.p, hs.r, alpha=alpha, at=S(5))
             xs = x
             qn = float(fetch(6)[S(5)])
             rnorm = math.sqrt(qn)

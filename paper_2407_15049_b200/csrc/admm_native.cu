@@ -142,9 +142,11 @@ int cg_loop(Ctx& c, const double* x0, double* x, const double* Wf, double* r, do
     for (int k = 0; k < a->cg_cap; ++k) {
         // operator application, then the update with alpha = qr / pq taken on the device:
         // pq and the new <r, r> are read together (one synchronize per iteration)
-        CL_TRY(c, cl_diag_cg_apply(a->n, a->ld, a->aval, a->rho, beta, r, a->p, Wf, a->Q, a->slab + S_PQ, a->ws,
-                                   (void*)c.st));
-        CL_TRY(c, cl_cg_step_dev(c.N, qr, a->slab + S_PQ, xs, x, a->p, r, a->Q, a->slab + S_QN, a->ws, (void*)c.st));
+        // (Q is never stored: its first n doubles hold the per-row coefficients it is rebuilt from)
+        CL_TRY(c, cl_diag_cg_apply_rows(a->n, a->ld, a->aval, a->rho, beta, r, a->p, Wf, a->Q, a->slab + S_PQ,
+                                        a->ws, (void*)c.st));
+        CL_TRY(c, cl_diag_cg_step(a->n, a->ld, a->rho, a->Q, Wf, 0.0, qr, a->slab + S_PQ, xs, x, a->p, r,
+                                  a->slab + S_QN, a->ws, (void*)c.st));
         if (!fetch(c, S_PQ, 2)) return 0;
         const double pq = H(c, S_PQ);
         if (!isfinite(pq) || pq <= 0.0) {          // the device update was skipped

@@ -1183,7 +1183,8 @@ struct DiagCg {
     const double* r;      // p <- r + beta p first (NULL: p is read as is)
     double* p;
     const double* Wf;
-    double* Q;
+    double* Q;            // NULL: only the per-row coefficients are written
+    double* coef_g;       // per-row rho a_c y_c (NULL: not written)
 };
 
 // One operator application of the half-step system (admm.py:45):
@@ -1227,6 +1228,7 @@ __global__ void __launch_bounds__(NT) diag_cg_apply_kernel(DiagCg a, double* ws,
             for (int q = 0; q < h2; ++q) sdot += part[rr * h2 + q];
             const double av = __ldg(a.aval + r0 + rr);
             coef[rr] = a.rho * (av * (av * sdot));      // rho * a_c * y_c
+            if (a.coef_g != nullptr) a.coef_g[r0 + rr] = coef[rr];
         }
         __syncthreads();
 #pragma unroll
@@ -1237,7 +1239,7 @@ __global__ void __launch_bounds__(NT) diag_cg_apply_kernel(DiagCg a, double* ws,
                 double2 q;
                 q.x = fma(c, wv[u].x, a.rho * pv[u].x);
                 q.y = fma(c, wv[u].y, a.rho * pv[u].y);
-                st2(a.Q + 2 * (base + e), q);
+                if (a.Q != nullptr) st2(a.Q + 2 * (base + e), q);
                 dacc[0] += dot2(pv[u], q);
             }
         }
@@ -1277,6 +1279,49 @@ __global__ void __launch_bounds__(NT) cg_step_dev_kernel(int64_t n2, double qr, 
         const double2 rv = axpy2(-alpha, ld2cs(Q + off), ld2cs(r + off));
         st2(r + off, rv);
         dacc[0] += dot2(rv, rv);
+    }
+    reduce_and_finish<1>(dacc, 1, ws, dots_out);
+}
+
+// CG update with Q rebuilt from the per-row coefficients of diag_cg_apply (Q_c = coef_c Wf_c + rho p_c,
+// the same expression, so bit-identical to reading a stored Q): x_out = x_in + alpha p; r -= alpha Q;
+// dots[0] = <r, r>. One operand less to stream than writing Q and reading it back. alpha is taken
+// from the host, or as qr / *pq on the device when pq != NULL (skip semantics of cg_step_dev).
+__global__ void __launch_bounds__(NT) diag_cg_step_kernel(int64_t n, int ld, double rho, const double* coef,
+                                                          const double* Wf, double alpha, double qr,
+                                                          const double* pq_ptr, const double* x_in, double* x_out,
+                                                          const double* p, double* r, double* ws, double* dots_out) {
+    if (pq_ptr != nullptr) {
+        const double pq = *pq_ptr;
+        if (!(isfinite(pq) && pq > 0.0)) return;
+        alpha = qr / pq;
+    }
+    const int h2 = ld >> 1;
+    const int rb = (NT * DC_U) / h2;
+    const int64_t nblk = (n + rb - 1) / rb;
+    double dacc[1] = {0.0};
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int64_t r0 = blk * rb;
+        const int nr = (int)min((int64_t)rb, n - r0);
+        const int units = nr * h2;
+        const int64_t base = r0 * (int64_t)h2;
+#pragma unroll
+        for (int u = 0; u < DC_U; ++u) {
+            const int e = threadIdx.x + u * NT;
+            if (e < units) {
+                const int64_t off = 2 * (base + e);
+                const double c = __ldg(coef + r0 + e / h2);
+                const double2 wv = ld2cs(Wf + off);
+                const double2 pv = ld2cs(p + off);
+                double2 q;
+                q.x = fma(c, wv.x, rho * pv.x);
+                q.y = fma(c, wv.y, rho * pv.y);
+                st2(x_out + off, axpy2(alpha, pv, ld2cs(x_in + off)));
+                const double2 rv = axpy2(-alpha, q, ld2cs(r + off));
+                st2(r + off, rv);
+                dacc[0] += dot2(rv, rv);
+            }
+        }
     }
     reduce_and_finish<1>(dacc, 1, ws, dots_out);
 }
@@ -1640,12 +1685,50 @@ int cl_diag_cg_apply(int64_t n, int32_t ld, const double* aval, double rho, doub
     if (n == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double), st);
     DiagCg d;
     d.n = n; d.ld = ld; d.aval = aval; d.rho = rho; d.beta = beta; d.r = r; d.p = p; d.Wf = Wf; d.Q = Q;
+    d.coef_g = nullptr;
     const int rb = (NT * DC_U) / (ld / 2);
     const int64_t nblk = (n + rb - 1) / rb;
     int64_t wave = (int64_t)resident_blocks((const void*)diag_cg_apply_kernel) * NSM;
     if (wave > CL_RED_BLOCKS) wave = CL_RED_BLOCKS;
     const int grid = (int)(nblk > wave ? wave : nblk);
     diag_cg_apply_kernel<<<grid, NT, 0, st>>>(d, ws, dots_out);
+    return (int)cudaGetLastError();
+}
+
+static int diag_cg_grid(const void* k, int64_t n, int32_t ld) {
+    const int rb = (NT * DC_U) / (ld / 2);
+    const int64_t nblk = (n + rb - 1) / rb;
+    int64_t wave = (int64_t)resident_blocks(k) * NSM;
+    if (wave > CL_RED_BLOCKS) wave = CL_RED_BLOCKS;
+    return (int)(nblk > wave ? wave : nblk);
+}
+
+int cl_diag_cg_apply_rows(int64_t n, int32_t ld, const double* aval, double rho, double beta, const double* r,
+                          double* p, const double* Wf, double* coef, double* dots_out, double* ws, void* stream) {
+    if (n < 0 || ld < 2 || (ld & 1) || ld / 2 > NT * DC_U || dots_out == nullptr || ws == nullptr) return CL_EARG;
+    if (n > 0 && (aval == nullptr || p == nullptr || Wf == nullptr || coef == nullptr)) return CL_EARG;
+    if (!aligned16(p) || !aligned16(Wf) || (r != nullptr && !aligned16(r))) return CL_EARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (n == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double), st);
+    DiagCg d;
+    d.n = n; d.ld = ld; d.aval = aval; d.rho = rho; d.beta = beta; d.r = r; d.p = p; d.Wf = Wf; d.Q = nullptr;
+    d.coef_g = coef;
+    diag_cg_apply_kernel<<<diag_cg_grid((const void*)diag_cg_apply_kernel, n, ld), NT, 0, st>>>(d, ws, dots_out);
+    return (int)cudaGetLastError();
+}
+
+int cl_diag_cg_step(int64_t n, int32_t ld, double rho, const double* coef, const double* Wf, double alpha,
+                    double qr, const double* pq, const double* x_in, double* x_out, const double* p, double* r,
+                    double* dots_out, double* ws, void* stream) {
+    if (n < 0 || ld < 2 || (ld & 1) || ld / 2 > NT * DC_U || dots_out == nullptr || ws == nullptr) return CL_EARG;
+    if (n > 0 && (coef == nullptr || Wf == nullptr || x_in == nullptr || x_out == nullptr || p == nullptr ||
+                  r == nullptr))
+        return CL_EARG;
+    if (!aligned16(Wf) || !aligned16(x_in) || !aligned16(x_out) || !aligned16(p) || !aligned16(r)) return CL_EARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (n == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double), st);
+    diag_cg_step_kernel<<<diag_cg_grid((const void*)diag_cg_step_kernel, n, ld), NT, 0, st>>>(
+        n, ld, rho, coef, Wf, alpha, qr, pq, x_in, x_out, p, r, ws, dots_out);
     return (int)cudaGetLastError();
 }
 

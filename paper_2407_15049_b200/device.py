@@ -201,6 +201,22 @@ class Device:
         self.launches += 1
         check(rc, "cl_diag_cg_apply")
 
+    def diag_cg_apply_rows(self, aval, ld, rho, p, Wf, coef, r=None, beta=0.0, at=0):
+        """diag_cg_apply writing the per-row coefficients rho a_c y_c to coef (n doubles) instead of Q."""
+        rc = self.lib.cl_diag_cg_apply_rows(int(p.shape[0]), int(ld), ptr(aval), float(rho), float(beta), ptr(r),
+                                            ptr(p), ptr(Wf), ptr(coef), self.slot(at), ptr(self.ws), self.sp)
+        self.launches += 1
+        check(rc, "cl_diag_cg_apply_rows")
+
+    def diag_cg_step(self, ld, rho, coef, Wf, x_in, x_out, p, r, alpha=0.0, qr=0.0, pq_at=None, at=0):
+        """CG update with Q = coef Wf + rho p rebuilt per row; alpha = qr / slab[pq_at] on the
+        device when pq_at is given; <r, r> -> slab[at]."""
+        rc = self.lib.cl_diag_cg_step(int(p.shape[0]), int(ld), float(rho), ptr(coef), ptr(Wf), float(alpha),
+                                      float(qr), None if pq_at is None else self.slot(pq_at), ptr(x_in), ptr(x_out),
+                                      ptr(p), ptr(r), self.slot(at), ptr(self.ws), self.sp)
+        self.launches += 1
+        check(rc, "cl_diag_cg_step")
+
     def _halo_struct(self, pat, X, ld):
         P = pat.struct(c_coeff=1.0)
         halo = getattr(pat, "halo", None)

@@ -364,3 +364,40 @@ def test_cg_step_dev_alpha_and_rejected_curvature(dev, pq):
     else:
         assert torch.equal(x, x0) and torch.equal(r, r0)
     del ctypes
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,ld", [(0, 4), (1, 2), (777, 26), (4099, 64), (300, 202)])
+def test_diag_cg_rows_pair_matches_stored_q(dev, n, ld):
+    """cl_diag_cg_apply_rows + cl_diag_cg_step (Q rebuilt per row, never stored) give the
+    same p, x and r bit for bit as cl_diag_cg_apply + cl_cg_step with a stored Q, and the
+    same <p, Q>; host and device alpha agree."""
+    import torch
+    from paper_2407_15049_b200.device import ptr
+    rng = np.random.default_rng(n + ld)
+    T = lambda: torch.as_tensor(rng.standard_normal((n, ld))).cuda().contiguous()  # noqa: E731
+    aval = torch.as_tensor(rng.standard_normal(n) + 2.0).cuda()
+    Wf, p0, r0, x0 = T(), T(), T(), T()
+    rho, beta = 1.7, 0.37
+    # stored-Q reference
+    p1, r1, x1, Q = p0.clone(), r0.clone(), x0.clone(), torch.empty_like(p0)
+    dev.diag_cg_apply(aval, ld, rho, p1, Wf, Q, r=r1, beta=beta, at=800)
+    pq = float(dev.fetch(801)[800])
+    alpha = 2.3 / pq if n else 0.0
+    dev.cg_step(alpha, x1, x1, p1, r1, Q, at=801)
+    rr1 = float(dev.fetch(802)[801])
+    # row-coefficient pair, host alpha then device alpha
+    for dev_alpha in (False, True):
+        p2, r2, x2 = p0.clone(), r0.clone(), x0.clone()
+        coef = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
+        dev.diag_cg_apply_rows(aval, ld, rho, p2, Wf, coef, r=r2, beta=beta, at=810)
+        assert float(dev.fetch(811)[810]) == pq
+        if dev_alpha and n:
+            dev.diag_cg_step(ld, rho, coef, Wf, x2, x2, p2, r2, qr=2.3, pq_at=810, at=811)
+        else:
+            dev.diag_cg_step(ld, rho, coef, Wf, x2, x2, p2, r2, alpha=alpha, at=811)
+        torch.cuda.synchronize()
+        assert torch.equal(p1, p2) and torch.equal(x1, x2) and torch.equal(r1, r2)
+        rr2 = float(dev.fetch(812)[811])
+        assert abs(rr2 - rr1) <= 1e-12 * max(rr1, 1e-300)
+    del ptr
