@@ -15,7 +15,9 @@
 // kept). The V half-step's start and the step end are therefore launched
 // right after the U half-step's start, assuming U (then V) is kept, and the
 // decisions of all three are read at ONE synchronize. When a CG does iterate
-// the speculative work is recomputed with the new factor. Every kernel that
+// the speculative work is recomputed with the new factor. Speculation trades
+// whole passes for synchronizes, so it is used only while a pass is cheaper
+// than a host round trip (n*ld <= SPEC_MAX_ELEMS); larger steps run in order. Every kernel that
 // counts sees exactly the operands of the sequential order, so the iterates
 // are bit-identical to the Python-driven twin (admm._admm_step_diag_py,
 // tests/test_gpu_admm_native.py).
@@ -28,6 +30,8 @@
 #include "culorads.h"
 
 namespace {
+
+constexpr int64_t SPEC_MAX_ELEMS = int64_t(1) << 20;   // 8 MB per factor: a pass costs about a round trip
 
 struct Ctx {
     const cl_admm_diag_args* a;
@@ -219,11 +223,17 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
         lincomb(c, a->nlam, 2, in, cf, a->n, -1, false);    // nlam = rho b - lam (HalfStep.rhs)
     }
 
-    // U start; V start and step end speculatively assuming U (then V) is kept; one synchronize
+    // U start; at small n also the V start and the step end, speculatively assuming U (then V)
+    // is kept, read at one synchronize
+    const bool spec = c.N <= SPEC_MAX_ELEMS;
     cg_init(c, a->U, a->V, a->r, S_RHSU);
-    cg_init(c, a->V, a->U, a->r_v, S_RHSV);
-    step_end(c, a->U, a->V);
-    if (!fetch(c, S_RHSU, S_END - S_RHSU)) RET_RC();
+    if (spec) {
+        cg_init(c, a->V, a->U, a->r_v, S_RHSV);
+        step_end(c, a->U, a->V);
+        if (!fetch(c, S_RHSU, S_END - S_RHSU)) RET_RC();
+    } else if (!fetch(c, S_RHSU, 2)) {
+        RET_RC();
+    }
     int last_is_x = 0;
     double pqb = 0.0;
 
@@ -247,6 +257,9 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
             fail(out, 3, 0, 1, 0.0);
             return CL_OK;
         }
+    } else if (!spec) {
+        cg_init(c, a->V, a->U, a->r_v, S_RHSV);
+        if (!fetch(c, S_RHSV, 2)) RET_RC();
     }
     out->u_reused = u_kept;
     const double* Uc = u_kept ? a->U : a->U_new;
@@ -271,7 +284,7 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
 
     // step end (admm.py:165-166 and the gap inputs of admm.py:212-217), written out of place
     // into ax / lam_new so that a non-finite V leaves the multiplier untouched
-    if (!(u_kept && v_kept)) {
+    if (!(u_kept && v_kept && spec)) {
         step_end(c, Uc, Vc);
         if (!fetch(c, S_XXV, S_E0 + 3 - S_XXV)) RET_RC();
         if (!v_kept && !isfinite(H(c, S_XXV))) {

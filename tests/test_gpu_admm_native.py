@@ -35,7 +35,7 @@ def _run_steps(native, p, steps, seed=0, r=6):
         admm.NATIVE = True
 
 
-@pytest.mark.parametrize("r", [6, 70])
+@pytest.mark.parametrize("r", [6, 70, 400])     # r = 400: n*ld > 2^20, the in-order (unspeculated) step
 def test_native_step_bit_identical_to_python_step(r):
     from paper_2407_15049_b200 import graphs, problem
     p = problem.build_maxcut(graphs.random_sparse(3000, deg=6.0, seed=4))

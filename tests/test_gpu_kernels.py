@@ -379,6 +379,13 @@ def test_diag_cg_rows_pair_matches_stored_q(dev, n, ld):
     aval = torch.as_tensor(rng.standard_normal(n) + 2.0).cuda()
     Wf, p0, r0, x0 = T(), T(), T(), T()
     rho, beta = 1.7, 0.37
+    if n == 0:            # empty problem: both calls succeed and report a zero dot
+        coef = torch.empty(1, dtype=torch.float64, device="cuda")
+        dev.slab[810:812] = 5.0
+        dev.diag_cg_apply_rows(aval, ld, rho, p0, Wf, coef, r=r0, beta=beta, at=810)
+        dev.diag_cg_step(ld, rho, coef, Wf, x0, x0, p0, r0, alpha=1.0, at=811)
+        assert list(dev.fetch(812)[810:812]) == [0.0, 0.0]
+        return
     # stored-Q reference
     p1, r1, x1, Q = p0.clone(), r0.clone(), x0.clone(), torch.empty_like(p0)
     dev.diag_cg_apply(aval, ld, rho, p1, Wf, Q, r=r1, beta=beta, at=800)
