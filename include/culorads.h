@@ -171,13 +171,20 @@ int cl_single_entry_apply(int64_t nrows, const int64_t* indptr, const int32_t* i
  *     nlam = rho b - lam) and the initial CG residual r = rhs - Q(x0) with
  *     Q(x0) = rho (a y Wf + x0), y = a <x0, Wf>  (admm.py:45/72) -- rhs and Q are
  *     never stored; dots_out[0] = ||rhs||^2, dots_out[1] = ||r||^2.
+ *     cwf != NULL also stores C Wf itself (n x ld).
  *   cl_diag_admm_step_end: <C V, U> (admm.py:215), ax = A(U V^T), the residual
  *     ax - b and the dual ascent lam_new = lam + rho (ax - b) (admm.py:165-166);
  *     dots_out[0] = <C V, U>, [1] = ||ax - b||^2, [2] = lam_new . b.
+ *   cl_diag_admm_step_end_rows: the same step end as one streaming pass, with the
+ *     objective taken as <C U, V> from the C U the V half-step's start stored
+ *     (cl_diag_admm_cg_init with Wf = U, cwf = CU): no second SpMM, no halo.
  * C carries cv values (and ghost rows in a row-sharded solve). */
 int cl_diag_admm_cg_init(const cl_pattern* C, const double* Wf, const double* x0, int32_t ld, double scale, double rho,
-                         const double* nlam, const double* aval, double* r, double* dots_out, double* ws,
+                         const double* nlam, const double* aval, double* r, double* cwf, double* dots_out, double* ws,
                          void* stream);
+int cl_diag_admm_step_end_rows(int64_t n, int32_t ld, const double* CU, const double* U, const double* V,
+                               const double* aval, const double* b, const double* lam, double rho, double* ax,
+                               double* lam_new, double* dots_out, double* ws, void* stream);
 int cl_diag_admm_step_end(const cl_pattern* C, const double* U, const double* V, int32_t ld, const double* aval,
                           const double* b, const double* lam, double rho, double* ax, double* lam_new, double* dots_out,
                           double* ws, void* stream);
@@ -283,7 +290,8 @@ typedef struct {
     double* r;                 /* CG residual of the U half-step, n x ld */
     double* r_v;               /* CG residual of the V half-step (started speculatively) */
     double* p;                 /* CG direction / operator output, n x ld */
-    double* Q;
+    double* Q;                 /* n x ld; its first n doubles hold the CG's per-row coefficients */
+    double* cu;                /* C U_new, n x ld: written by the V half-step's start, read by the step end */
     double* nlam;              /* m-vector scratch */
     double* res;               /* m-vector scratch */
     cl_pattern cpat;           /* C (cv values) */

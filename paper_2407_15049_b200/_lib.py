@@ -27,7 +27,7 @@ CL_EARG = 1001
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint_eval_halo",
            "cl_diag_constraint_eval", "cl_sddmm",
            "cl_gather_rows", "cl_diag_cg_apply", "cl_diag_cg_apply_rows", "cl_diag_cg_step", "cl_cg_step", "cl_cg_step_dev", "cl_admm_step_diag", "cl_alm_inner_diag",
-           "cl_diag_admm_cg_init", "cl_diag_admm_step_end", "cl_single_entry_apply", "cl_lanczos_loop",
+           "cl_diag_admm_cg_init", "cl_diag_admm_step_end", "cl_diag_admm_step_end_rows", "cl_single_entry_apply", "cl_lanczos_loop",
            "cl_pattern_assemble",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
            "cl_set_l2_fetch_granularity", "cl_get_l2_fetch_granularity", "cl_version", "cl_device_ok")
@@ -70,7 +70,7 @@ class AdmmDiagArgs(ctypes.Structure):
     _fields_ = [("n", I64), ("ld", I32), ("aval", P), ("b", P), ("lam", P), ("lam_new", P), ("ax", P),
                 ("ax_valid", I32),
                 ("pnorm2_known", D), ("U", P), ("V", P), ("U_new", P), ("V_new", P),
-                ("r", P), ("r_v", P), ("p", P), ("Q", P), ("nlam", P), ("res", P),
+                ("r", P), ("r_v", P), ("p", P), ("Q", P), ("cu", P), ("nlam", P), ("res", P),
                 ("cpat", Pattern), ("rho", D), ("scale", D), ("binf", D), ("rel_floor", D),
                 ("primal_coeff", D), ("cg_cap", I32), ("slab", P), ("host", P), ("ws", P), ("stream", P)]
 
@@ -126,7 +126,8 @@ def _declare(lib):
     lib.cl_diag_cg_step.argtypes = [I64, I32, D, P, P, D, D, P, P, P, P, P, P, P, P]
     lib.cl_admm_step_diag.argtypes = [ctypes.POINTER(AdmmDiagArgs), ctypes.POINTER(AdmmStepStats)]
     lib.cl_alm_inner_diag.argtypes = [ctypes.POINTER(AlmInnerArgs), ctypes.POINTER(AlmInnerStats)]
-    lib.cl_diag_admm_cg_init.argtypes = [ctypes.POINTER(Pattern), P, P, I32, D, D, P, P, P, P, P, P]
+    lib.cl_diag_admm_cg_init.argtypes = [ctypes.POINTER(Pattern), P, P, I32, D, D, P, P, P, P, P, P, P]
+    lib.cl_diag_admm_step_end_rows.argtypes = [I64, I32, P, P, P, P, P, P, D, P, P, P, P, P]
     lib.cl_diag_admm_step_end.argtypes = [ctypes.POINTER(Pattern), P, P, I32, P, P, P, D, P, P, P, P, P]
     lib.cl_single_entry_apply.argtypes = [I64, P, P, P, I32, P, P, D, P, P, P, P]
     lib.cl_pattern_assemble.argtypes = [ctypes.POINTER(Pattern), P, P]

@@ -57,8 +57,15 @@ class HalfStep:
         self.p = dev.empty(n, ld)
         self.Q = dev.empty(n, ld)
         self.coef = self.Q.view(-1)[:n]      # per-row CG coefficients (Q itself is not stored in the loop)
+        self.cu = None
         self.nlam = dev.empty(m)
         self.rhob = dev.empty(m)
+
+    def cu_buffer(self):
+        """C U of the diagonal ADMM step (written by the V half-step's start, read by the step end)."""
+        if self.cu is None:
+            self.cu = self.dev.empty(self.n, self.ld)
+        return self.cu
 
     def apply(self, W, Wf, rho, out, dot_with=None, at=None):
         """out = rho*(A*(A(W Wf^T)) Wf + W); optional <dot_with, out> -> slab[at]."""
@@ -342,6 +349,7 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
         hs.r_v = dev.empty(n, ld)
     a.U, a.V, a.U_new, a.V_new = state.U.data_ptr(), state.V.data_ptr(), U_new.data_ptr(), V_new.data_ptr()
     a.r, a.r_v, a.p, a.Q = hs.r.data_ptr(), hs.r_v.data_ptr(), hs.p.data_ptr(), hs.Q.data_ptr()
+    a.cu = hs.cu_buffer().data_ptr()
     nlam = hs.nlam
     a.nlam, a.res = nlam.data_ptr(), hs.y.data_ptr()
     a.cpat = ops.c_mat.cpat.struct(c_coeff=1.0)
@@ -419,9 +427,9 @@ def _admm_step_diag_py(state, ops, scale, cg_cap, rel_floor, coeff, hs, pool):
     rel = mn if mn > rel_floor else rel_floor
     dev.lincomb(hs.nlam, [ops.b, lam], [rho, -1.0])
 
-    def half(x0, x, Wf, xx_prev):
+    def half(x0, x, Wf, xx_prev, cw=None):
         """-> (status, eps, its, rnorm, last_is_x, pq, kept); status 4: previous iterate not finite"""
-        dev.diag_admm_cg_init(cpat, Wf, x0, ld, scale, rho, hs.nlam, ops.diag_aval, hs.r, at=S(1))
+        dev.diag_admm_cg_init(cpat, Wf, x0, ld, scale, rho, hs.nlam, ops.diag_aval, hs.r, at=S(1), cw=cw)
         h = fetch(4 if xx_prev else 3)
         if xx_prev and not math.isfinite(float(h[S(3)])):
             return 4, 0.0, 0, 0.0, 0, 0.0, 0
@@ -465,7 +473,8 @@ def _admm_step_diag_py(state, ops, scale, cg_cap, rel_floor, coeff, hs, pool):
     Uc = state.U if st_u[6] else U_new
     if not st_u[6]:
         dev.lincomb(None, [U_new], [0.0], dots=[(0, 0)], at=S(3))
-    st_v = half(state.V, V_new, Uc, not st_u[6])
+    cu = hs.cu_buffer()
+    st_v = half(state.V, V_new, Uc, not st_u[6], cw=cu)          # also stores C Uc for the step end
     if st_v[0] == 4:
         raise DivergedError("CG iterate diverged", last_iterate=U_new)
     if st_v[0]:
@@ -474,7 +483,7 @@ def _admm_step_diag_py(state, ops, scale, cg_cap, rel_floor, coeff, hs, pool):
     if not st_v[6]:
         dev.lincomb(None, [V_new], [0.0], dots=[(0, 0)], at=S(7))
     lam_new = hs.lam_spare if getattr(hs, "lam_spare", None) is not None else dev.empty(p.m)
-    dev.diag_admm_step_end(cpat, Uc, Vc, ld, ops.diag_aval, ops.b, lam, rho, ax, lam_new, at=S(10))
+    dev.diag_admm_step_end_rows(cu, Uc, Vc, ld, ops.diag_aval, ops.b, lam, rho, ax, lam_new, at=S(10))
     h = fetch(13)
     if not st_v[6] and not math.isfinite(float(h[S(7)])):
         raise DivergedError("CG iterate diverged", last_iterate=V_new)

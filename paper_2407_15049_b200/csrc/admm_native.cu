@@ -7,9 +7,10 @@
 // (admm.py:65), the dual ascent -- between launches of the fused kernels:
 //
 //   cl_diag_admm_cg_init   rhs + initial CG residual of a half-step
-//   cl_diag_cg_apply       CG operator (+ deferred direction update)
-//   cl_cg_step             x/r update
-//   cl_diag_admm_step_end  objective, A(UV^T), residual, dual ascent, lam.b
+//   cl_diag_cg_apply_rows  CG operator (+ deferred direction update)
+//   cl_diag_cg_step        x/r update
+//   cl_diag_admm_step_end_rows  objective, A(UV^T), residual, dual ascent, lam.b
+//                          (streams the C U the V start stored: no second SpMM)
 //
 // Speculation: most steps' CG solves stop at their start (the iterate is
 // kept). The V half-step's start and the step end are therefore launched
@@ -114,20 +115,20 @@ void selfdot(Ctx& c, const double* x, int slot) {
 }
 
 // half-step start: rhs (never stored), Q(x0), r = rhs - Q(x0), ||rhs||^2 and ||r||^2
-void cg_init(Ctx& c, const double* x0, const double* Wf, double* r, int slot) {
+// (the V half-step's start, cw = a->cu, also stores C U for the step end)
+void cg_init(Ctx& c, const double* x0, const double* Wf, double* r, int slot, double* cw) {
     const cl_admm_diag_args* a = c.a;
     cl_pattern P = a->cpat;
     P.c_coeff = 1.0;
-    CL_TRY(c, cl_diag_admm_cg_init(&P, Wf, x0, a->ld, a->scale, a->rho, a->nlam, a->aval, r, a->slab + slot, a->ws,
-                                   (void*)c.st));
+    CL_TRY(c, cl_diag_admm_cg_init(&P, Wf, x0, a->ld, a->scale, a->rho, a->nlam, a->aval, r, cw, a->slab + slot,
+                                   a->ws, (void*)c.st));
 }
 
+// step end from the C U stored by the last V start (whose Wf is the U passed here)
 void step_end(Ctx& c, const double* U, const double* V) {
     const cl_admm_diag_args* a = c.a;
-    cl_pattern P = a->cpat;
-    P.c_coeff = 1.0;
-    CL_TRY(c, cl_diag_admm_step_end(&P, U, V, a->ld, a->aval, a->b, a->lam, a->rho, a->ax, a->lam_new,
-                                    a->slab + S_E0, a->ws, (void*)c.st));
+    CL_TRY(c, cl_diag_admm_step_end_rows(a->n, a->ld, a->cu, U, V, a->aval, a->b, a->lam, a->rho, a->ax, a->lam_new,
+                                         a->slab + S_E0, a->ws, (void*)c.st));
 }
 
 // max(v, 1e-300) with Python semantics (v is kept unless 1e-300 > v; NaN stays NaN)
@@ -185,7 +186,7 @@ void fail(cl_admm_step_stats* out, int status, int half, int is_new, double pq) 
 
 extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats* out) {
     if (a == nullptr || out == nullptr || a->n < 0 || a->ld < 2 || (a->ld & 1) || a->cg_cap < 0 ||
-        a->r_v == nullptr)
+        a->r_v == nullptr || a->cu == nullptr)
         return CL_EARG;
     Ctx c;
     c.a = a;
@@ -226,9 +227,9 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
     // U start; at small n also the V start and the step end, speculatively assuming U (then V)
     // is kept, read at one synchronize
     const bool spec = c.N <= SPEC_MAX_ELEMS;
-    cg_init(c, a->U, a->V, a->r, S_RHSU);
+    cg_init(c, a->U, a->V, a->r, S_RHSU, nullptr);
     if (spec) {
-        cg_init(c, a->V, a->U, a->r_v, S_RHSV);
+        cg_init(c, a->V, a->U, a->r_v, S_RHSV, a->cu);
         step_end(c, a->U, a->V);
         if (!fetch(c, S_RHSU, S_END - S_RHSU)) RET_RC();
     } else if (!fetch(c, S_RHSU, 2)) {
@@ -251,14 +252,14 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
             return CL_OK;
         }
         selfdot(c, a->U_new, S_XXU);
-        cg_init(c, a->V, a->U_new, a->r_v, S_RHSV);       // the speculative V start used the old U
+        cg_init(c, a->V, a->U_new, a->r_v, S_RHSV, a->cu);       // the speculative V start used the old U
         if (!fetch(c, S_XXU, S_END - S_XXU)) RET_RC();
         if (!isfinite(H(c, S_XXU))) {                    // U's iterate is not finite
             fail(out, 3, 0, 1, 0.0);
             return CL_OK;
         }
     } else if (!spec) {
-        cg_init(c, a->V, a->U, a->r_v, S_RHSV);
+        cg_init(c, a->V, a->U, a->r_v, S_RHSV, a->cu);
         if (!fetch(c, S_RHSV, 2)) RET_RC();
     }
     out->u_reused = u_kept;

@@ -242,6 +242,7 @@ struct EpiDev {
     // diagonal-constraint ADMM epilogues (EPI 2: CG start, EPI 3: step end)
     double rho;
     double* rout;         // EPI 2: initial CG residual
+    double* cw;           // EPI 2: C Wf itself (optional; the step end reads it back)
     const double* bvec;   // EPI 3: b
     const double* lam;    // EPI 3: multiplier at the step start
     double* axo;          // EPI 3: A(U V^T)
@@ -970,6 +971,7 @@ __global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : 3) spm
                         rr = axpy2(-1.0, q, rr);
                         if (active) {
                             st2(E.rout + off, rr);
+                            if (E.cw != nullptr) st2(E.cw + off, acc);
                             dacc[0] += dot2(o, o);
                             dacc[1] += dot2(rr, rr);
                         }
@@ -1324,6 +1326,53 @@ __global__ void __launch_bounds__(NT) diag_cg_step_kernel(int64_t n, int ld, dou
         }
     }
     reduce_and_finish<1>(dacc, 1, ws, dots_out);
+}
+
+// ADMM step end for diagonal constraints from a stored C U (written by the V half-step's
+// start, cl_diag_admm_cg_init): <C U, V> (objective), A(U V^T)_c = a_c <U_c, V_c>, the
+// residual, the dual ascent lam + rho (A(UV^T) - b) and lam_new . b, in one streaming pass
+// instead of a second SpMM. Rows stream as in diag_cg_apply_kernel.
+__global__ void __launch_bounds__(NT) diag_step_end_rows_kernel(int64_t n, int ld, const double* CU, const double* U,
+                                                                const double* V, const double* aval, const double* b,
+                                                                const double* lam, double rho, double* ax_out,
+                                                                double* lam_out, double* ws, double* dots_out) {
+    __shared__ double part[NT * DC_U];
+    const int h2 = ld >> 1;
+    const int rb = (NT * DC_U) / h2;
+    const int64_t nblk = (n + rb - 1) / rb;
+    double dacc[3] = {0.0, 0.0, 0.0};
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int64_t r0 = blk * rb;
+        const int nr = (int)min((int64_t)rb, n - r0);
+        const int units = nr * h2;
+        const int64_t base = r0 * (int64_t)h2;
+#pragma unroll
+        for (int u = 0; u < DC_U; ++u) {
+            const int e = threadIdx.x + u * NT;
+            if (e < units) {
+                const int64_t off = 2 * (base + e);
+                const double2 vv = ld2cs(V + off);
+                part[e] = dot2(ld2cs(U + off), vv);
+                dacc[0] += dot2(ld2cs(CU + off), vv);
+            }
+        }
+        __syncthreads();
+        for (int rr = threadIdx.x; rr < nr; rr += NT) {
+            double sdot = 0.0;
+            for (int q = 0; q < h2; ++q) sdot += part[rr * h2 + q];
+            const int64_t row = r0 + rr;
+            const double ax = __ldg(aval + row) * sdot;
+            const double bb = __ldg(b + row);
+            const double res = ax - bb;
+            const double ln = fma(rho, res, __ldg(lam + row));
+            ax_out[row] = ax;
+            lam_out[row] = ln;
+            dacc[1] += res * res;
+            dacc[2] += ln * bb;
+        }
+        __syncthreads();
+    }
+    reduce_and_finish<3>(dacc, 3, ws, dots_out);
 }
 
 __global__ void __launch_bounds__(NT) gather_rows_scalar_kernel(const int32_t* __restrict__ idx, int64_t count, int ld,
@@ -1792,12 +1841,13 @@ static int diag_admm_launch(int mode, const cl_pattern* S, const double* X, int3
 }
 
 int cl_diag_admm_cg_init(const cl_pattern* C, const double* Wf, const double* x0, int32_t ld, double scale, double rho,
-                         const double* nlam, const double* aval, double* r, double* dots_out, double* ws,
+                         const double* nlam, const double* aval, double* r, double* cwf, double* dots_out, double* ws,
                          void* stream) {
     if (Wf == nullptr || x0 == nullptr || nlam == nullptr || aval == nullptr || r == nullptr) return CL_EARG;
-    if (!aligned16(Wf) || !aligned16(x0) || !aligned16(r)) return CL_EARG;
+    if (!aligned16(Wf) || !aligned16(x0) || !aligned16(r) || (cwf != nullptr && !aligned16(cwf))) return CL_EARG;
     EpiDev E;
     memset(&E, 0, sizeof(E));
+    E.cw = cwf;
     E.ny = 1; E.Y[0] = Wf; E.ycoef[0] = rho;
     E.nz = 1; E.Z[0] = x0;
     E.ndot = 2;
@@ -1819,6 +1869,21 @@ int cl_diag_admm_step_end(const cl_pattern* C, const double* U, const double* V,
     E.ndot = 3;
     E.dmul = aval; E.rho = rho; E.bvec = b; E.lam = lam; E.axo = ax; E.lamo = lam_new;
     return diag_admm_launch(3, C, V, ld, 1.0, E, dots_out, ws, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cl_diag_admm_step_end_rows(int64_t n, int32_t ld, const double* CU, const double* U, const double* V,
+                               const double* aval, const double* b, const double* lam, double rho, double* ax,
+                               double* lam_new, double* dots_out, double* ws, void* stream) {
+    if (n < 0 || ld < 2 || (ld & 1) || ld / 2 > NT * DC_U || dots_out == nullptr || ws == nullptr) return CL_EARG;
+    if (n > 0 && (CU == nullptr || U == nullptr || V == nullptr || aval == nullptr || b == nullptr ||
+                  lam == nullptr || ax == nullptr || lam_new == nullptr))
+        return CL_EARG;
+    if (n > 0 && (!aligned16(CU) || !aligned16(U) || !aligned16(V))) return CL_EARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (n == 0) return (int)cudaMemsetAsync(dots_out, 0, 3 * sizeof(double), st);
+    diag_step_end_rows_kernel<<<diag_cg_grid((const void*)diag_step_end_rows_kernel, n, ld), NT, 0, st>>>(
+        n, ld, CU, U, V, aval, b, lam, rho, ax, lam_new, ws, dots_out);
+    return (int)cudaGetLastError();
 }
 
 int cl_single_entry_apply(int64_t nrows, const int64_t* indptr, const int32_t* indices, const double* slot_a,

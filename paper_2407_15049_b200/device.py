@@ -225,11 +225,13 @@ class Device:
             P.nown = halo.nown
         return P
 
-    def diag_admm_cg_init(self, cpat, Wf, x0, ld, scale, rho, nlam, aval, r, at):
-        """Fused rhs + initial CG residual (cl_diag_admm_cg_init); ||rhs||^2, ||r||^2 -> slab[at:at+2]."""
+    def diag_admm_cg_init(self, cpat, Wf, x0, ld, scale, rho, nlam, aval, r, at, cw=None):
+        """Fused rhs + initial CG residual (cl_diag_admm_cg_init); ||rhs||^2, ||r||^2 -> slab[at:at+2];
+        C Wf itself -> cw when given."""
         P = self._halo_struct(cpat, Wf, ld)
         rc = self.lib.cl_diag_admm_cg_init(ctypes.byref(P), ptr(Wf), ptr(x0), int(ld), float(scale), float(rho),
-                                           ptr(nlam), ptr(aval), ptr(r), self.slot(at), ptr(self.ws), self.sp)
+                                           ptr(nlam), ptr(aval), ptr(r), ptr(cw), self.slot(at), ptr(self.ws),
+                                           self.sp)
         self.launches += 1
         check(rc, "cl_diag_admm_cg_init")
 
@@ -240,6 +242,15 @@ class Device:
                                             float(rho), ptr(ax), ptr(lam_new), self.slot(at), ptr(self.ws), self.sp)
         self.launches += 1
         check(rc, "cl_diag_admm_step_end")
+
+    def diag_admm_step_end_rows(self, CU, U, V, ld, aval, b, lam, rho, ax, lam_new, at):
+        """Step end from a stored C U (cl_diag_admm_step_end_rows): <CU, V>, ||ax - b||^2,
+        lam_new . b -> slab[at:at+3]."""
+        rc = self.lib.cl_diag_admm_step_end_rows(int(U.shape[0]), int(ld), ptr(CU), ptr(U), ptr(V), ptr(aval), ptr(b),
+                                                 ptr(lam), float(rho), ptr(ax), ptr(lam_new), self.slot(at),
+                                                 ptr(self.ws), self.sp)
+        self.launches += 1
+        check(rc, "cl_diag_admm_step_end_rows")
 
     def single_entry_apply(self, apat, ld, W, Wf, rho, out, at=0):
         """Fused half-step operator for single-entry constraints; <W, out> -> slab[at]."""

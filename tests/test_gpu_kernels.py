@@ -335,6 +335,28 @@ def test_fused_admm_passes_match_numpy(dev, ld):
     assert np.abs(lam_new.cpu().numpy() - ln).max() <= 1e-11 * (1 + np.abs(ln).max())
     assert close(s[62], np.sum((C @ Vh) * Uh)) and close(s[63], res @ res)
     assert close(s[64], ln @ ops.b.cpu().numpy())
+    # the stored C Wf and the streaming step end built on it (cl_diag_admm_step_end_rows)
+    cw, r2 = torch.empty_like(Wf), torch.empty_like(Wf)
+    dev.diag_admm_cg_init(ops.c_mat.cpat, U, x0, ld, scale, rho, nlam, aval, r2, at=66, cw=cw)
+    CUh = C @ Uh
+    assert np.abs(cw.cpu().numpy() - CUh).max() <= 1e-12 * (1 + np.abs(CUh).max())
+    ax2, lam2 = torch.empty_like(ax), torch.empty_like(ax)
+    dev.diag_admm_step_end_rows(cw, U, V, ld, aval, ops.b, lam, rho, ax2, lam2, at=70)
+    s2 = dev.fetch(73)
+    assert np.abs(ax2.cpu().numpy() - axh).max() <= 1e-11 * (1 + np.abs(axh).max())
+    assert np.abs(lam2.cpu().numpy() - ln).max() <= 1e-11 * (1 + np.abs(ln).max())
+    assert close(s2[70], np.sum(CUh * Vh)) and close(s2[71], res @ res)
+    assert close(s2[72], ln @ ops.b.cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_step_end_rows_empty(dev):
+    import torch
+    e = torch.empty((0, 4), dtype=torch.float64, device="cuda")
+    m = torch.empty(0, dtype=torch.float64, device="cuda")
+    dev.slab[80:83] = 3.0
+    dev.diag_admm_step_end_rows(e, e, e, 4, m, m, m, 1.0, m, m, at=80)
+    assert list(dev.fetch(83)[80:83]) == [0.0, 0.0, 0.0]
 
 
 @pytest.mark.parametrize("pq", [2.5, -1.0, 0.0, float("nan"), float("inf")])
