@@ -524,11 +524,27 @@ __global__ void __launch_bounds__(NT, 4) diag_constraint_kernel(DiagCon a) {
 // one thread per row fold its units in order. Products 1 and 2 are summed
 // per unit (q1 = A(R D^T + D R^T) in the line search).
 #define DC_U 8
+#ifndef CL_SMALLN
+#define CL_SMALLN 1         // small problems: spread rows over at least FLAT_MIN_BLK blocks / one tile per CTA
+#endif
+#define FLAT_MIN_BLK (2 * NSM)
+
+// Rows per block iteration of the flat row kernels: NT*DC_U double2 units, or fewer when
+// that would leave SMs idle (small n), so every SM has work and each thread few units.
+__host__ __device__ __forceinline__ int flat_rows(int64_t n, int h2) {
+    int rb = (NT * DC_U) / h2;
+#if CL_SMALLN
+    const int64_t spread = (n + FLAT_MIN_BLK - 1) / FLAT_MIN_BLK;
+    if (spread < rb) rb = spread < 1 ? 1 : (int)spread;
+#endif
+    return rb;
+}
+
 template <int NOP>
 __global__ void __launch_bounds__(NT) diag_constraint_flat_kernel(DiagCon a) {
     __shared__ double part[2][NT * DC_U];
     const int h2 = a.ld >> 1;
-    const int rb = (NT * DC_U) / h2;                  // rows per block iteration (>= 1)
+    const int rb = flat_rows(a.n, h2);                // rows per block iteration (>= 1)
     const bool two = a.nprod1 == 2, three = a.out2 != nullptr;
     const int64_t nblk = (a.n + rb - 1) / rb;
     for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
@@ -1061,9 +1077,16 @@ int sp_blocks_per_sm() {
 template <int G, int VEC, int EPI, int GHOST>
 void sp_launch(const SpDev& a0, const EpiDev& E, double* ws, double* dots, cudaStream_t st) {
     SpDev a = a0;
-    a.ntiles = (a.nrows + a.tr - 1) / a.tr;
     int grid = sp_blocks_per_sm<G, VEC, EPI, GHOST>() * NSM;
     if (grid > CL_RED_BLOCKS) grid = CL_RED_BLOCKS;
+#if CL_SMALLN
+    {   // few rows: shorter tiles so that every resident CTA gets one (latency, not staging, bounds)
+        constexpr int NG = NT / G;
+        const int64_t spread = (a.nrows + (int64_t)NG * grid - 1) / ((int64_t)NG * grid);
+        if (spread < a.tr / NG) a.tr = (int)(spread < 1 ? 1 : spread) * NG;
+    }
+#endif
+    a.ntiles = (a.nrows + a.tr - 1) / a.tr;
     if ((int64_t)grid > a.ntiles) grid = (int)a.ntiles;
     spmm_tiled_kernel<G, VEC, EPI, GHOST><<<grid, NT, 0, st>>>(a, E, ws, dots);
 }
@@ -1198,7 +1221,7 @@ __global__ void __launch_bounds__(NT) diag_cg_apply_kernel(DiagCg a, double* ws,
     __shared__ double part[NT * DC_U];
     __shared__ double coef[NT * DC_U];
     const int h2 = a.ld >> 1;
-    const int rb = (NT * DC_U) / h2;
+    const int rb = flat_rows(a.n, h2);
     const int64_t nblk = (a.n + rb - 1) / rb;
     double dacc[1] = {0.0};
     for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
@@ -1299,7 +1322,7 @@ __global__ void __launch_bounds__(NT) diag_cg_step_kernel(int64_t n, int ld, dou
         alpha = qr / pq;
     }
     const int h2 = ld >> 1;
-    const int rb = (NT * DC_U) / h2;
+    const int rb = flat_rows(n, h2);
     const int64_t nblk = (n + rb - 1) / rb;
     double dacc[1] = {0.0};
     for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
@@ -1338,7 +1361,7 @@ __global__ void __launch_bounds__(NT) diag_step_end_rows_kernel(int64_t n, int l
                                                                 double* lam_out, double* ws, double* dots_out) {
     __shared__ double part[NT * DC_U];
     const int h2 = ld >> 1;
-    const int rb = (NT * DC_U) / h2;
+    const int rb = flat_rows(n, h2);
     const int64_t nblk = (n + rb - 1) / rb;
     double dacc[3] = {0.0, 0.0, 0.0};
     for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
@@ -1669,7 +1692,7 @@ int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const dou
     }
     if (ld >= 2 && ld / 2 <= NT * DC_U && aligned16(X1) && aligned16(Y1) && (X2 == nullptr || aligned16(X2)) &&
         (Y2 == nullptr || aligned16(Y2)) && (X3 == nullptr || aligned16(X3)) && (Y3 == nullptr || aligned16(Y3))) {
-        const int rb = (NT * DC_U) / (ld / 2);
+        const int rb = flat_rows(n, ld / 2);
         const int64_t nblk = (n + rb - 1) / rb;
         // one full wave of resident CTAs (the shared-memory fold limits CTAs per SM)
 #define CL_DCF(NO)                                                                                  \
@@ -1735,7 +1758,7 @@ int cl_diag_cg_apply(int64_t n, int32_t ld, const double* aval, double rho, doub
     DiagCg d;
     d.n = n; d.ld = ld; d.aval = aval; d.rho = rho; d.beta = beta; d.r = r; d.p = p; d.Wf = Wf; d.Q = Q;
     d.coef_g = nullptr;
-    const int rb = (NT * DC_U) / (ld / 2);
+    const int rb = flat_rows(n, ld / 2);
     const int64_t nblk = (n + rb - 1) / rb;
     int64_t wave = (int64_t)resident_blocks((const void*)diag_cg_apply_kernel) * NSM;
     if (wave > CL_RED_BLOCKS) wave = CL_RED_BLOCKS;
@@ -1745,7 +1768,7 @@ int cl_diag_cg_apply(int64_t n, int32_t ld, const double* aval, double rho, doub
 }
 
 static int diag_cg_grid(const void* k, int64_t n, int32_t ld) {
-    const int rb = (NT * DC_U) / (ld / 2);
+    const int rb = flat_rows(n, ld / 2);
     const int64_t nblk = (n + rb - 1) / rb;
     int64_t wave = (int64_t)resident_blocks(k) * NSM;
     if (wave > CL_RED_BLOCKS) wave = CL_RED_BLOCKS;
