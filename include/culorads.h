@@ -393,15 +393,37 @@ typedef struct {
     double* r;
     double* h;                 /* k_max device doubles (Gram projections) */
     cl_pattern S;
-    double* slab;              /* 2 device doubles */
-    double* host;              /* 2 pinned host doubles */
+    double* slab;              /* 2 * CL_LANCZOS_BATCH device doubles */
+    double* host;              /* 2 * CL_LANCZOS_BATCH pinned host doubles */
     double* ws;
     void* stream;
     double* alphas;
     double* betas;
+    double* dbeta;             /* k_max device doubles: the betas as the device sees them */
 } cl_lanczos_args;
 
+/* The loop enqueues CL_LANCZOS_BATCH steps with the scalars kept on the device
+ * (cl_lanczos_update), then reads their alphas and ||r||^2 at one synchronize and
+ * replays the reference's stop tests in order. Steps past the stop are discarded
+ * (they only touch basis rows >= k). */
+#define CL_LANCZOS_BATCH 16
 int cl_lanczos_loop(const cl_lanczos_args* a, int32_t* k_out);
+
+/* cl_admm_step_diag as ONE cooperative launch (csrc/admm_fused.cu) for small
+ * problems, where launch and round-trip latency bound the step: every phase runs
+ * in one kernel between grid-wide barriers and the scalar decisions are taken on
+ * the device; one synchronize per step. Same args and stats (host: 16 pinned
+ * doubles); iterates equal cl_admm_step_diag's to rounding (global sums are added
+ * in another fixed order). Requires n >= 1 and a C pattern with cv values only. */
+int cl_admm_step_diag_fused(const cl_admm_diag_args* a, cl_admm_step_stats* out);
+
+/* Lanczos vector updates with device-resident scalars (spectral.py:45-61):
+ *   mode 0: r = u - (*alpha) qk [- (*beta) qkm1 when beta != NULL]
+ *   mode 1: qn = r / sqrt(*rr), *beta_out = sqrt(*rr)
+ * Bit-identical to cl_lincomb with the same coefficients taken on the host. */
+int cl_lanczos_update(int32_t mode, int64_t n, const double* alpha, const double* beta, const double* u,
+                      const double* qk, const double* qkm1, double* r, const double* rr, double* beta_out, double* qn,
+                      void* stream);
 
 /* L2 fetch granularity hint of the current device (cudaLimitMaxL2FetchGranularity, 0..128 bytes). */
 int cl_set_l2_fetch_granularity(int32_t bytes);

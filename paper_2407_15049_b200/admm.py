@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import time
 from collections import deque
 from dataclasses import dataclass
@@ -320,6 +321,10 @@ def _resid(ops, ax, res, at):
 
 
 NATIVE = True     # diagonal constraints, one device: run the step's control flow in C++
+# Problems with n*ld at most this many doubles run each ADMM step as one cooperative
+# launch (cl_admm_step_diag_fused): there, latency rather than HBM bounds the step.
+FUSED = os.environ.get("CULORADS_FUSED", "1") != "0"
+FUSED_MAX_ELEMS = int(os.environ.get("CULORADS_FUSED_MAX", 1 << 18))
 
 
 def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, hs, pool):
@@ -360,9 +365,14 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
     a.ws = dev.ws.data_ptr()
     a.stream = dev.stream.cuda_stream
     st = _lib.AdmmStepStats()
-    rc = dev.lib.cl_admm_step_diag(ctypes.byref(a), ctypes.byref(st))
-    dev.launches += 8 + 3 * (st.it_u + st.it_v)
-    _lib.check(rc, f"cl_admm_step_diag (admm_native.cu:{st.err_line})")
+    if FUSED and n >= 1 and n * ld <= FUSED_MAX_ELEMS:
+        rc = dev.lib.cl_admm_step_diag_fused(ctypes.byref(a), ctypes.byref(st))
+        dev.launches += 1
+        _lib.check(rc, "cl_admm_step_diag_fused")
+    else:
+        rc = dev.lib.cl_admm_step_diag(ctypes.byref(a), ctypes.byref(st))
+        dev.launches += 8 + 3 * (st.it_u + st.it_v)
+        _lib.check(rc, f"cl_admm_step_diag (admm_native.cu:{st.err_line})")
     if st.status:
         if st.bad_half == 0:
             last = U_new if st.bad_is_new else state.U

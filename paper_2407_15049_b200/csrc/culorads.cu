@@ -1398,6 +1398,33 @@ __global__ void __launch_bounds__(NT) diag_step_end_rows_kernel(int64_t n, int l
     reduce_and_finish<3>(dacc, 3, ws, dots_out);
 }
 
+// Lanczos vector updates with the scalars left on the device (spectral.py:45-61), so the
+// loop needs no host round trip per step. Same arithmetic as cl_lincomb with host
+// coefficients (o = fma(c_j, v_j, o) from 0 in operand order), hence bit-identical:
+//   mode 0: r = u - alpha q_k [- beta q_{k-1}]     alpha = *alpha_p, beta = *beta_p
+//   mode 1: q_next = (1 / sqrt(*rr_p)) r, and *beta_out = sqrt(*rr_p)
+__global__ void __launch_bounds__(NT) lanczos_update_kernel(int mode, int64_t n, const double* alpha_p,
+                                                            const double* beta_p, const double* u, const double* qk,
+                                                            const double* qkm1, double* r, const double* rr_p,
+                                                            double* beta_out, double* qn) {
+    const int64_t stride = (int64_t)gridDim.x * NT;
+    if (mode == 0) {
+        const double na = -*alpha_p;
+        const double nb = beta_p != nullptr ? -*beta_p : 0.0;
+        for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += stride) {
+            double o = fma(1.0, u[i], 0.0);
+            o = fma(na, qk[i], o);
+            if (beta_p != nullptr) o = fma(nb, qkm1[i], o);
+            r[i] = o;
+        }
+    } else {
+        const double beta = sqrt(*rr_p);
+        const double cf = 1.0 / beta;
+        if (blockIdx.x == 0 && threadIdx.x == 0) *beta_out = beta;
+        for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += stride) qn[i] = fma(cf, r[i], 0.0);
+    }
+}
+
 __global__ void __launch_bounds__(NT) gather_rows_scalar_kernel(const int32_t* __restrict__ idx, int64_t count, int ld,
                                                                 const double* __restrict__ X, double* __restrict__ out) {
     const int64_t total = count * ld;
@@ -1983,6 +2010,21 @@ int cl_diag_alm_update(const cl_diag_update_args* a, double* dots_out, double* w
     else if (a->nh <= 10) CL_DU(10);
     else CL_DU(CL_MAXIN);
 #undef CL_DU
+    return (int)cudaGetLastError();
+}
+
+int cl_lanczos_update(int32_t mode, int64_t n, const double* alpha, const double* beta, const double* u,
+                      const double* qk, const double* qkm1, double* r, const double* rr, double* beta_out, double* qn,
+                      void* stream) {
+    if (n < 0 || (mode != 0 && mode != 1)) return CL_EARG;
+    if (mode == 0 && (alpha == nullptr || u == nullptr || qk == nullptr || r == nullptr ||
+                      (beta != nullptr && qkm1 == nullptr)))
+        return CL_EARG;
+    if (mode == 1 && (rr == nullptr || beta_out == nullptr || r == nullptr || qn == nullptr)) return CL_EARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t nb = (n + NT - 1) / NT;
+    const int grid = (int)(nb < 1 ? 1 : (nb > NSM * 8 ? NSM * 8 : nb));
+    lanczos_update_kernel<<<grid, NT, 0, st>>>(mode, n, alpha, beta, u, qk, qkm1, r, rr, beta_out, qn);
     return (int)cudaGetLastError();
 }
 

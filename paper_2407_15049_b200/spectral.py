@@ -61,6 +61,8 @@ def _lanczos_native(op, n, k_max, Q, u, r, h, dev, alphas, betas):
     a.slab, a.host = dev.slot(520).value, dev.host.data_ptr() + 8 * 520
     a.ws, a.stream = dev.ws.data_ptr(), dev.stream.cuda_stream
     a.alphas, a.betas = alphas.ctypes.data, betas.ctypes.data
+    dbeta = dev.zeros(max(k_max, 1))
+    a.dbeta = dbeta.data_ptr()
     k = _lib.I32(0)
     rc = dev.lib.cl_lanczos_loop(ctypes.byref(a), ctypes.byref(k))
     dev.launches += 9 * k.value

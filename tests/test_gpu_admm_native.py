@@ -11,11 +11,12 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _run_steps(native, p, steps, seed=0, r=6):
+def _run_steps(native, p, steps, seed=0, r=6, fused=False):
     import torch
     from paper_2407_15049_b200 import admm, alm, linops
     from paper_2407_15049_b200.device import padded_ld
     admm.NATIVE = native
+    admm.FUSED = fused
     try:
         ops = linops.build_operators(p)
         dev = ops.dev
@@ -33,6 +34,7 @@ def _run_steps(native, p, steps, seed=0, r=6):
         return state.U.cpu().numpy(), state.V.cpu().numpy(), dual.lam.cpu().numpy(), stats
     finally:
         admm.NATIVE = True
+        admm.FUSED = True
 
 
 @pytest.mark.parametrize("r", [6, 70, 400])     # r = 400: n*ld > 2^20, the in-order (unspeculated) step
@@ -58,7 +60,46 @@ def test_native_solve_trace_bit_identical():
         slow = driver.solve(p, cfg)
     finally:
         admm.NATIVE = True
-    fast = driver.solve(p, cfg)
+    admm.FUSED = False
+    try:
+        fast = driver.solve(p, cfg)
+    finally:
+        admm.FUSED = True
     tr = lambda rep: np.array([r[2:7] for r in rep.trace_rows], dtype=float)  # noqa: E731
     assert tr(fast).tobytes() == tr(slow).tobytes()
     assert fast.objective == slow.objective and fast.status == slow.status
+
+
+@pytest.mark.parametrize("r,deg", [(6, 6.0), (11, 48.0), (70, 6.0)])
+def test_fused_step_matches_native_step(r, deg):
+    """The one-launch step (cl_admm_step_diag_fused) against the multi-launch native step:
+    same CG iteration counts and reuse decisions, iterates equal to rounding (global sums
+    are added in a different fixed order)."""
+    from paper_2407_15049_b200 import graphs, problem
+    p = problem.build_maxcut(graphs.random_sparse(800, deg=deg, seed=4))
+    a = _run_steps(True, p, 6, r=r, fused=True)
+    b = _run_steps(True, p, 6, r=r, fused=False)
+    assert sum(s[0] + s[1] for s in b[3]) > 0
+    for x, y in zip(a[:3], b[:3]):
+        assert np.abs(x - y).max() <= 1e-9 * (1.0 + np.abs(y).max())
+    for sa, sb in zip(a[3], b[3]):
+        assert sa[0] == sb[0] and sa[1] == sb[1] and sa[4] == sb[4]
+        for u, v in zip(sa[2:4] + sa[5:], sb[2:4] + sb[5:]):
+            assert abs(u - v) <= 1e-8 * (1.0 + abs(v))
+
+
+def test_fused_solve_trace_close_to_native():
+    """A whole G1-shaped solve with fused steps: same status, objective to 1e-9 relative."""
+    from paper_2407_15049_b200 import admm, driver
+    from tests._golden import cfg_of, load, problem_from
+    z = load("solve_g1_like.npz")
+    p = problem_from(z)
+    cfg = driver.SolverConfig(**cfg_of(z))
+    admm.FUSED = False
+    try:
+        ref = driver.solve(p, cfg)
+    finally:
+        admm.FUSED = True
+    fused = driver.solve(p, cfg)
+    assert fused.status == ref.status
+    assert abs(fused.objective - ref.objective) <= 1e-9 * abs(ref.objective)

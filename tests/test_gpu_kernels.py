@@ -276,17 +276,28 @@ def test_single_entry_detection_rejects_general_constraints(dev):
     assert ops.adj.apat.single_a is None
 
 
-@pytest.mark.parametrize("case", ["maxcut", "completion"])
+@pytest.mark.parametrize("case", ["maxcut", "completion", "tiny", "breakdown"])
 def test_native_lanczos_bit_identical(dev, case):
-    """cl_lanczos_loop (operator assembled once) vs the Python-driven loop: same eigenvalue
-    estimate to the bit, and the same basis size."""
+    """cl_lanczos_loop (operator assembled once, CL_LANCZOS_BATCH steps per round trip) vs
+    the Python-driven loop: same eigenvalue estimate to the bit, and the same basis size;
+    also for a basis smaller than one batch (tiny) and a Krylov breakdown inside a batch
+    (complete graph, constant multiplier: C - A*(lam) has two distinct eigenvalues)."""
     from paper_2407_15049_b200 import graphs, linops, problem, spectral
+    lam = None
     if case == "maxcut":
         p = problem.build_maxcut(graphs.random_sparse(700, deg=8.0, seed=5))
+    elif case == "tiny":
+        p = problem.build_maxcut(graphs.GraphEdgeList(3, np.array([0, 1]), np.array([1, 2]), np.ones(2)))
+    elif case == "breakdown":
+        n = 40
+        iu, ju = np.triu_indices(n, 1)
+        p = problem.build_maxcut(graphs.GraphEdgeList(n, iu, ju, np.ones(iu.size)))
+        lam = np.full(p.m, 0.3)
     else:
         p = problem.build_matrix_completion(graphs.random_completion(60, 50, 900, seed=5))
     ops = linops.build_operators(p)
-    lam = np.random.default_rng(7).standard_normal(p.m)
+    if lam is None:
+        lam = np.random.default_rng(7).standard_normal(p.m)
     res = {}
     for native in (True, False):
         spectral.NATIVE = native

@@ -128,14 +128,15 @@ def _scalar_problem(a=1.0, b=1.0):
                       a_row=np.array([0]), a_col=np.array([0]), a_val=np.array([a]), b=np.array([b]))
 
 
-@pytest.mark.parametrize("native", [True, False])
-def test_admm_fixed_point_and_converged_start(native):
+@pytest.mark.parametrize("native,fused", [(True, True), (True, False), (False, False)])
+def test_admm_fixed_point_and_converged_start(native, fused):
     """n = m = 1 (a padded single column): a feasible complementary point stays put."""
     import torch
     from paper_2407_15049_b200 import admm, alm, linops
     p = _scalar_problem()
     ops = linops.build_operators(p)
     admm.NATIVE = native
+    admm.FUSED = fused
     try:
         U = linops.to_factor(np.array([[1.0]]), ops.dev)
         st = admm.AdmmState(U=U.clone(), V=U.clone(), dual=alm.DualVector(lam=ops.dev.zeros(1), rho=2.0), r=1)
@@ -147,6 +148,7 @@ def test_admm_fixed_point_and_converged_start(native):
         assert res.steps == 0
     finally:
         admm.NATIVE = True
+        admm.FUSED = True
 
 
 def test_alm_gradient_matches_finite_differences_and_value_matches_dense():
