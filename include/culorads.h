@@ -400,6 +400,7 @@ typedef struct {
     double* alphas;
     double* betas;
     double* dbeta;             /* k_max device doubles: the betas as the device sees them */
+    double* dalpha;            /* k_max device doubles (cl_lanczos_loop_fused) */
 } cl_lanczos_args;
 
 /* The loop enqueues CL_LANCZOS_BATCH steps with the scalars kept on the device
@@ -408,6 +409,10 @@ typedef struct {
  * (they only touch basis rows >= k). */
 #define CL_LANCZOS_BATCH 16
 int cl_lanczos_loop(const cl_lanczos_args* a, int32_t* k_out);
+/* The same loop as ONE cooperative launch (small n, k_max <= 4096): the stop test runs
+ * on the device; one synchronize for the whole basis. Coefficients agree with
+ * cl_lanczos_loop to rounding (global sums in another fixed order). */
+int cl_lanczos_loop_fused(const cl_lanczos_args* a, int32_t* k_out);
 
 /* cl_admm_step_diag as ONE cooperative launch (csrc/admm_fused.cu) for small
  * problems, where launch and round-trip latency bound the step: every phase runs

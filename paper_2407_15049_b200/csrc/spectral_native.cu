@@ -109,3 +109,226 @@ extern "C" int cl_lanczos_loop(const cl_lanczos_args* a, int32_t* k_out) {
     *k_out = k;
     return c.rc;
 }
+
+// ---------------------------------------------------------------------------
+// The whole loop as ONE cooperative launch for small n (latency-bound there):
+// the stop test runs on the device, phases are separated by grid barriers, and
+// global sums are reduced deterministically (per-block partials added in a fixed
+// order by every block). Coefficients agree with cl_lanczos_loop to rounding.
+// ---------------------------------------------------------------------------
+
+namespace {
+
+constexpr int LT = 256;
+constexpr int LW = LT / 32;
+
+__device__ unsigned int lz_bar_count = 0;
+__device__ unsigned int lz_bar_gen = 0;
+struct LzOut {
+    int k;
+    int err;
+};
+__device__ LzOut lz_out;
+
+__device__ void lz_sync(unsigned nblk) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned gen = atomicAdd(&lz_bar_gen, 0u);
+        __threadfence();
+        if (atomicAdd(&lz_bar_count, 1u) == nblk - 1) {
+            atomicExch(&lz_bar_count, 0u);
+            __threadfence();
+            atomicAdd(&lz_bar_gen, 1u);
+        } else {
+            const long long t0 = clock64();
+            volatile unsigned* vg = &lz_bar_gen;
+            while (*vg == gen) {
+                if (clock64() - t0 > (1LL << 31)) {     // ~1 s: give up rather than hang
+                    lz_out.err = 1;
+                    break;
+                }
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// grid-wide sum of one value per thread, identical in every thread
+__device__ double lz_sum(double v, double* ws, int& region) {
+    __shared__ double sh[LW];
+    __shared__ double tot;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double* base = ws + region * CL_RED_BLOCKS;
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < LW; ++w) s += sh[w];
+        base[blockIdx.x] = s;
+    }
+    lz_sync(gridDim.x);
+    if (wid == 0) {
+        double s = 0.0;
+        for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(base + b);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) tot = s;
+    }
+    __syncthreads();
+    const double t = tot;
+    __syncthreads();
+    region ^= 1;
+    return t;
+}
+
+struct Lz {
+    int64_t n;
+    int k_max;
+    double breakdown;
+    double* Q;
+    int64_t ldq;
+    double* u;
+    double* r;
+    double* h;
+    const int64_t* indptr;
+    const int32_t* indices;
+    const double* vals;
+    double* alpha;
+    double* beta;
+    double* ws;
+};
+
+__global__ void __launch_bounds__(LT) lanczos_fused_kernel(Lz z) {
+    extern __shared__ double hs[];
+    const int64_t n = z.n;
+    const int64_t i0 = (int64_t)blockIdx.x * LT + threadIdx.x, di = (int64_t)gridDim.x * LT;
+    const int lane = threadIdx.x & 31;
+    const int gw = (int)((blockIdx.x * LT + threadIdx.x) >> 5), nw = (int)(gridDim.x * LW);
+    int region = 0;
+    double amax = 0.0;
+    bool anan = false;
+    int k = 0;
+    while (k < z.k_max) {
+        const double* qk = z.Q + (int64_t)k * z.ldq;
+        // u = S q_k, alpha = <S q_k, q_k>
+        double part = 0.0;
+        for (int64_t i = i0; i < n; i += di) {
+            const int64_t s0 = __ldg(z.indptr + i), s1 = __ldg(z.indptr + i + 1);
+            double acc = 0.0;
+            for (int64_t s = s0; s < s1; ++s) acc = fma(__ldg(z.vals + s), __ldcg(qk + __ldg(z.indices + s)), acc);
+            z.u[i] = acc;
+            part += acc * __ldcg(qk + i);
+        }
+        const double alpha = lz_sum(part, z.ws, region);
+        if (blockIdx.x == 0 && threadIdx.x == 0) z.alpha[k] = alpha;
+        // r = u - alpha q_k - beta_{k-1} q_{k-1}
+        const double na = -alpha;
+        const double nb = k > 0 ? -__ldcg(z.beta + k - 1) : 0.0;
+        const double* qm = k > 0 ? z.Q + (int64_t)(k - 1) * z.ldq : nullptr;
+        for (int64_t i = i0; i < n; i += di) {
+            double o = fma(1.0, z.u[i], 0.0);
+            o = fma(na, __ldcg(qk + i), o);
+            if (qm != nullptr) o = fma(nb, __ldcg(qm + i), o);
+            z.r[i] = o;
+        }
+        // full reorthogonalisation against q_0..q_k, twice (spectral.py:55-56)
+        for (int pass = 0; pass < 2; ++pass) {
+            lz_sync(gridDim.x);
+            for (int t = gw; t <= k; t += nw) {       // h_t = <q_t, r>, one warp per basis vector
+                const double* qt = z.Q + (int64_t)t * z.ldq;
+                double s = 0.0;
+                for (int64_t i = lane; i < n; i += 32) s += __ldcg(qt + i) * __ldcg(z.r + i);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                if (lane == 0) z.h[t] = s;
+            }
+            lz_sync(gridDim.x);
+            for (int t = threadIdx.x; t <= k; t += LT) hs[t] = __ldcg(z.h + t);
+            __syncthreads();
+            for (int64_t i = i0; i < n; i += di) {
+                double s = 0.0;
+                for (int t = 0; t <= k; ++t) s += hs[t] * __ldcg(z.Q + (int64_t)t * z.ldq + i);
+                z.r[i] -= s;
+            }
+        }
+        ++k;
+        double rr = 0.0;
+        for (int64_t i = i0; i < n; i += di) {
+            const double v = z.r[i];
+            rr += v * v;
+        }
+        const double beta = sqrt(lz_sum(rr, z.ws, region));
+        // scale = max(max|alpha|, 1.0) with numpy/Python semantics (a NaN alpha makes it NaN)
+        const double aa = fabs(alpha);
+        if (isnan(aa)) anan = true;
+        else if (aa > amax) amax = aa;
+        const double scale = anan ? NAN : (1.0 > amax ? 1.0 : amax);
+        if (k == z.k_max || beta <= z.breakdown * scale) break;
+        if (blockIdx.x == 0 && threadIdx.x == 0) z.beta[k - 1] = beta;
+        const double cf = 1.0 / beta;
+        double* qn = z.Q + (int64_t)k * z.ldq;
+        for (int64_t i = i0; i < n; i += di) qn[i] = fma(cf, z.r[i], 0.0);
+        lz_sync(gridDim.x);       // the next SpMV gathers q_k from every block
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) lz_out.k = k;
+}
+
+int lz_max_blocks = 0;
+
+}  // namespace
+
+extern "C" int cl_lanczos_loop_fused(const cl_lanczos_args* a, int32_t* k_out) {
+    if (a == nullptr || k_out == nullptr || a->n < 1 || a->k_max < 1 || a->ldq < a->n || a->dbeta == nullptr ||
+        a->dalpha == nullptr || a->S.indptr == nullptr || (a->S.cv == nullptr && a->S.nnz > 0) ||
+        (a->S.at_ptr != nullptr && (a->S.w1 != nullptr || a->S.w2 != nullptr)) || a->S.ghost != nullptr)
+        return CL_EARG;
+    const size_t smem = sizeof(double) * (size_t)a->k_max;
+    if (smem > 32 * 1024) return CL_EARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(a->stream);
+    if (lz_max_blocks == 0) {
+        int nb = 0, dev = 0, nsm = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lanczos_fused_kernel, LT, 32 * 1024);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return (int)e;
+        lz_max_blocks = nb * nsm;
+        if (lz_max_blocks > CL_RED_BLOCKS) lz_max_blocks = CL_RED_BLOCKS;
+        if (lz_max_blocks < 1) return CL_EARG;
+    }
+    Lz z;
+    z.n = a->n; z.k_max = a->k_max; z.breakdown = a->breakdown; z.Q = a->Q; z.ldq = a->ldq;
+    z.u = a->u; z.r = a->r; z.h = a->h;
+    z.indptr = a->S.indptr; z.indices = a->S.indices; z.vals = a->S.cv;
+    z.alpha = a->dalpha; z.beta = a->dbeta; z.ws = a->ws;
+    // one row per thread, and at least 16 warps for the projections
+    int64_t nb = (a->n + LT - 1) / LT;
+    if (nb < 2) nb = 2;
+    if (nb > lz_max_blocks) nb = lz_max_blocks;
+    void* args[] = {&z};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)lanczos_fused_kernel, dim3((unsigned)nb), dim3(LT), args,
+                                                smem, st);
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbolAsync(a->host, lz_out, sizeof(LzOut), 0, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return (int)e;
+    LzOut o;
+    memcpy(&o, a->host, sizeof(o));
+    if (o.err) {
+        LzOut zz;
+        memset(&zz, 0, sizeof(zz));
+        const unsigned zero = 0;
+        cudaMemcpyToSymbol(lz_out, &zz, sizeof(zz));
+        cudaMemcpyToSymbol(lz_bar_count, &zero, sizeof(zero));
+        return CL_EARG + 1;
+    }
+    const int k = o.k;
+    e = cudaMemcpy(a->alphas, a->dalpha, sizeof(double) * (size_t)k, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && k > 1)
+        e = cudaMemcpy(a->betas, a->dbeta, sizeof(double) * (size_t)(k - 1), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return (int)e;
+    *k_out = k;
+    return CL_OK;
+}

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -48,6 +49,9 @@ def _host_callback_op(apply_s, dev):
 
 
 NATIVE = True     # one device, assembled operator: run the Lanczos loop's control flow in C++
+# Small operators run the whole loop as one cooperative launch (cl_lanczos_loop_fused).
+FUSED = os.environ.get("CULORADS_FUSED", "1") != "0"
+FUSED_MAX_N = int(os.environ.get("CULORADS_LANCZOS_FUSED_MAX", 1 << 16))
 
 
 def _lanczos_native(op, n, k_max, Q, u, r, h, dev, alphas, betas):
@@ -62,11 +66,17 @@ def _lanczos_native(op, n, k_max, Q, u, r, h, dev, alphas, betas):
     a.ws, a.stream = dev.ws.data_ptr(), dev.stream.cuda_stream
     a.alphas, a.betas = alphas.ctypes.data, betas.ctypes.data
     dbeta = dev.zeros(max(k_max, 1))
-    a.dbeta = dbeta.data_ptr()
+    dalpha = dev.zeros(max(k_max, 1))
+    a.dbeta, a.dalpha = dbeta.data_ptr(), dalpha.data_ptr()
     k = _lib.I32(0)
-    rc = dev.lib.cl_lanczos_loop(ctypes.byref(a), ctypes.byref(k))
-    dev.launches += 9 * k.value
-    _lib.check(rc, "cl_lanczos_loop")
+    if FUSED and n <= FUSED_MAX_N and k_max <= 4096:
+        rc = dev.lib.cl_lanczos_loop_fused(ctypes.byref(a), ctypes.byref(k))
+        dev.launches += 1
+        _lib.check(rc, "cl_lanczos_loop_fused")
+    else:
+        rc = dev.lib.cl_lanczos_loop(ctypes.byref(a), ctypes.byref(k))
+        dev.launches += 9 * k.value
+        _lib.check(rc, "cl_lanczos_loop")
     return k.value
 
 

@@ -301,11 +301,18 @@ def test_native_lanczos_bit_identical(dev, case):
     res = {}
     for native in (True, False):
         spectral.NATIVE = native
+        spectral.FUSED = False
         try:
             res[native] = spectral.dual_infeasibility(p, ops, lam, tol=1e-7, seed=3)
         finally:
             spectral.NATIVE = True
+            spectral.FUSED = True
     assert res[True] == res[False]
+    # the one-launch loop (cl_lanczos_loop_fused): the same estimate to rounding
+    fused = spectral.dual_infeasibility(p, ops, lam, tol=1e-7, seed=3)
+    assert fused[1] == res[True][1]
+    for u, v in ((fused[0], res[True][0]), (fused[2], res[True][2])):
+        assert abs(u - v) <= 1e-9 * (1.0 + abs(v))
 
 
 @pytest.mark.parametrize("ld", [2, 26, 66, 130])
