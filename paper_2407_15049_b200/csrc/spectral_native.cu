@@ -239,8 +239,16 @@ __global__ void __launch_bounds__(LT) lanczos_fused_kernel(Lz z) {
             lz_sync(gridDim.x);
             for (int t = gw; t <= k; t += nw) {       // h_t = <q_t, r>, one warp per basis vector
                 const double* qt = z.Q + (int64_t)t * z.ldq;
-                double s = 0.0;
-                for (int64_t i = lane; i < n; i += 32) s += __ldcg(qt + i) * __ldcg(z.r + i);
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                int64_t i = lane;
+                for (; i + 96 < n; i += 128) {
+                    s0 += __ldcg(qt + i) * __ldcg(z.r + i);
+                    s1 += __ldcg(qt + i + 32) * __ldcg(z.r + i + 32);
+                    s2 += __ldcg(qt + i + 64) * __ldcg(z.r + i + 64);
+                    s3 += __ldcg(qt + i + 96) * __ldcg(z.r + i + 96);
+                }
+                for (; i < n; i += 32) s0 += __ldcg(qt + i) * __ldcg(z.r + i);
+                double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
                 if (lane == 0) z.h[t] = s;
@@ -249,9 +257,17 @@ __global__ void __launch_bounds__(LT) lanczos_fused_kernel(Lz z) {
             for (int t = threadIdx.x; t <= k; t += LT) hs[t] = __ldcg(z.h + t);
             __syncthreads();
             for (int64_t i = i0; i < n; i += di) {
-                double s = 0.0;
-                for (int t = 0; t <= k; ++t) s += hs[t] * __ldcg(z.Q + (int64_t)t * z.ldq + i);
-                z.r[i] -= s;
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                const double* qi = z.Q + i;
+                int t = 0;
+                for (; t + 3 <= k; t += 4) {
+                    s0 += hs[t] * __ldcg(qi + (int64_t)t * z.ldq);
+                    s1 += hs[t + 1] * __ldcg(qi + (int64_t)(t + 1) * z.ldq);
+                    s2 += hs[t + 2] * __ldcg(qi + (int64_t)(t + 2) * z.ldq);
+                    s3 += hs[t + 3] * __ldcg(qi + (int64_t)(t + 3) * z.ldq);
+                }
+                for (; t <= k; ++t) s0 += hs[t] * __ldcg(qi + (int64_t)t * z.ldq);
+                z.r[i] -= (s0 + s1) + (s2 + s3);
             }
         }
         ++k;
@@ -304,9 +320,9 @@ extern "C" int cl_lanczos_loop_fused(const cl_lanczos_args* a, int32_t* k_out) {
     z.u = a->u; z.r = a->r; z.h = a->h;
     z.indptr = a->S.indptr; z.indices = a->S.indices; z.vals = a->S.cv;
     z.alpha = a->dalpha; z.beta = a->dbeta; z.ws = a->ws;
-    // one row per thread, and at least 16 warps for the projections
+    // one row per thread, and at least 128 warps for the projections
     int64_t nb = (a->n + LT - 1) / LT;
-    if (nb < 2) nb = 2;
+    if (nb < 16) nb = 16;
     if (nb > lz_max_blocks) nb = lz_max_blocks;
     void* args[] = {&z};
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)lanczos_fused_kernel, dim3((unsigned)nb), dim3(LT), args,
