@@ -374,6 +374,11 @@ typedef struct {
 } cl_alm_inner_stats;
 
 int cl_alm_inner_diag(const cl_alm_inner_args* a, cl_alm_inner_stats* out);
+/* The same inner solve as ONE cooperative launch (csrc/alm_fused.cu) for small
+ * problems: thread 0 of every block replays the scalar algebra from grid-reduced
+ * values, vector passes run between grid barriers; one synchronize per inner solve.
+ * Iterates agree with cl_alm_inner_diag to rounding. Requires n >= 1. */
+int cl_alm_inner_diag_fused(const cl_alm_inner_args* a, cl_alm_inner_stats* out);
 
 /* Slot values of a pattern (c_coeff cv + adjoint rows against w1/w2, linops.py:100
  * assemble) written to vals[nnz] -- the pre-pass cl_pattern_spmm runs internally. */

@@ -26,7 +26,7 @@ CL_EARG = 1001
 
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint_eval_halo",
            "cl_diag_constraint_eval", "cl_sddmm",
-           "cl_gather_rows", "cl_diag_cg_apply", "cl_diag_cg_apply_rows", "cl_diag_cg_step", "cl_cg_step", "cl_cg_step_dev", "cl_admm_step_diag", "cl_admm_step_diag_fused", "cl_alm_inner_diag",
+           "cl_gather_rows", "cl_diag_cg_apply", "cl_diag_cg_apply_rows", "cl_diag_cg_step", "cl_cg_step", "cl_cg_step_dev", "cl_admm_step_diag", "cl_admm_step_diag_fused", "cl_alm_inner_diag", "cl_alm_inner_diag_fused",
            "cl_diag_admm_cg_init", "cl_diag_admm_step_end", "cl_diag_admm_step_end_rows", "cl_single_entry_apply", "cl_lanczos_loop", "cl_lanczos_loop_fused",
            "cl_pattern_assemble", "cl_lanczos_update",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
@@ -127,6 +127,7 @@ def _declare(lib):
     lib.cl_admm_step_diag.argtypes = [ctypes.POINTER(AdmmDiagArgs), ctypes.POINTER(AdmmStepStats)]
     lib.cl_admm_step_diag_fused.argtypes = [ctypes.POINTER(AdmmDiagArgs), ctypes.POINTER(AdmmStepStats)]
     lib.cl_alm_inner_diag.argtypes = [ctypes.POINTER(AlmInnerArgs), ctypes.POINTER(AlmInnerStats)]
+    lib.cl_alm_inner_diag_fused.argtypes = [ctypes.POINTER(AlmInnerArgs), ctypes.POINTER(AlmInnerStats)]
     lib.cl_diag_admm_cg_init.argtypes = [ctypes.POINTER(Pattern), P, P, I32, D, D, P, P, P, P, P, P, P]
     lib.cl_diag_admm_step_end_rows.argtypes = [I64, I32, P, P, P, P, P, P, D, P, P, P, P, P]
     lib.cl_diag_admm_step_end.argtypes = [ctypes.POINTER(Pattern), P, P, I32, P, P, P, D, P, P, P, P, P]

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import time
 from collections import deque
 from dataclasses import dataclass, field
@@ -496,6 +497,10 @@ class InnerResult:
 
 
 NATIVE = True     # diagonal constraints, one device: run the inner loop's control flow in C++
+# Problems with n*ld at most this many doubles run the whole inner solve as one
+# cooperative launch (cl_alm_inner_diag_fused): latency, not HBM, bounds them.
+FUSED = os.environ.get("CULORADS_FUSED", "1") != "0"
+FUSED_MAX_ELEMS = int(os.environ.get("CULORADS_FUSED_MAX", 1 << 18))
 
 
 def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory, recorder):
@@ -533,9 +538,14 @@ def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory
     a.rec = rec.ctypes.data
     a.gnorms = gn.ctypes.data
     st = _lib.AlmInnerStats()
-    rc = dev.lib.cl_alm_inner_diag(ctypes.byref(a), ctypes.byref(st))
-    dev.launches += 2 + 5 * st.iterations
-    _lib.check(rc, f"cl_alm_inner_diag (alm_native.cu:{st.err_line})")
+    if FUSED and n >= 1 and n * ld <= FUSED_MAX_ELEMS:
+        rc = dev.lib.cl_alm_inner_diag_fused(ctypes.byref(a), ctypes.byref(st))
+        dev.launches += 1
+        _lib.check(rc, "cl_alm_inner_diag_fused")
+    else:
+        rc = dev.lib.cl_alm_inner_diag(ctypes.byref(a), ctypes.byref(st))
+        dev.launches += 2 + 5 * st.iterations
+        _lib.check(rc, f"cl_alm_inner_diag (alm_native.cu:{st.err_line})")
     if st.ax_is_ax2:
         core.ax, core.ax2 = core.ax2, core.ax
     if recorder:

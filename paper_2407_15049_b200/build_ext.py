@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "culorads.cu"), os.path.join(HERE, "csrc", "admm_native.cu"),
        os.path.join(HERE, "csrc", "alm_native.cu"), os.path.join(HERE, "csrc", "spectral_native.cu"),
-       os.path.join(HERE, "csrc", "admm_fused.cu")]
+       os.path.join(HERE, "csrc", "admm_fused.cu"), os.path.join(HERE, "csrc", "alm_fused.cu")]
 HDR = [os.path.join(ROOT, "include", "culorads.h")]
 OUT = os.path.join(HERE, "libculorads.so")
 
