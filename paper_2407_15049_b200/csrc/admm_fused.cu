@@ -27,6 +27,7 @@
 #include <string.h>
 
 #include "culorads.h"
+#include "grid_bar.cuh"
 
 namespace {
 
@@ -42,13 +43,13 @@ constexpr int FK = 3;                   // values per reduction (max)
 #define FZ_UNROLL 8         // gathers in flight per lane
 #endif
 
-__device__ unsigned int g_bar_count = 0;
-__device__ unsigned int g_bar_gen = 0;
 struct FzOut {
+    unsigned long long ctr;  // grid-barrier arrival counter (monotonic, grid_bar.cuh)
     cl_admm_step_stats st;
-    int err;                // a barrier timed out (the step's results are void)
+    int err;                 // a barrier timed out (the step's results are void)
 };
 __device__ FzOut g_out;
+__shared__ unsigned long long s_tgt;
 
 __device__ __forceinline__ double2 ldcg2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
 __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
@@ -57,30 +58,9 @@ __device__ __forceinline__ double2 axpy2(double a, double2 x, double2 y) {
     return make_double2(fma(a, x.x, y.x), fma(a, x.y, y.y));
 }
 
-// Grid-wide barrier (all blocks co-resident: cooperative launch). A block that
-// waits far too long flags g_out.err and proceeds, so a fault cannot hang the GPU.
-__device__ void grid_sync(unsigned nblk) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned gen = atomicAdd(&g_bar_gen, 0u);
-        __threadfence();
-        if (atomicAdd(&g_bar_count, 1u) == nblk - 1) {
-            atomicExch(&g_bar_count, 0u);
-            __threadfence();
-            atomicAdd(&g_bar_gen, 1u);
-        } else {
-            const long long t0 = clock64();
-            volatile unsigned* vg = &g_bar_gen;
-            while (*vg == gen) {
-                if (clock64() - t0 > (1LL << 31)) {     // ~1 s
-                    g_out.err = 1;
-                    break;
-                }
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
+__device__ __forceinline__ void grid_sync(unsigned) {
+    const GridBar b = {&g_out.ctr, 0, &g_out.err};
+    grid_bar(b, &s_tgt);
 }
 
 struct Fz {
@@ -88,6 +68,7 @@ struct Fz {
     int h2;      // double2 units per row
     int G;       // lanes per row (power of two <= 32)
     double rel;  // CG relative tolerance (host-independent: computed in the kernel)
+    unsigned long long bar_base;
 };
 
 // Sum of K per-thread values over the whole grid, identical in every thread.
@@ -314,6 +295,7 @@ __global__ void __launch_bounds__(FT) admm_step_fused_kernel(Fz f) {
     cl_admm_step_stats st;
     memset(&st, 0, sizeof(st));
     const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
+    if (threadIdx.x == 0) s_tgt = f.bar_base;
 
     // constraint values at the step start and the primal measure
     double pn2 = a.pnorm2_known;
@@ -418,6 +400,7 @@ __global__ void __launch_bounds__(FT) admm_step_fused_kernel(Fz f) {
 }
 
 int g_max_blocks = 0;
+unsigned long long g_bar_base = 0;
 
 }  // namespace
 
@@ -445,6 +428,7 @@ extern "C" int cl_admm_step_diag_fused(const cl_admm_diag_args* a, cl_admm_step_
     f.h2 = a->ld / 2;
     f.G = f.h2 <= 1 ? 1 : f.h2 <= 2 ? 2 : f.h2 <= 4 ? 4 : f.h2 <= 8 ? 8 : f.h2 <= 16 ? 16 : 32;
     f.rel = 0.0;
+    f.bar_base = g_bar_base;
     // FZ_ROWS rows per lane group: latency (gather chains) against barrier cost (blocks)
     const int64_t rows_per_block = FZ_ROWS * (int64_t)(FT / f.G);
     int64_t nb = (a->n + rows_per_block - 1) / rows_per_block;
@@ -460,12 +444,12 @@ extern "C" int cl_admm_step_diag_fused(const cl_admm_diag_args* a, cl_admm_step_
     memcpy(&o, a->host, sizeof(FzOut));
     *out = o.st;
     out->err_line = 0;
+    g_bar_base = o.ctr;
     if (o.err) {   // a barrier gave up: reset its state, report the step as failed
         FzOut z;
         memset(&z, 0, sizeof(z));
-        const unsigned zero = 0;
         cudaMemcpyToSymbol(g_out, &z, sizeof(z));
-        cudaMemcpyToSymbol(g_bar_count, &zero, sizeof(zero));
+        g_bar_base = 0;
         return CL_EARG + 1;
     }
     return CL_OK;

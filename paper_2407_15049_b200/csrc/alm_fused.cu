@@ -26,6 +26,7 @@
 #include <time.h>
 
 #include "culorads.h"
+#include "grid_bar.cuh"
 
 namespace {
 
@@ -37,14 +38,13 @@ constexpr int AK = 7 + 2 * AMAXH;                  // values of the largest redu
 constexpr int MAXB = CL_ALM_MAXBUF;
 static_assert(2 * AK * AMAXB <= CL_WS_DOUBLES, "reduction regions fit the workspace");
 
-__device__ unsigned int a_bar_count = 0;
-__device__ unsigned int a_bar_gen = 0;
-
 struct AOut {
+    unsigned long long ctr;  // grid-barrier arrival counter (monotonic, grid_bar.cuh)
     int iterations, n_records, n_gnorms, hit_cap, status, ax_is_ax2, err;
     unsigned long long t0;   // global timer at the start
 };
 __device__ AOut a_out;
+__shared__ unsigned long long s_tgt;
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -52,28 +52,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-__device__ void a_sync(unsigned nblk) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned gen = atomicAdd(&a_bar_gen, 0u);
-        __threadfence();
-        if (atomicAdd(&a_bar_count, 1u) == nblk - 1) {
-            atomicExch(&a_bar_count, 0u);
-            __threadfence();
-            atomicAdd(&a_bar_gen, 1u);
-        } else {
-            const long long t0 = clock64();
-            volatile unsigned* vg = &a_bar_gen;
-            while (*vg == gen) {
-                if (clock64() - t0 > (1LL << 31)) {     // ~1 s: give up rather than hang
-                    a_out.err = 1;
-                    break;
-                }
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
+__device__ __forceinline__ void a_sync(unsigned) {
+    const GridBar b = {&a_out.ctr, 0, &a_out.err};
+    grid_bar(b, &s_tgt);
 }
 
 __device__ __forceinline__ double2 ldcg2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
@@ -241,6 +222,7 @@ struct Az {
     int h2;
     double* rec;      // device: 4 * rec_cap
     double* gnorms;   // device: rec_cap
+    unsigned long long bar_base;
 };
 
 struct Lanes {
@@ -378,6 +360,7 @@ __global__ void __launch_bounds__(AT) alm_fused_kernel(Az z) {
     int region = 0;
     double v[AK];
     if (writer) a_out.t0 = gtimer();
+    if (t0) s_tgt = z.bar_base;
 
     if (t0) {
         c.cap = a.memory;
@@ -672,6 +655,7 @@ __global__ void __launch_bounds__(AT) alm_fused_kernel(Az z) {
 double* g_scratch = nullptr;
 int64_t g_scratch_cap = 0;
 int g_max_blocks = 0;
+unsigned long long g_bar_base = 0;
 
 double host_now() {
     timespec ts;
@@ -713,6 +697,7 @@ extern "C" int cl_alm_inner_diag_fused(const cl_alm_inner_args* a, cl_alm_inner_
     z.h2 = a->ld / 2;
     z.G = z.h2 <= 1 ? 1 : z.h2 <= 2 ? 2 : z.h2 <= 4 ? 4 : z.h2 <= 8 ? 8 : z.h2 <= 16 ? 16 : 32;
     z.rec = g_scratch;
+    z.bar_base = g_bar_base;
     z.gnorms = g_scratch + 4 * (int64_t)(a->rec_cap > 0 ? a->rec_cap : 1);
     int64_t nb = (a->n * z.G + AT - 1) / AT;   // one row per lane group
     if (nb > g_max_blocks) nb = g_max_blocks;
@@ -725,12 +710,12 @@ extern "C" int cl_alm_inner_diag_fused(const cl_alm_inner_args* a, cl_alm_inner_
     if (e != cudaSuccess) return (int)e;
     AOut o;
     memcpy(&o, a->host, sizeof(o));
+    g_bar_base = o.ctr;
     if (o.err) {
         AOut zz;
         memset(&zz, 0, sizeof(zz));
-        const unsigned zero = 0;
         cudaMemcpyToSymbol(a_out, &zz, sizeof(zz));
-        cudaMemcpyToSymbol(a_bar_count, &zero, sizeof(zero));
+        g_bar_base = 0;
         return CL_EARG + 1;
     }
     const int nrec = o.n_records < a->rec_cap ? o.n_records : a->rec_cap;

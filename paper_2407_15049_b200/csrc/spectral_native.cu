@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include "culorads.h"
+#include "grid_bar.cuh"
 
 namespace {
 
@@ -122,36 +123,17 @@ namespace {
 constexpr int LT = 256;
 constexpr int LW = LT / 32;
 
-__device__ unsigned int lz_bar_count = 0;
-__device__ unsigned int lz_bar_gen = 0;
 struct LzOut {
+    unsigned long long ctr;  // grid-barrier arrival counter (monotonic, grid_bar.cuh)
     int k;
     int err;
 };
 __device__ LzOut lz_out;
+__shared__ unsigned long long s_tgt;
 
-__device__ void lz_sync(unsigned nblk) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned gen = atomicAdd(&lz_bar_gen, 0u);
-        __threadfence();
-        if (atomicAdd(&lz_bar_count, 1u) == nblk - 1) {
-            atomicExch(&lz_bar_count, 0u);
-            __threadfence();
-            atomicAdd(&lz_bar_gen, 1u);
-        } else {
-            const long long t0 = clock64();
-            volatile unsigned* vg = &lz_bar_gen;
-            while (*vg == gen) {
-                if (clock64() - t0 > (1LL << 31)) {     // ~1 s: give up rather than hang
-                    lz_out.err = 1;
-                    break;
-                }
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
+__device__ __forceinline__ void lz_sync(unsigned) {
+    const GridBar b = {&lz_out.ctr, 0, &lz_out.err};
+    grid_bar(b, &s_tgt);
 }
 
 // grid-wide sum of one value per thread, identical in every thread
@@ -199,6 +181,7 @@ struct Lz {
     double* alpha;
     double* beta;
     double* ws;
+    unsigned long long bar_base;
 };
 
 __global__ void __launch_bounds__(LT) lanczos_fused_kernel(Lz z) {
@@ -208,6 +191,7 @@ __global__ void __launch_bounds__(LT) lanczos_fused_kernel(Lz z) {
     const int lane = threadIdx.x & 31;
     const int gw = (int)((blockIdx.x * LT + threadIdx.x) >> 5), nw = (int)(gridDim.x * LW);
     int region = 0;
+    if (threadIdx.x == 0) s_tgt = z.bar_base;
     double amax = 0.0;
     bool anan = false;
     int k = 0;
@@ -293,6 +277,7 @@ __global__ void __launch_bounds__(LT) lanczos_fused_kernel(Lz z) {
 }
 
 int lz_max_blocks = 0;
+unsigned long long lz_bar_base = 0;
 
 }  // namespace
 
@@ -320,6 +305,7 @@ extern "C" int cl_lanczos_loop_fused(const cl_lanczos_args* a, int32_t* k_out) {
     z.u = a->u; z.r = a->r; z.h = a->h;
     z.indptr = a->S.indptr; z.indices = a->S.indices; z.vals = a->S.cv;
     z.alpha = a->dalpha; z.beta = a->dbeta; z.ws = a->ws;
+    z.bar_base = lz_bar_base;
     // one row per thread, and at least 128 warps for the projections
     int64_t nb = (a->n + LT - 1) / LT;
     if (nb < 16) nb = 16;
@@ -332,12 +318,12 @@ extern "C" int cl_lanczos_loop_fused(const cl_lanczos_args* a, int32_t* k_out) {
     if (e != cudaSuccess) return (int)e;
     LzOut o;
     memcpy(&o, a->host, sizeof(o));
+    lz_bar_base = o.ctr;
     if (o.err) {
         LzOut zz;
         memset(&zz, 0, sizeof(zz));
-        const unsigned zero = 0;
         cudaMemcpyToSymbol(lz_out, &zz, sizeof(zz));
-        cudaMemcpyToSymbol(lz_bar_count, &zero, sizeof(zero));
+        lz_bar_base = 0;
         return CL_EARG + 1;
     }
     const int k = o.k;
