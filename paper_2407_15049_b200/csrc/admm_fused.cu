@@ -27,11 +27,14 @@
 #include <string.h>
 
 #include "culorads.h"
+#include "fused_rows.cuh"
 #include "grid_bar.cuh"
 
 namespace {
 
-constexpr int FT = 256;                 // threads per block
+using namespace fused;
+
+constexpr int FT = THREADS;             // threads per block
 constexpr int FW = FT / 32;
 constexpr int FMAXB = CL_RED_BLOCKS;    // partial slots per reduced value
 constexpr int FK = 3;                   // values per reduction (max)
@@ -50,13 +53,6 @@ struct FzOut {
 };
 __device__ FzOut g_out;
 __shared__ unsigned long long s_tgt;
-
-__device__ __forceinline__ double2 ldcg2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
-__device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
-__device__ __forceinline__ double dot2(double2 a, double2 b) { return fma(a.y, b.y, __dmul_rn(a.x, b.x)); }
-__device__ __forceinline__ double2 axpy2(double a, double2 x, double2 y) {
-    return make_double2(fma(a, x.x, y.x), fma(a, x.y, y.y));
-}
 
 __device__ __forceinline__ void grid_sync(unsigned) {
     const GridBar b = {&g_out.ctr, 0, &g_out.err};
@@ -106,30 +102,12 @@ __device__ void greduce(double (&v)[K], double* ws, int& region) {
     region ^= 1;
 }
 
-// lanes of one row: group g of G lanes, gl = lane within the group
-struct Lanes {
-    int gl;
-    unsigned mask;
-    int64_t first, stride;   // rows: first, first + stride, ...
-};
-
-__device__ __forceinline__ Lanes lanes(int G) {
-    Lanes L;
-    const int lane = threadIdx.x & 31;
-    L.gl = lane % G;
-    L.mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - L.gl));
-    L.first = ((int64_t)blockIdx.x * FT + threadIdx.x) / G;
-    L.stride = (int64_t)gridDim.x * FT / G;
-    return L;
-}
-
 // <X_i, Y_i> over the row's units, reduced over the row's lanes (all lanes get it)
 __device__ __forceinline__ double row_dot(const Lanes& L, int G, int h2, const double* X, const double* Y,
                                           int64_t i) {
     double s = 0.0;
     for (int u = L.gl; u < h2; u += G) s += dot2(ldcg2(X + 2 * (i * h2 + u)), ldcg2(Y + 2 * (i * h2 + u)));
-    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(L.mask, s, o);
-    return s;
+    return gsum(L, G, s);
 }
 
 // Half-step start (cl_diag_admm_cg_init): rhs = -scale C Wf + rho Wf + a (rho b - lam) Wf,
@@ -222,7 +200,7 @@ __device__ int cg_loop(const Fz& f, const double* x0, double* x, const double* W
                 st2(p + off, pv);
                 sd += dot2(pv, ldcg2(Wf + off));
             }
-            for (int o = G / 2; o > 0; o >>= 1) sd += __shfl_xor_sync(L.mask, sd, o);
+            sd = gsum(L, G, sd);
             const double av = __ldg(a.aval + i);
             const double c = a.rho * (av * (av * sd));
             for (int u = L.gl; u < h2; u += G) {
@@ -426,7 +404,7 @@ extern "C" int cl_admm_step_diag_fused(const cl_admm_diag_args* a, cl_admm_step_
     Fz f;
     f.a = *a;
     f.h2 = a->ld / 2;
-    f.G = f.h2 <= 1 ? 1 : f.h2 <= 2 ? 2 : f.h2 <= 4 ? 4 : f.h2 <= 8 ? 8 : f.h2 <= 16 ? 16 : 32;
+    f.G = lanes_for(f.h2);
     f.rel = 0.0;
     f.bar_base = g_bar_base;
     // FZ_ROWS rows per lane group: latency (gather chains) against barrier cost (blocks)

@@ -26,11 +26,14 @@
 #include <time.h>
 
 #include "culorads.h"
+#include "fused_rows.cuh"
 #include "grid_bar.cuh"
 
 namespace {
 
-constexpr int AT = 256;
+using namespace fused;
+
+constexpr int AT = THREADS;
 constexpr int AW = AT / 32;
 constexpr int AMAXB = 512;                         // blocks (ws: 2 regions x AK x AMAXB doubles)
 constexpr int AMAXH = 2 * CL_ALM_MAXMEM + 1;       // history operands of the update
@@ -55,13 +58,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void a_sync(unsigned) {
     const GridBar b = {&a_out.ctr, 0, &a_out.err};
     grid_bar(b, &s_tgt);
-}
-
-__device__ __forceinline__ double2 ldcg2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
-__device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
-__device__ __forceinline__ double dot2(double2 a, double2 b) { return fma(a.y, b.y, __dmul_rn(a.x, b.x)); }
-__device__ __forceinline__ double2 axpy2(double a, double2 x, double2 y) {
-    return make_double2(fma(a, x.x, y.x), fma(a, x.y, y.y));
 }
 
 // Sum of K (<= AK) per-thread values over the grid, identical in every thread.
@@ -224,27 +220,6 @@ struct Az {
     double* gnorms;   // device: rec_cap
     unsigned long long bar_base;
 };
-
-struct Lanes {
-    int gl;
-    unsigned mask;
-    int64_t first, stride;
-};
-
-__device__ __forceinline__ Lanes lanes(int G) {
-    Lanes L;
-    const int lane = threadIdx.x & 31;
-    L.gl = lane % G;
-    L.mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - L.gl));
-    L.first = ((int64_t)blockIdx.x * AT + threadIdx.x) / G;
-    L.stride = (int64_t)gridDim.x * AT / G;
-    return L;
-}
-
-__device__ __forceinline__ double gsum(const Lanes& L, int G, double s) {
-    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(L.mask, s, o);
-    return s;
-}
 
 // C X for one column unit of row i (sequential over the row's slots, as the tiled SpMM)
 __device__ __forceinline__ double2 c_row(const cl_pattern& P, const double* X, int h2, int64_t s0, int64_t s1, int u) {
@@ -695,7 +670,7 @@ extern "C" int cl_alm_inner_diag_fused(const cl_alm_inner_args* a, cl_alm_inner_
     Az z;
     z.a = *a;
     z.h2 = a->ld / 2;
-    z.G = z.h2 <= 1 ? 1 : z.h2 <= 2 ? 2 : z.h2 <= 4 ? 4 : z.h2 <= 8 ? 8 : z.h2 <= 16 ? 16 : 32;
+    z.G = lanes_for(z.h2);
     z.rec = g_scratch;
     z.bar_base = g_bar_base;
     z.gnorms = g_scratch + 4 * (int64_t)(a->rec_cap > 0 ? a->rec_cap : 1);
