@@ -321,10 +321,20 @@ def _resid(ops, ax, res, at):
 
 
 NATIVE = True     # diagonal constraints, one device: run the step's control flow in C++
-# Problems with n*ld at most this many doubles run each ADMM step as one cooperative
-# launch (cl_admm_step_diag_fused): there, latency rather than HBM bounds the step.
+# Problems with at most this many row-lanes (n times the lanes that share a factor row,
+# lanes_for(ld)) run each ADMM step as one cooperative launch (cl_admm_step_diag_fused):
+# there, latency rather than HBM bounds the step (measured crossover).
 FUSED = os.environ.get("CULORADS_FUSED", "1") != "0"
-FUSED_MAX_ELEMS = int(os.environ.get("CULORADS_FUSED_MAX", 1 << 18))
+FUSED_MAX_LANES = int(os.environ.get("CULORADS_FUSED_MAX", 1 << 19))
+
+
+def lanes_for(ld):
+    """Lanes per factor row of the one-launch kernels (fused_rows.cuh lanes_for)."""
+    h2 = max(ld // 2, 1)
+    g = 1
+    while g < h2 and g < 32:
+        g *= 2
+    return g
 
 
 def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, hs, pool):
@@ -365,7 +375,7 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
     a.ws = dev.ws.data_ptr()
     a.stream = dev.stream.cuda_stream
     st = _lib.AdmmStepStats()
-    if FUSED and n >= 1 and n * ld <= FUSED_MAX_ELEMS:
+    if FUSED and n >= 1 and n * lanes_for(ld) <= FUSED_MAX_LANES:
         rc = dev.lib.cl_admm_step_diag_fused(ctypes.byref(a), ctypes.byref(st))
         dev.launches += 1
         _lib.check(rc, "cl_admm_step_diag_fused")

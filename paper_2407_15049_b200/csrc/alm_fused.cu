@@ -659,13 +659,14 @@ extern "C" int cl_alm_inner_diag_fused(const cl_alm_inner_args* a, cl_alm_inner_
         if (g_max_blocks < 1) return CL_EARG;
     }
     const int64_t need = 5 * (int64_t)(a->rec_cap > 0 ? a->rec_cap : 1);
-    if (need > g_scratch_cap) {
-        if (g_scratch) cudaFree(g_scratch);
+    if (need > g_scratch_cap) {   // stream-ordered: no device-wide synchronize
+        if (g_scratch) cudaFreeAsync(g_scratch, st);
         g_scratch = nullptr;
         g_scratch_cap = 0;
-        cudaError_t e = cudaMalloc(&g_scratch, sizeof(double) * (size_t)need);
+        const int64_t cap = need < 4096 ? 4096 : need;
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&g_scratch), sizeof(double) * (size_t)cap, st);
         if (e != cudaSuccess) return (int)e;
-        g_scratch_cap = need;
+        g_scratch_cap = cap;
     }
     Az z;
     z.a = *a;

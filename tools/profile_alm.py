@@ -1,6 +1,6 @@
 """Time ALM inner iterations and ADMM steps of the device solver on synthetic MaxCut (dev probe).
 
-    python tools/profile_alm.py N DEG ALM_ITERS ADMM_STEPS
+    python tools/profile_alm.py N DEG ALM_ITERS ADMM_STEPS [RANK]
 """
 import math
 import os
@@ -21,7 +21,7 @@ steps = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 p = problem.build_maxcut(graphs.random_sparse(n, deg=deg, seed=0))
 ops = linops.build_operators(p)
 dev = ops.dev
-r = driver.initial_rank(p.m, p.n)
+r = int(sys.argv[5]) if len(sys.argv) > 5 else driver.initial_rank(p.m, p.n)
 ld = padded_ld(r)
 rng = np.random.default_rng(0)
 R = linops.to_factor(rng.standard_normal((n, r)) / math.sqrt(n * r), dev, ld)
