@@ -148,11 +148,25 @@ __device__ void cg_init(const Fz& f, const double* x0, const double* Wf, double*
                     acc.y = fma(c[t], x[t].y, acc.y);
                 }
             }
-            for (; s < s1; ++s) {
-                const double c = __ldg(cv + s);
-                const double2 x = ldcg2(Wf + 2 * ((int64_t)__ldg(ix + s) * h2 + u));
-                acc.x = fma(c, x.x, acc.x);
-                acc.y = fma(c, x.y, acc.y);
+            if (s < s1) {   // the last partial chunk, predicated: its gathers are in flight together
+                int j[FZ_UNROLL];
+                double c[FZ_UNROLL];
+                double2 x[FZ_UNROLL];
+#pragma unroll
+                for (int t = 0; t < FZ_UNROLL; ++t) {
+                    const bool ok = s + t < s1;
+                    j[t] = ok ? __ldg(ix + s + t) : 0;
+                    c[t] = ok ? __ldg(cv + s + t) : 0.0;
+                }
+#pragma unroll
+                for (int t = 0; t < FZ_UNROLL; ++t)
+                    x[t] = s + t < s1 ? ldcg2(Wf + 2 * ((int64_t)j[t] * h2 + u)) : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int t = 0; t < FZ_UNROLL; ++t)
+                    if (s + t < s1) {
+                        acc.x = fma(c[t], x[t].x, acc.x);
+                        acc.y = fma(c[t], x[t].y, acc.y);
+                    }
             }
             const int64_t off = 2 * (i * h2 + u);
             const double2 yv = ldcg2(Wf + off), zv = ldcg2(x0 + off);

@@ -242,11 +242,24 @@ __device__ __forceinline__ double2 c_row(const cl_pattern& P, const double* X, i
             acc.y = fma(c[t], x[t].y, acc.y);
         }
     }
-    for (; s < s1; ++s) {
-        const double c = __ldg(P.cv + s);
-        const double2 x = ldcg2(X + 2 * ((int64_t)__ldg(P.indices + s) * h2 + u));
-        acc.x = fma(c, x.x, acc.x);
-        acc.y = fma(c, x.y, acc.y);
+    if (s < s1) {   // the last partial chunk, predicated: its gathers are in flight together
+        int j[8];
+        double c[8];
+        double2 x[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const bool ok = s + t < s1;
+            j[t] = ok ? __ldg(P.indices + s + t) : 0;
+            c[t] = ok ? __ldg(P.cv + s + t) : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) x[t] = s + t < s1 ? ldcg2(X + 2 * ((int64_t)j[t] * h2 + u)) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            if (s + t < s1) {
+                acc.x = fma(c[t], x[t].x, acc.x);
+                acc.y = fma(c[t], x[t].y, acc.y);
+            }
     }
     return acc;
 }
