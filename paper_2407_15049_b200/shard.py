@@ -412,7 +412,11 @@ def build_sharded_operators(p, rank, world, dev, group=None):
 
 
 def solve_sharded(p, cfg=None, *, group=None, dev=None):
-    """driver.solve on this rank's row block; every rank returns the same report."""
+    """driver.solve on this rank's row block; every rank returns the same report.
+
+    With ``cfg.reorder`` the rows are first relabelled in the locality order (as the
+    1-GPU solve does); the report's U/V/lam are then this rank's block in that labelling
+    and ``report.perm`` maps it back (row k is the caller's row perm[k])."""
     from . import driver
     from .device import default_device
 
@@ -420,5 +424,18 @@ def solve_sharded(p, cfg=None, *, group=None, dev=None):
     rank = dist.get_rank(group)
     dev = dev or default_device()
     dev.world, dev.group = world, group
-    ops = build_sharded_operators(p, rank, world, dev, group)
+    cfg = cfg or driver.SolverConfig()
+    solve_p, perm = p, None
+    if cfg.reorder:
+        # the locality order (reorder.py) is computed identically on every rank; contiguous
+        # row blocks of a mesh in this order touch only neighbouring blocks, so halos shrink
+        # from most of the factor to the band at the block boundaries
+        from . import reorder
+        order = reorder.locality_order(p)
+        if reorder.locality_gain(p, order) >= 2.0:
+            solve_p, _ = reorder.permute(p, order)
+            perm = order
+    ops = build_sharded_operators(solve_p, rank, world, dev, group)
+    if perm is not None:
+        ops.perm = perm
     return driver.solve(p, cfg, ops=ops)

@@ -92,10 +92,10 @@ def _lanczos_smallest(op, n, seed, max_basis, dev, rows=None, perm=None):
     betas = np.zeros(max(k_max - 1, 0))
     q0 = rng.standard_normal(n_all)
     q0 /= np.linalg.norm(q0)
-    if rows is not None:
-        q0 = q0[rows[0]:rows[1]]
     if perm is not None:
         q0 = q0[perm]              # locality-ordered operator: the same start vector, relabelled
+    if rows is not None:
+        q0 = q0[rows[0]:rows[1]]
     Q[0, :n] = torch.as_tensor(q0).to(dev.dev)
     u = dev.zeros(npad)
     r = dev.zeros(npad)
