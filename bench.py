@@ -327,6 +327,11 @@ def run_ours(args, rank, world, local_rank):
     else:
         # weak scaling: every rank owns n rows of one random graph on world*n vertices;
         # remote factor rows arrive by the halo all-gather inside the SpMM (shard.py)
+        if args.graph != "random" or args.reorder:
+            if rank == 0:
+                print("bench: --graph/--reorder apply at N=1 only (the N>1 instance is generated "
+                      "per rank); running the random graph", file=sys.stderr)
+            args.graph, args.reorder = "random", False
         from paper_2407_15049_b200 import shard
         dev.group, dev.world = None, world
         ops = shard.sharded_maxcut_ops(world * n, args.deg, args.seed, rank, world, dev)
