@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-solver", action="store_true", help="skip the solver-level rates and the G1 solve")
+    ap.add_argument("--no-completion", action="store_true",
+                    help="skip the matrix-completion operator rates (configs[3] at one GPU's share)")
     ap.add_argument("--n-g1", type=int, default=800)
     ap.add_argument("--graph", choices=("random", "delaunay"), default="random",
                     help="random: BASELINE configs[2] (default); delaunay: mesh-like graph of degree 6")
@@ -251,6 +253,83 @@ def solver_rates(ops, dev, R, n, r, ld, n_g1):
         "trace_rows": len(rep.trace_rows), "cpu_trace_rows": len(ref["trace"]),
     }
     return out
+
+
+def completion_rates(dev, peak, n_total, m, seed):
+    """BASELINE configs[3] (matrix completion, n = 2e7, m = 2e8 sampled entries, row-sharded
+    over 8 GPUs) at one GPU's share: n_total rows, m entries. Per-kernel CUDA-event times
+    and algorithmic GB/s of the completion operators, plus ALM / ADMM iteration rates."""
+    import torch
+
+    from paper_2407_15049_b200 import admm, alm, driver, graphs, linops, problem
+    from paper_2407_15049_b200 import roofline as RL
+    from paper_2407_15049_b200.device import padded_ld
+
+    t0 = time.perf_counter()
+    half = int(n_total) // 2
+    p = problem.build_matrix_completion(graphs.random_completion(half, int(n_total) - half, int(m), seed=seed))
+    ops = linops.build_operators(p, dev=dev)
+    t_build = time.perf_counter() - t0
+    r = driver.initial_rank(p.m, p.n)
+    ld = padded_ld(r)
+    rng = np.random.default_rng(seed)
+    U = linops.to_factor(rng.standard_normal((p.n, r)) / math.sqrt(p.n), dev, ld)
+    V = linops.to_factor(rng.standard_normal((p.n, r)) / math.sqrt(p.n), dev, ld)
+    lam = linops.to_vec(rng.standard_normal(p.m), dev)
+    out = dev.empty(p.n, ld)
+    y = dev.empty(p.m)
+
+    def timeit(fn, reps=10):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(dev.stream)
+        for _ in range(reps):
+            fn()
+        e1.record(dev.stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    con = ops.cop.con
+    nnz_a = int(con.pi.numel())
+    om = ops.adj.omega
+    apat = ops.adj.apat
+    hs = admm.HalfStep(ops, p.n, ld)
+    kern = {}
+    for name, fn, nbytes in (
+            ("constraint_eval A(UV^T)", lambda: dev.constraint_eval(con, ld, U, V, y),
+             RL.constraint_eval_bytes(p.m, nnz_a, ld)),
+            ("adjoint SpMM (C + A*(lam)) V", lambda: dev.spmm(om, V, ld, out=out, c_coeff=1.0, w1=lam),
+             RL.pattern_spmm_bytes(p.n, om.nnz, ld, at_entries=int(om.at_con.numel()) if om.at_con is not None
+                                   else 0)),
+            ("ADMM operator (single-entry fused)", lambda: hs.apply(U, V, 1.5, out, dot_with=U, at=0),
+             p.n * (RL.I8 + 3 * ld * RL.F8) + apat.nnz * (RL.I4 + RL.F8 + 2 * ld * RL.F8))):
+        ms = timeit(fn)
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        kern[name] = {"ms": ms, "bytes": int(nbytes), "GB/s": gbs, "frac": gbs / peak}
+    dual = alm.DualVector(lam=lam.clone(), rho=2.0)
+    core = alm.AlmCore(ops, p.n, ld)
+    R = U.clone()
+    alm._inner(core, R, dual.lam, 2.0, 1.0, 0.0, 3, None, 8, alm._RankRecorder(None, r))
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    res = alm._inner(core, R, dual.lam, 2.0, 1.0, 0.0, 10, None, 8, alm._RankRecorder(None, r))
+    torch.cuda.synchronize()
+    alm_ms = 1e3 * (time.perf_counter() - t) / max(res.iterations, 1)
+    st = admm.AdmmState(U=U.clone(), V=V.clone(), dual=dual, r=r)
+    pool = admm._Pool(dev, p.n, ld)
+    admm.admm_step(st, ops, hs=hs, pool=pool)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    cg = 0
+    for _ in range(2):
+        s_ = admm.admm_step(st, ops, hs=hs, pool=pool)
+        cg += s_.cg_iters_u + s_.cg_iters_v
+    torch.cuda.synchronize()
+    admm_ms = 1e3 * (time.perf_counter() - t) / 2
+    return {"instance": f"matrix completion n={p.n}, m={p.m} sampled entries (BASELINE configs[3] at one "
+                        f"of 8 GPUs' share), rank {r}, ld {ld}", "build_s": t_build, "kernels": kern,
+            "alm_inner_ms_per_iter": alm_ms, "admm_ms_per_step": admm_ms, "admm_cg_iters_per_step": cg / 2}
 
 
 def run_reference(args, rank):
@@ -479,6 +558,9 @@ def run_ours(args, rank, world, local_rank):
     solver = None
     if world == 1 and not args.no_solver:
         solver = solver_rates(ops, dev, R, n, r, ld, args.n_g1)
+    completion = None
+    if world == 1 and not args.no_completion:
+        completion = completion_rates(dev, peak, 2.5e6, 2.5e7, args.seed)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         n_s = int(min(n, 2e6))
@@ -507,6 +589,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "solver": solver,
+        "completion": completion,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -37,7 +37,7 @@ def test_reference_arm_line():
 
 @pytest.mark.gpu
 def test_device_arm_line():
-    d = _run("--steps", "2", "--warmup", "3", "--nrows", "200000", "--no-cpu-baseline", "--no-solver")
+    d = _run("--steps", "2", "--warmup", "3", "--nrows", "200000", "--no-cpu-baseline", "--no-solver", "--no-completion")
     assert d["metric"] == _metric() and d["unit"] == "GB/s" and d["value"] > 0
     assert d["steps"] == 2 and d["warmup"] == 3 and d["dtype"] == "f64" and d["vs_baseline"] is None
     assert d["config"]["workload"] and "model" not in d["config"]
