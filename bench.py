@@ -206,7 +206,7 @@ def solver_rates(ops, dev, R, n, r, ld, n_g1):
     core = alm.AlmCore(ops, n, ld)
     Rw = R.clone()
     rec = alm._RankRecorder(None, r)
-    alm._inner(core, Rw, dual.lam, rho, 1.0, 0.0, 3, None, 8, rec)
+    alm._inner(core, Rw.clone(), dual.lam, rho, 1.0, 0.0, 20, None, 8, rec)   # warm-up: fills the history pool
     torch.cuda.synchronize()
     t = time.perf_counter()
     res = alm._inner(core, Rw, dual.lam, rho, 1.0, 0.0, 20, None, 8, rec)
@@ -310,7 +310,7 @@ def completion_rates(dev, peak, n_total, m, seed):
     dual = alm.DualVector(lam=lam.clone(), rho=2.0)
     core = alm.AlmCore(ops, p.n, ld)
     R = U.clone()
-    alm._inner(core, R, dual.lam, 2.0, 1.0, 0.0, 3, None, 8, alm._RankRecorder(None, r))
+    alm._inner(core, R.clone(), dual.lam, 2.0, 1.0, 0.0, 10, None, 8, alm._RankRecorder(None, r))   # warm-up: fills the history pool
     torch.cuda.synchronize()
     t = time.perf_counter()
     res = alm._inner(core, R, dual.lam, 2.0, 1.0, 0.0, 10, None, 8, alm._RankRecorder(None, r))

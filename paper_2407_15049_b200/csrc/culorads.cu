@@ -395,7 +395,7 @@ __device__ __forceinline__ double group_dot_rows(const double* __restrict__ x, c
     return p;
 }
 
-template <int G, int VEC>
+template <int G, int VEC, int NP>    // NP = 1: X1 Y1 only (A(UV^T)); 3: up to three products
 __global__ void __launch_bounds__(NT) constraint_kernel(int64_t m, const int64_t* __restrict__ indptr,
                                                         const int32_t* __restrict__ pi,
                                                         const int32_t* __restrict__ pj,
@@ -409,6 +409,88 @@ __global__ void __launch_bounds__(NT) constraint_kernel(int64_t m, const int64_t
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - gl));
     const int64_t groups_total = (int64_t)gridDim.x * (NT / G);
     const int64_t nw = gh.nown;
+    if (VEC == 2 && ld <= 2 * G) {
+        // One double2 per lane per row: the positions of two nonzeros are read, then all
+        // their gathers are issued together, then reduced in the order of the general
+        // loop below (same arithmetic, bit for bit; fewer dependent memory round trips).
+        const int col = gl * 2;
+        const bool act = col < ld;
+        const double2 z2 = make_double2(0.0, 0.0);
+        for (int64_t c = ((int64_t)blockIdx.x * NT + threadIdx.x) / G; c < m; c += groups_total) {
+            const int64_t t0 = __ldg(indptr + c), t1 = __ldg(indptr + c + 1);
+            double a1 = 0.0, a2 = 0.0;
+            for (int64_t t = t0; t < t1; t += 2) {
+                const bool two = t + 1 < t1;
+                const int64_t i0 = __ldg(pi + t), j0 = __ldg(pj + t);
+                const int64_t i1 = two ? (int64_t)__ldg(pi + t + 1) : i0, j1 = two ? (int64_t)__ldg(pj + t + 1) : j0;
+                const double v0 = __ldg(val + t), v1 = two ? __ldg(val + t + 1) : 0.0;
+                double2 x1a = z2, y1a = z2, x1b = z2, y1b = z2, x2a = z2, y2a = z2, x2b = z2, y2b = z2;
+                double2 x3a = z2, y3a = z2, x3b = z2, y3b = z2;
+                if (act) {
+                    x1a = ld2(grow(X1, gh.g[0], i0, nw, ld) + col);
+                    y1a = ld2(grow(Y1, gh.g[1], j0, nw, ld) + col);
+                    if (two) {
+                        x1b = ld2(grow(X1, gh.g[0], i1, nw, ld) + col);
+                        y1b = ld2(grow(Y1, gh.g[1], j1, nw, ld) + col);
+                    }
+                    if (NP > 1 && X2 != nullptr) {
+                        x2a = ld2(grow(X2, gh.g[2], i0, nw, ld) + col);
+                        y2a = ld2(grow(Y2, gh.g[3], j0, nw, ld) + col);
+                        if (two) {
+                            x2b = ld2(grow(X2, gh.g[2], i1, nw, ld) + col);
+                            y2b = ld2(grow(Y2, gh.g[3], j1, nw, ld) + col);
+                        }
+                    }
+                    if (NP > 1 && X3 != nullptr) {
+                        x3a = ld2(grow(X3, gh.g[4], i0, nw, ld) + col);
+                        y3a = ld2(grow(Y3, gh.g[5], j0, nw, ld) + col);
+                        if (two) {
+                            x3b = ld2(grow(X3, gh.g[4], i1, nw, ld) + col);
+                            y3b = ld2(grow(Y3, gh.g[5], j1, nw, ld) + col);
+                        }
+                    }
+                }
+                double p1a = 0.0, p1b = 0.0, p2a = 0.0, p2b = 0.0, p3a = 0.0, p3b = 0.0;
+                if (act) {
+                    p1a += dot2(x1a, y1a);
+                    p1b += dot2(x1b, y1b);
+                    if (NP > 1) {
+                        p2a += dot2(x2a, y2a);
+                        p2b += dot2(x2b, y2b);
+                        p3a += dot2(x3a, y3a);
+                        p3b += dot2(x3b, y3b);
+                    }
+                }
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) {
+                    p1a += __shfl_xor_sync(gmask, p1a, o);
+                    p1b += __shfl_xor_sync(gmask, p1b, o);
+                    if (NP > 1) {
+                        p2a += __shfl_xor_sync(gmask, p2a, o);
+                        p2b += __shfl_xor_sync(gmask, p2b, o);
+                        p3a += __shfl_xor_sync(gmask, p3a, o);
+                        p3b += __shfl_xor_sync(gmask, p3b, o);
+                    }
+                }
+                double xa = p1a, xb = p1b;
+                if (NP > 1 && X2 != nullptr) {
+                    xa += p2a;
+                    xb += p2b;
+                }
+                a1 += v0 * xa;
+                if (NP > 1 && X3 != nullptr) a2 += v0 * p3a;
+                if (two) {
+                    a1 += v1 * xb;
+                    if (NP > 1 && X3 != nullptr) a2 += v1 * p3b;
+                }
+            }
+            if (gl == 0) {
+                out1[c] = a1;
+                if (X3 != nullptr) out2[c] = a2;
+            }
+        }
+        return;
+    }
     for (int64_t c = ((int64_t)blockIdx.x * NT + threadIdx.x) / G; c < m; c += groups_total) {
         const int64_t t0 = __ldg(indptr + c), t1 = __ldg(indptr + c + 1);
         double a1 = 0.0, a2 = 0.0;
@@ -1668,10 +1750,16 @@ int cl_constraint_eval_halo(int64_t m, const int64_t* indptr, const int32_t* pi,
     const int64_t threads = m * G;
     int64_t g = (threads + NT - 1) / NT;
     const int grid = (int)(g > 65535 * 8 ? 65535 * 8 : g);
-#define CL_CK(GG)                                                                                           \
-    constraint_kernel<GG, 2><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2, gh)
+    const bool one = X2 == nullptr && X3 == nullptr;
+#define CL_CK(GG)                                                                                             \
+    if (one)                                                                                                  \
+        constraint_kernel<GG, 2, 1><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, \
+                                                         out2, gh);                                           \
+    else                                                                                                      \
+        constraint_kernel<GG, 2, 3><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, \
+                                                         out2, gh)
     if (ld == 1) {
-        constraint_kernel<1, 1><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2, gh);
+        constraint_kernel<1, 1, 3><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2, gh);
     } else {
         switch (G) {
             case 1: CL_CK(1); break;

@@ -60,7 +60,7 @@ timeit("half-step apply (generic)", lambda: hs.apply(U, V, 1.5, out, dot_with=U,
 dual = alm.DualVector(lam=lam.clone(), rho=2.0)
 core = alm.AlmCore(ops, p.n, ld)
 R = U.clone()
-alm._inner(core, R, dual.lam, 2.0, 1.0, 0.0, 3, None, 8, alm._RankRecorder(None, r))
+alm._inner(core, R.clone(), dual.lam, 2.0, 1.0, 0.0, 10, None, 8, alm._RankRecorder(None, r))   # warm-up: fills the history pool
 torch.cuda.synchronize()
 t = time.perf_counter()
 res = alm._inner(core, R, dual.lam, 2.0, 1.0, 0.0, 10, None, 8, alm._RankRecorder(None, r))
