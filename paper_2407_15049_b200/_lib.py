@@ -23,6 +23,20 @@ CL_WS_ALLOC = CL_WS_DOUBLES + 8
 CL_OUT = 255
 CL_DOT_PAIRS, CL_DOT_OUT_ALL, CL_DOT_FIRST_TWO = 0, 1, 2
 CL_EARG = 1001
+# cudaError codes with which a cooperative launch is refused before anything runs
+# (LaunchOutOfResources, CooperativeLaunchTooLarge, NotPermitted, NotSupported): the
+# one-launch paths then give way to the multi-launch ones
+COOP_REFUSED = (701, 720, 800, 801)
+
+
+def coop_refused(rc, what):
+    """True (with a one-time warning) when a cooperative launch was refused."""
+    if rc not in COOP_REFUSED:
+        return False
+    import warnings
+    warnings.warn(f"{what}: cooperative launch refused (cudaError {rc}); using the multi-launch path",
+                  RuntimeWarning, stacklevel=3)
+    return True
 
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint_eval_halo",
            "cl_diag_constraint_eval", "cl_sddmm",

@@ -374,12 +374,17 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
     a.host = dev.host.data_ptr() + 8 * 470
     a.ws = dev.ws.data_ptr()
     a.stream = dev.stream.cuda_stream
+    global FUSED
     st = _lib.AdmmStepStats()
-    if FUSED and n >= 1 and n * lanes_for(ld) <= FUSED_MAX_LANES:
+    fused = FUSED and n >= 1 and n * lanes_for(ld) <= FUSED_MAX_LANES
+    if fused:
         rc = dev.lib.cl_admm_step_diag_fused(ctypes.byref(a), ctypes.byref(st))
-        dev.launches += 1
-        _lib.check(rc, "cl_admm_step_diag_fused")
-    else:
+        if _lib.coop_refused(rc, "cl_admm_step_diag_fused"):
+            FUSED = fused = False
+        else:
+            dev.launches += 1
+            _lib.check(rc, "cl_admm_step_diag_fused")
+    if not fused:
         rc = dev.lib.cl_admm_step_diag(ctypes.byref(a), ctypes.byref(st))
         dev.launches += 8 + 3 * (st.it_u + st.it_v)
         _lib.check(rc, f"cl_admm_step_diag (admm_native.cu:{st.err_line})")

@@ -537,12 +537,17 @@ def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory
     a.rec_cap = cap
     a.rec = rec.ctypes.data
     a.gnorms = gn.ctypes.data
+    global FUSED
     st = _lib.AlmInnerStats()
-    if FUSED and n >= 1 and n * ld <= FUSED_MAX_ELEMS:
+    fused = FUSED and n >= 1 and n * ld <= FUSED_MAX_ELEMS
+    if fused:
         rc = dev.lib.cl_alm_inner_diag_fused(ctypes.byref(a), ctypes.byref(st))
-        dev.launches += 1
-        _lib.check(rc, "cl_alm_inner_diag_fused")
-    else:
+        if _lib.coop_refused(rc, "cl_alm_inner_diag_fused"):
+            FUSED = fused = False
+        else:
+            dev.launches += 1
+            _lib.check(rc, "cl_alm_inner_diag_fused")
+    if not fused:
         rc = dev.lib.cl_alm_inner_diag(ctypes.byref(a), ctypes.byref(st))
         dev.launches += 2 + 5 * st.iterations
         _lib.check(rc, f"cl_alm_inner_diag (alm_native.cu:{st.err_line})")

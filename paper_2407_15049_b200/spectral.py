@@ -69,11 +69,16 @@ def _lanczos_native(op, n, k_max, Q, u, r, h, dev, alphas, betas):
     dalpha = dev.zeros(max(k_max, 1))
     a.dbeta, a.dalpha = dbeta.data_ptr(), dalpha.data_ptr()
     k = _lib.I32(0)
-    if FUSED and n <= FUSED_MAX_N and k_max <= 4096:
+    global FUSED
+    fused = FUSED and n <= FUSED_MAX_N and k_max <= 4096
+    if fused:
         rc = dev.lib.cl_lanczos_loop_fused(ctypes.byref(a), ctypes.byref(k))
-        dev.launches += 1
-        _lib.check(rc, "cl_lanczos_loop_fused")
-    else:
+        if _lib.coop_refused(rc, "cl_lanczos_loop_fused"):
+            FUSED = fused = False
+        else:
+            dev.launches += 1
+            _lib.check(rc, "cl_lanczos_loop_fused")
+    if not fused:
         rc = dev.lib.cl_lanczos_loop(ctypes.byref(a), ctypes.byref(k))
         dev.launches += 9 * k.value
         _lib.check(rc, "cl_lanczos_loop")

@@ -37,3 +37,16 @@ def test_no_cpu_fallback_without_device():
         pytest.skip("device present")
     with pytest.raises(_lib.CulLoradsError):
         _lib.load(require_device=True)
+
+
+def test_cooperative_launch_refusal_is_recognised():
+    """A refused cooperative launch (nothing ran) hands over to the multi-launch path with a
+    warning; a barrier timeout (CL_EARG + 1) or a fault is not treated as a refusal."""
+    import warnings
+    from paper_2407_15049_b200 import _lib
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        assert _lib.coop_refused(720, "cl_admm_step_diag_fused")
+        assert not _lib.coop_refused(0, "x") and not _lib.coop_refused(_lib.CL_EARG + 1, "x")
+        assert not _lib.coop_refused(700, "x")          # an illegal address is a fault, not a refusal
+    assert len(w) == 1 and "multi-launch" in str(w[0].message)
