@@ -19,13 +19,12 @@ import time
 from collections import deque
 from dataclasses import dataclass
 
-import numpy as np
 import torch
 
 from .alm import DualVector
-from .device import F64, padded_ld
+from .device import padded_ld
 from .exceptions import DivergedError, SpdViolationError
-from .linops import objective_dev, to_factor, to_vec
+from .linops import to_factor, to_vec
 
 
 @dataclass

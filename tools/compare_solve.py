@@ -9,7 +9,6 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("n", type=float)
