@@ -14,7 +14,9 @@ value = algorithmic HBM bytes of the step (paper_2407_15049_b200/roofline.py)
 divided by the device time per step, aggregated over ranks (GB/s). The
 ``reference`` arm times the reference algorithm's CPU implementation (the
 numpy/scipy restatement in oracle/, threaded over row blocks) on a bounded
-sample of the same synthetic family.
+sample of the same synthetic family. At N=1 the line also carries ``solver``
+(iteration rates, the G1-shaped full solve against the CPU oracle) and
+``completion`` (the matrix-completion operators at configs[3]'s one-GPU share).
 """
 
 from __future__ import annotations
