@@ -24,6 +24,9 @@
 #include <stdint.h>
 #include <string.h>
 #include <time.h>
+#ifdef AFZ_PROF
+#include <stdio.h>
+#endif
 
 #include "culorads.h"
 #include "fused_rows.cuh"
@@ -45,6 +48,9 @@ struct AOut {
     unsigned long long ctr;  // grid-barrier arrival counter (monotonic, grid_bar.cuh)
     int iterations, n_records, n_gnorms, hit_cap, status, ax_is_ax2, err;
     unsigned long long t0;   // global timer at the start
+#ifdef AFZ_PROF
+    long long cyc[6];        // block 0: direction coefs, dir pass, line search, best_step, update, bookkeeping
+#endif
 };
 __device__ AOut a_out;
 __shared__ unsigned long long s_tgt;
@@ -82,12 +88,28 @@ __device__ void a_reduce(double* v, int K, double* ws, int& region) {
         base[k * AMAXB + blockIdx.x] = s;
     }
     a_sync(gridDim.x);
-    for (int k = wid; k < K; k += AW) {   // warp w adds the partials of values w, w + AW, ...
-        double s = 0.0;
-        for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(base + k * AMAXB + b);
+    {   // warp w adds the partials of values w, w + AW, ...: all their loads in flight at once
+        constexpr int KPW = (AK + AW - 1) / AW;
+        double acc[KPW];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) tot[k] = s;
+        for (int q = 0; q < KPW; ++q) acc[q] = 0.0;
+        for (unsigned b = lane; b < gridDim.x; b += 32) {
+#pragma unroll
+            for (int q = 0; q < KPW; ++q) {
+                const int k = wid + q * AW;
+                if (k < K) acc[q] += __ldcg(base + k * AMAXB + b);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < KPW; ++q) {
+            const int k = wid + q * AW;
+            if (k < K) {     // warp-uniform
+                double t = acc[q];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                if (lane == 0) tot[k] = t;
+            }
+        }
     }
     __syncthreads();
 #pragma unroll
@@ -407,7 +429,15 @@ __global__ void __launch_bounds__(AT) alm_fused_kernel(Az z) {
         }
     }
 
+#ifdef AFZ_PROF
+    long long pc[6] = {0, 0, 0, 0, 0, 0};
+    long long tk = clock64();
+#define AFZ_T(k) do { if (writer) { const long long _t = clock64(); pc[k] += _t - tk; tk = _t; } } while (0)
+#else
+#define AFZ_T(k) do { } while (0)
+#endif
     for (int it = 0; it < a.max_iter; ++it) {
+        AFZ_T(5);
         if (t0) {
             c.gnorm = sqrt(c.gg);
             if (blockIdx.x == 0 && c.ngn < a.rec_cap) z.gnorms[c.ngn] = c.gnorm;
@@ -417,48 +447,65 @@ __global__ void __launch_bounds__(AT) alm_fused_kernel(Az z) {
             else if (a.reduce_factor >= 0.0 && c.gnorm <= a.reduce_factor * c.gnorm0) c.stop = 1;
             if (c.stop) c.hit = 0;
             if (!c.stop) {
-                // direction coefficients (alm.py:98 via the Gram matrix), as alm_native.cu
                 c.Dn = c.free_[--c.nfree];
-                c.nt = 0;
-                c.tb[c.nt] = c.g;
-                c.tc[c.nt] = -1.0;
-                ++c.nt;
-                double alphas[CL_ALM_MAXMEM];
-                for (int k = c.cnt - 1, q = 0; k >= 0; --k, ++q) {
-                    const Pair& pr = hat(c, k);
-                    double acc = 0.0;
-                    for (int j = 0; j < c.nt; ++j) acc += c.G[pr.d][c.tb[j]] * c.tc[j];
-                    const double av = pr.beta * (pr.sigma * acc);
-                    int pos = -1;
-                    for (int j = 0; j < c.nt; ++j)
-                        if (c.tb[j] == pr.y) pos = j;
-                    if (pos < 0) {
-                        c.tb[c.nt] = pr.y;
-                        c.tc[c.nt] = 0.0;
-                        pos = c.nt++;
-                    }
-                    c.tc[pos] = c.tc[pos] - av;
-                    alphas[q] = av;
-                }
-                for (int k = 0; k < c.cnt; ++k) {
-                    const Pair& pr = hat(c, k);
-                    const double av = alphas[c.cnt - 1 - k];
-                    double acc = 0.0;
-                    for (int j = 0; j < c.nt; ++j) acc += c.G[pr.y][c.tb[j]] * c.tc[j];
-                    const double bb = pr.beta * acc;
-                    int pos = -1;
-                    for (int j = 0; j < c.nt; ++j)
-                        if (c.tb[j] == pr.d) pos = j;
-                    if (pos < 0) {
-                        c.tb[c.nt] = pr.d;
-                        c.tc[c.nt] = 0.0;
-                        pos = c.nt++;
-                    }
-                    c.tc[pos] = c.tc[pos] + (av - bb) * pr.sigma;
-                }
+                c.nt = 1;
+                c.tb[0] = c.g;
+                c.tc[0] = -1.0;
             }
         }
         __syncthreads();
+        if (!c.stop && threadIdx.x < 32) {
+            // direction coefficients (alm.py:98 via the Gram matrix, as alm_native.cu), warp 0:
+            // every Gram-row dot is a warp sum, the bookkeeping is identical in all lanes
+            const int ln = threadIdx.x;
+            int nt = c.nt;
+            double alphas[CL_ALM_MAXMEM];
+            auto dotG = [&](int x) {
+                double acc = ln < nt ? c.G[x][c.tb[ln]] * c.tc[ln] : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                return acc;
+            };
+            auto slot = [&](int buf) {     // position of buffer buf among the operands, or -1
+                const unsigned hit = __ballot_sync(0xffffffffu, ln < nt && c.tb[ln] == buf);
+                return hit ? __ffs(hit) - 1 : -1;
+            };
+            for (int k = c.cnt - 1, q = 0; k >= 0; --k, ++q) {
+                const Pair pr = hat(c, k);
+                const double av = pr.beta * (pr.sigma * dotG(pr.d));
+                int pos = slot(pr.y);
+                __syncwarp();
+                if (pos < 0) {
+                    if (ln == 0) {
+                        c.tb[nt] = pr.y;
+                        c.tc[nt] = 0.0;
+                    }
+                    pos = nt++;
+                }
+                if (ln == 0) c.tc[pos] = c.tc[pos] - av;
+                __syncwarp();
+                alphas[q] = av;
+            }
+            for (int k = 0; k < c.cnt; ++k) {
+                const Pair pr = hat(c, k);
+                const double av = alphas[c.cnt - 1 - k];
+                const double bb = pr.beta * dotG(pr.y);
+                int pos = slot(pr.d);
+                __syncwarp();
+                if (pos < 0) {
+                    if (ln == 0) {
+                        c.tb[nt] = pr.d;
+                        c.tc[nt] = 0.0;
+                    }
+                    pos = nt++;
+                }
+                if (ln == 0) c.tc[pos] = c.tc[pos] + (av - bb) * pr.sigma;
+                __syncwarp();
+            }
+            if (ln == 0) c.nt = nt;
+        }
+        __syncthreads();
+        AFZ_T(0);
         if (c.stop) break;
 
         // ---- direction D = sum tc_k B[tb_k] and its Gram row ----
@@ -484,6 +531,7 @@ __global__ void __launch_bounds__(AT) alm_fused_kernel(Az z) {
                 v[nt] += dot2(o, o);
             }
         a_reduce(v, nt + 1, ws, region);
+        AFZ_T(1);
         if (t0) {
             for (int k = 0; k < nt; ++k) gset(c, c.Dn, c.tb[k], v[k]);
             gset(c, c.Dn, c.Dn, v[nt]);
@@ -528,6 +576,7 @@ __global__ void __launch_bounds__(AT) alm_fused_kernel(Az z) {
             }
         }
         a_reduce(v, 8, ws, region);
+        AFZ_T(2);
         if (t0) {
             const double p1 = a.scale * (v[0] + v[2]);
             const double p2 = a.scale * v[1];
@@ -549,6 +598,7 @@ __global__ void __launch_bounds__(AT) alm_fused_kernel(Az z) {
             }
         }
         __syncthreads();
+        AFZ_T(3);
         if (c.stop) break;
 
         // ---- step + gradient + Gram rows (AlmCore.grad_value) ----
@@ -568,6 +618,7 @@ __global__ void __launch_bounds__(AT) alm_fused_kernel(Az z) {
         for (int k = 0; k < AK; ++k) v[k] = 0.0;
         update_pass(z, c, refresh, ax_cur, ax_out, D, a.bufs[c.g], v);
         a_reduce(v, 7 + 2 * c.nh, ws, region);
+        AFZ_T(4);
         if (t0) {
             if (!refresh) c.ax_alt_cur ^= 1;
             c.L = a.scale * v[0] + v[3] + 0.5 * a.rho * v[4];
@@ -630,6 +681,10 @@ __global__ void __launch_bounds__(AT) alm_fused_kernel(Az z) {
         __syncthreads();
         if (c.stop) break;
     }
+#ifdef AFZ_PROF
+    if (writer)
+        for (int k = 0; k < 6; ++k) a_out.cyc[k] = pc[k];
+#endif
     if (writer) {
         a_out.iterations = c.iterations;
         a_out.n_records = c.nrec;
@@ -715,6 +770,12 @@ extern "C" int cl_alm_inner_diag_fused(const cl_alm_inner_args* a, cl_alm_inner_
     if (e != cudaSuccess) return (int)e;
     for (int k = 0; k < nrec; ++k)     // device timer -> host clock (the launch time is the common origin)
         a->rec[4 * k + 3] = h0 + 1e-9 * (a->rec[4 * k + 3] - (double)o.t0);
+#ifdef AFZ_PROF
+    fprintf(stderr, "alm_fused cycles/iter: coefs %.0f dir %.0f ls %.0f best %.0f upd %.0f book %.0f (iters %d)\n",
+            (double)o.cyc[0] / o.iterations, (double)o.cyc[1] / o.iterations, (double)o.cyc[2] / o.iterations,
+            (double)o.cyc[3] / o.iterations, (double)o.cyc[4] / o.iterations, (double)o.cyc[5] / o.iterations,
+            o.iterations);
+#endif
     out->iterations = o.iterations;
     out->n_records = o.n_records;
     out->n_gnorms = o.n_gnorms;
