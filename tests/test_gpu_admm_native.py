@@ -103,3 +103,24 @@ def test_fused_solve_trace_close_to_native():
     fused = driver.solve(p, cfg)
     assert fused.status == ref.status
     assert abs(fused.objective - ref.objective) <= 1e-9 * abs(ref.objective)
+
+
+def test_small_solve_runs_the_one_launch_paths():
+    """The G1-shaped solve takes the one-launch paths: about one launch per ADMM step and per
+    ALM inner solve (the multi-launch loops need about ten per step), and the same solve
+    with them disabled launches several times more kernels."""
+    from paper_2407_15049_b200 import admm, alm, driver, spectral
+    from tests._golden import cfg_of, load, problem_from
+    z = load("solve_g1_like.npz")
+    p = problem_from(z)
+    cfg = driver.SolverConfig(**cfg_of(z))
+    fused = driver.solve(p, cfg)
+    admm.FUSED = alm.FUSED = spectral.FUSED = False
+    try:
+        multi = driver.solve(p, cfg)
+    finally:
+        admm.FUSED = alm.FUSED = spectral.FUSED = True
+    steps = fused.admm_steps
+    assert fused.gpu_launches < 3 * steps + 1000
+    assert multi.gpu_launches > 3 * fused.gpu_launches
+    assert fused.status == multi.status
