@@ -343,9 +343,25 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
     dev = ops.dev
     p = ops.problem
     n, ld = state.U.shape
-    a = _lib.AdmmDiagArgs()
-    a.n, a.ld = n, ld
-    a.aval, a.b, a.lam = ops.diag_aval.data_ptr(), ops.b.data_ptr(), state.dual.lam.data_ptr()
+    if getattr(hs, "r_v", None) is None:
+        hs.r_v = dev.empty(n, ld)
+    a = getattr(hs, "native_args", None)
+    if a is None:
+        # the fields that stay fixed over the steps of one HalfStep, set once (host time per
+        # step matters at small n, where a step costs tens of microseconds)
+        a = hs.native_args = _lib.AdmmDiagArgs()
+        a.n, a.ld = n, ld
+        a.aval, a.b = ops.diag_aval.data_ptr(), ops.b.data_ptr()
+        a.r, a.r_v, a.p, a.Q = hs.r.data_ptr(), hs.r_v.data_ptr(), hs.p.data_ptr(), hs.Q.data_ptr()
+        a.cu = hs.cu_buffer().data_ptr()
+        a.nlam, a.res = hs.nlam.data_ptr(), hs.y.data_ptr()
+        a.cpat = ops.c_mat.cpat.struct(c_coeff=1.0)
+        a.binf = float(p.b_norminf)
+        a.slab = dev.slot(470).value
+        a.host = dev.host.data_ptr() + 8 * 470
+        a.ws = dev.ws.data_ptr()
+        a.stream = dev.stream.cuda_stream
+    a.lam = state.dual.lam.data_ptr()
     lam_new = hs.lam_spare if getattr(hs, "lam_spare", None) is not None else dev.empty(p.m)
     a.lam_new = lam_new.data_ptr()
     if state.ax is None:
@@ -359,20 +375,9 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
     a.ax = ax.data_ptr()
     U_new = pool.get() if pool else dev.empty(n, ld)
     V_new = pool.get() if pool else dev.empty(n, ld)
-    if getattr(hs, "r_v", None) is None:
-        hs.r_v = dev.empty(n, ld)
     a.U, a.V, a.U_new, a.V_new = state.U.data_ptr(), state.V.data_ptr(), U_new.data_ptr(), V_new.data_ptr()
-    a.r, a.r_v, a.p, a.Q = hs.r.data_ptr(), hs.r_v.data_ptr(), hs.p.data_ptr(), hs.Q.data_ptr()
-    a.cu = hs.cu_buffer().data_ptr()
-    nlam = hs.nlam
-    a.nlam, a.res = nlam.data_ptr(), hs.y.data_ptr()
-    a.cpat = ops.c_mat.cpat.struct(c_coeff=1.0)
-    a.rho, a.scale, a.binf = float(state.dual.rho), float(scale), float(p.b_norminf)
+    a.rho, a.scale = float(state.dual.rho), float(scale)
     a.rel_floor, a.primal_coeff, a.cg_cap = float(cg_rel_floor), float(cg_primal_coeff), int(cg_cap)
-    a.slab = dev.slot(470).value
-    a.host = dev.host.data_ptr() + 8 * 470
-    a.ws = dev.ws.data_ptr()
-    a.stream = dev.stream.cuda_stream
     global FUSED
     st = _lib.AdmmStepStats()
     fused = FUSED and n >= 1 and n * lanes_for(ld) <= FUSED_MAX_LANES
