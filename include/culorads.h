@@ -298,9 +298,10 @@ typedef struct {
     double rho, scale, binf, rel_floor, primal_coeff;
     int32_t cg_cap;
     double* slab;              /* 16 device doubles for the step's reductions */
-    double* host;              /* 16 pinned host doubles */
+    double* host;              /* 20 pinned host doubles */
     double* ws;                /* reduction workspace (CL_WS_ALLOC doubles) */
     void* stream;
+    int32_t want_balance;      /* one-launch step: also return ||U_new-U||^2, ||V_new-V||^2 */
 } cl_admm_diag_args;
 
 typedef struct {
@@ -317,6 +318,7 @@ typedef struct {
     double objective;          /* <C, U V^T> of the new factors (admm.py:215) */
     double lam_b;              /* lam_new . b */
     int32_t err_line;          /* diagnostics: admm_native.cu line of the first failing launch */
+    double du2, dv2;           /* ||U_new-U||^2, ||V_new-V||^2 when asked (want_balance), else -1 */
 } cl_admm_step_stats;
 
 int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats* out);
@@ -422,7 +424,7 @@ int cl_lanczos_loop_fused(const cl_lanczos_args* a, int32_t* k_out);
 /* cl_admm_step_diag as ONE cooperative launch (csrc/admm_fused.cu) for small
  * problems, where launch and round-trip latency bound the step: every phase runs
  * in one kernel between grid-wide barriers and the scalar decisions are taken on
- * the device; one synchronize per step. Same args and stats (host: 16 pinned
+ * the device; one synchronize per step. Same args and stats (host: 20 pinned
  * doubles); iterates equal cl_admm_step_diag's to rounding (global sums are added
  * in another fixed order). Requires n >= 1 and a C pattern with cv values only. */
 int cl_admm_step_diag_fused(const cl_admm_diag_args* a, cl_admm_step_stats* out);

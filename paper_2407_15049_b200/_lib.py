@@ -86,14 +86,15 @@ class AdmmDiagArgs(ctypes.Structure):
                 ("pnorm2_known", D), ("U", P), ("V", P), ("U_new", P), ("V_new", P),
                 ("r", P), ("r_v", P), ("p", P), ("Q", P), ("cu", P), ("nlam", P), ("res", P),
                 ("cpat", Pattern), ("rho", D), ("scale", D), ("binf", D), ("rel_floor", D),
-                ("primal_coeff", D), ("cg_cap", I32), ("slab", P), ("host", P), ("ws", P), ("stream", P)]
+                ("primal_coeff", D), ("cg_cap", I32), ("slab", P), ("host", P), ("ws", P), ("stream", P),
+                ("want_balance", I32)]
 
 
 class AdmmStepStats(ctypes.Structure):
     _fields_ = [("it_u", I32), ("it_v", I32), ("res_u", D), ("res_v", D), ("eps_u", D), ("eps_v", D),
                 ("pnorm2", D), ("hit_cap", I32), ("status", I32), ("bad_half", I32), ("bad_is_new", I32),
                 ("pq_bad", D), ("u_reused", I32), ("v_reused", I32), ("objective", D), ("lam_b", D),
-                ("err_line", I32)]
+                ("err_line", I32), ("du2", D), ("dv2", D)]
 
 
 CL_ALM_MAXMEM = 8

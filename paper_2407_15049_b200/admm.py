@@ -377,6 +377,7 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
     V_new = pool.get() if pool else dev.empty(n, ld)
     a.U, a.V, a.U_new, a.V_new = state.U.data_ptr(), state.V.data_ptr(), U_new.data_ptr(), V_new.data_ptr()
     a.rho, a.scale = float(state.dual.rho), float(scale)
+    a.want_balance = 1 if getattr(state, "want_balance", False) else 0
     a.rel_floor, a.primal_coeff, a.cg_cap = float(cg_rel_floor), float(cg_primal_coeff), int(cg_cap)
     global FUSED
     st = _lib.AdmmStepStats()
@@ -419,6 +420,7 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
     state.dual.lam = lam_new
     hs.lam_spare = old
     state.step_obj = (st.objective, st.lam_b)
+    state.step_bal = (st.du2, st.dv2) if st.du2 >= 0.0 else None
     return StepStats(st.it_u, st.it_v, st.res_u, st.res_v, bool(st.hit_cap))
 
 
@@ -650,6 +652,8 @@ def admm_run(state: AdmmState, ops, *, scale=1.0, eps=1e-5, gap_eps=None, min_st
             break
         U_prev, V_prev = state.U, state.V
         state.step_obj = None
+        state.step_bal = None
+        state.want_balance = step % rho_balance_every == 0
         stats = admm_step(state, ops, scale=scale, cg_cap=cg_cap, hs=hs, pool=pool)
         cg_total += stats.cg_iters_u + stats.cg_iters_v
         steps = step
@@ -668,7 +672,8 @@ def admm_run(state: AdmmState, ops, *, scale=1.0, eps=1e-5, gap_eps=None, min_st
                             state.dual.rho, state.r)
         done = p0 <= eps and (gap_eps is None or g3 < gap_eps) and step >= min_steps
         balance = (not done) and step % rho_balance_every == 0
-        if balance:
+        bal = state.step_bal                   # measured inside the one-launch step
+        if balance and bal is None:
             dev.lincomb(None, [state.U, U_prev], [1.0, -1.0], dots=[("out", "out")], at=445)
             dev.lincomb(None, [state.V, V_prev], [1.0, -1.0], dots=[("out", "out")], at=446)
         if U_prev is not state.U:
@@ -685,8 +690,10 @@ def admm_run(state: AdmmState, ops, *, scale=1.0, eps=1e-5, gap_eps=None, min_st
         else:
             gap_hist.clear()
         if balance:
-            s = dev.fetch(447)
-            dual_surrogate = state.dual.rho * (math.sqrt(float(s[445])) + math.sqrt(float(s[446])))
+            if bal is None:
+                s = dev.fetch(447)
+                bal = (float(s[445]), float(s[446]))
+            dual_surrogate = state.dual.rho * (math.sqrt(bal[0]) + math.sqrt(bal[1]))
             if pnorm > rho_balance_mu * dual_surrogate:
                 state.dual.rho = min(state.dual.rho * rho_balance_tau, rho_max)
             elif dual_surrogate > rho_balance_mu * pnorm:

@@ -387,6 +387,27 @@ __global__ void __launch_bounds__(FT) admm_step_fused_kernel(Fz f) {
     st.objective = e[0];
     st.pnorm2 = e[1];
     st.lam_b = e[2];
+    st.du2 = st.dv2 = -1.0;
+    if (a.want_balance) {   // admm_run's residual balancing (admm.py:184): ||U_new - U||^2, ||V_new - V||^2
+        double d[2] = {0.0, 0.0};
+        for (int64_t i = L.first; i < a.n; i += L.stride)
+            for (int u = L.gl; u < h2; u += G) {
+                const int64_t off = 2 * (i * h2 + u);
+                if (!u_kept) {
+                    const double2 x = ldcg2(a.U_new + off), y = ldcg2(a.U + off);
+                    const double2 df = make_double2(x.x - y.x, x.y - y.y);
+                    d[0] += dot2(df, df);
+                }
+                if (!v_kept) {
+                    const double2 x = ldcg2(a.V_new + off), y = ldcg2(a.V + off);
+                    const double2 df = make_double2(x.x - y.x, x.y - y.y);
+                    d[1] += dot2(df, df);
+                }
+            }
+        greduce<2>(d, ws, region);
+        st.du2 = d[0];
+        st.dv2 = d[1];
+    }
     st.hit_cap = (st.it_u >= a.cg_cap && st.res_u > st.eps_u) || (st.it_v >= a.cg_cap && st.res_v > st.eps_v);
     if (writer) g_out.st = st;
 }
@@ -402,7 +423,7 @@ extern "C" int cl_admm_step_diag_fused(const cl_admm_diag_args* a, cl_admm_step_
         a->cpat.indptr == nullptr || a->cpat.at_ptr != nullptr ||
         a->cpat.ghost != nullptr)
         return CL_EARG;
-    static_assert(sizeof(FzOut) <= 16 * sizeof(double), "the step's output fits the 16 host doubles");
+    static_assert(sizeof(FzOut) <= 20 * sizeof(double), "the step's output fits the 20 host doubles");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(a->stream);
     if (g_max_blocks == 0) {
         int nb = 0, dev = 0;

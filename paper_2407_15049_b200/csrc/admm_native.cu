@@ -195,6 +195,7 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
     c.line = 0;
     c.N = a->n * (int64_t)a->ld;
     memset(out, 0, sizeof(*out));
+    out->du2 = out->dv2 = -1.0;   // the balance measures come from the one-launch step only
 #define RET_RC()                \
     do {                        \
         out->err_line = c.line; \

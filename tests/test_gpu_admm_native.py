@@ -124,3 +124,37 @@ def test_small_solve_runs_the_one_launch_paths():
     assert fused.gpu_launches < 3 * steps + 1000
     assert multi.gpu_launches > 3 * fused.gpu_launches
     assert fused.status == multi.status
+
+
+def test_fused_step_returns_balance_measures():
+    """With want_balance the one-launch step returns ||U_new - U||^2 and ||V_new - V||^2
+    (admm_run's residual balancing reads them instead of two more passes and a round trip)."""
+    import torch
+    from paper_2407_15049_b200 import admm, alm, graphs, linops, problem
+    from paper_2407_15049_b200.device import padded_ld
+    p = problem.build_maxcut(graphs.random_sparse(800, deg=20.0, seed=2))
+    ops = linops.build_operators(p)
+    dev = ops.dev
+    r = 9
+    ld = padded_ld(r)
+    rng = np.random.default_rng(3)
+    R = linops.to_factor(rng.standard_normal((p.n, r)) / np.sqrt(p.n * r), dev, ld)
+    dual = alm.DualVector(lam=linops.to_vec(0.3 * rng.standard_normal(p.m), dev).clone(), rho=2.0)
+    st = admm.AdmmState(U=R.clone(), V=(R + 1e-3).contiguous(), dual=dual, r=r)
+    hs, pool = admm.HalfStep(ops, p.n, ld), admm._Pool(dev, p.n, ld)
+    seen = 0
+    for _ in range(6):
+        U0, V0 = st.U.clone(), st.V.clone()
+        st.want_balance = True
+        admm.admm_step(st, ops, scale=0.7, hs=hs, pool=pool, cg_cap=50)
+        assert st.step_bal is not None
+        torch.cuda.synchronize()
+        du2 = float(((st.U - U0) ** 2).sum())
+        dv2 = float(((st.V - V0) ** 2).sum())
+        assert abs(st.step_bal[0] - du2) <= 1e-12 * max(du2, 1e-300) + 1e-300
+        assert abs(st.step_bal[1] - dv2) <= 1e-12 * max(dv2, 1e-300) + 1e-300
+        seen += (du2 > 0) + (dv2 > 0)
+    assert seen > 0
+    st.want_balance = False
+    admm.admm_step(st, ops, scale=0.7, hs=hs, pool=pool, cg_cap=50)
+    assert st.step_bal is None
