@@ -24,6 +24,12 @@
  * then one block folds the partials in a fixed order. `ws` is a device
  * scratch of CL_WS_ALLOC doubles, zero-initialised once, private to the calling
  * stream (its last word is the completion counter, left at 0 after every call).
+ *
+ * The one-launch (cooperative) entry points (*_fused) keep their grid-barrier
+ * counter and output slot in a per-device symbol and their host-side state per
+ * device (csrc/fused_state.cuh); each call holds a per-family lock for its whole
+ * duration (launch + synchronize), so concurrent callers on any devices/streams
+ * are serialised, never interleaved on one counter.
  */
 #ifndef CULORADS_H
 #define CULORADS_H

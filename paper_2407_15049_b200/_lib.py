@@ -38,6 +38,21 @@ def coop_refused(rc, what):
                   RuntimeWarning, stacklevel=3)
     return True
 
+
+CL_EBARRIER = CL_EARG + 1    # a one-launch kernel's grid barrier timed out (its state was reset)
+
+
+def barrier_timeout(rc, what):
+    """True (with a warning) when a one-launch kernel's grid barrier gave up (about 1 s of
+    waiting: GPU time-slicing, MPS or a debugger). Its outputs are void; the caller reruns
+    the work on the multi-launch path from the inputs it kept."""
+    if rc != CL_EBARRIER:
+        return False
+    import warnings
+    warnings.warn(f"{what}: grid barrier timed out; rerunning on the multi-launch path",
+                  RuntimeWarning, stacklevel=3)
+    return True
+
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint_eval_halo",
            "cl_diag_constraint_eval", "cl_sddmm",
            "cl_gather_rows", "cl_diag_cg_apply", "cl_diag_cg_apply_rows", "cl_diag_cg_step", "cl_cg_step", "cl_cg_step_dev", "cl_admm_step_diag", "cl_admm_step_diag_fused", "cl_alm_inner_diag", "cl_alm_inner_diag_fused",

@@ -386,6 +386,13 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
         rc = dev.lib.cl_admm_step_diag_fused(ctypes.byref(a), ctypes.byref(st))
         if _lib.coop_refused(rc, "cl_admm_step_diag_fused"):
             FUSED = fused = False
+        elif _lib.barrier_timeout(rc, "cl_admm_step_diag_fused"):
+            # the step is void: U, V and lam were only read; ax may be overwritten
+            FUSED = fused = False
+            st = _lib.AdmmStepStats()
+            if state.ax is not None:
+                a.ax_valid = 0
+                a.pnorm2_known = -1.0
         else:
             dev.launches += 1
             _lib.check(rc, "cl_admm_step_diag_fused")

@@ -541,9 +541,14 @@ def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory
     st = _lib.AlmInnerStats()
     fused = FUSED and n >= 1 and n * ld <= FUSED_MAX_ELEMS
     if fused:
+        R_keep = R.clone()          # the one launch steps R in place; kept for a void launch
         rc = dev.lib.cl_alm_inner_diag_fused(ctypes.byref(a), ctypes.byref(st))
         if _lib.coop_refused(rc, "cl_alm_inner_diag_fused"):
             FUSED = fused = False
+        elif _lib.barrier_timeout(rc, "cl_alm_inner_diag_fused"):
+            FUSED = fused = False
+            R.copy_(R_keep)
+            st = _lib.AlmInnerStats()
         else:
             dev.launches += 1
             _lib.check(rc, "cl_alm_inner_diag_fused")

@@ -28,6 +28,7 @@
 
 #include "culorads.h"
 #include "fused_rows.cuh"
+#include "fused_state.cuh"
 #include "grid_bar.cuh"
 
 namespace {
@@ -412,8 +413,7 @@ __global__ void __launch_bounds__(FT) admm_step_fused_kernel(Fz f) {
     if (writer) g_out.st = st;
 }
 
-int g_max_blocks = 0;
-unsigned long long g_bar_base = 0;
+FusedState g_state;
 
 }  // namespace
 
@@ -425,27 +425,30 @@ extern "C" int cl_admm_step_diag_fused(const cl_admm_diag_args* a, cl_admm_step_
         return CL_EARG;
     static_assert(sizeof(FzOut) <= 20 * sizeof(double), "the step's output fits the 20 host doubles");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(a->stream);
-    if (g_max_blocks == 0) {
-        int nb = 0, dev = 0;
-        cudaError_t e = cudaGetDevice(&dev);
-        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, admm_step_fused_kernel, FT, 0);
-        int nsm = 0;
+    std::lock_guard<std::mutex> lock(g_state.mu);
+    int dev = 0;
+    FusedDevState* S = g_state.current(&dev);
+    if (S == nullptr) return CL_EARG;
+    if (S->max_blocks == 0) {
+        int nb = 0, nsm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, admm_step_fused_kernel, FT, 0);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         if (e != cudaSuccess) return (int)e;
-        g_max_blocks = nb * nsm;
-        if (g_max_blocks > FMAXB) g_max_blocks = FMAXB;
-        if (g_max_blocks < 1) return CL_EARG;
+        int mb = nb * nsm;
+        if (mb > FMAXB) mb = FMAXB;
+        if (mb < 1) return CL_EARG;
+        S->max_blocks = mb;
     }
     Fz f;
     f.a = *a;
     f.h2 = a->ld / 2;
     f.G = lanes_for(f.h2);
     f.rel = 0.0;
-    f.bar_base = g_bar_base;
+    f.bar_base = S->bar_base;
     // FZ_ROWS rows per lane group: latency (gather chains) against barrier cost (blocks)
     const int64_t rows_per_block = FZ_ROWS * (int64_t)(FT / f.G);
     int64_t nb = (a->n + rows_per_block - 1) / rows_per_block;
-    if (nb > g_max_blocks) nb = g_max_blocks;
+    if (nb > S->max_blocks) nb = S->max_blocks;
     if (nb < 1) nb = 1;
     void* args[] = {&f};
     cudaError_t e =
@@ -457,12 +460,13 @@ extern "C" int cl_admm_step_diag_fused(const cl_admm_diag_args* a, cl_admm_step_
     memcpy(&o, a->host, sizeof(FzOut));
     *out = o.st;
     out->err_line = 0;
-    g_bar_base = o.ctr;
+    S->bar_base = o.ctr;
     if (o.err) {   // a barrier gave up: reset its state, report the step as failed
         FzOut z;
         memset(&z, 0, sizeof(z));
-        cudaMemcpyToSymbol(g_out, &z, sizeof(z));
-        g_bar_base = 0;
+        cudaMemcpyToSymbolAsync(g_out, &z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+        cudaStreamSynchronize(st);
+        S->bar_base = 0;
         return CL_EARG + 1;
     }
     return CL_OK;

@@ -30,6 +30,7 @@
 
 #include "culorads.h"
 #include "fused_rows.cuh"
+#include "fused_state.cuh"
 #include "grid_bar.cuh"
 
 namespace {
@@ -695,10 +696,7 @@ __global__ void __launch_bounds__(AT) alm_fused_kernel(Az z) {
     }
 }
 
-double* g_scratch = nullptr;
-int64_t g_scratch_cap = 0;
-int g_max_blocks = 0;
-unsigned long long g_bar_base = 0;
+FusedState g_state;
 
 double host_now() {
     timespec ts;
@@ -716,35 +714,39 @@ extern "C" int cl_alm_inner_diag_fused(const cl_alm_inner_args* a, cl_alm_inner_
         return CL_EARG;
     memset(out, 0, sizeof(*out));
     cudaStream_t st = reinterpret_cast<cudaStream_t>(a->stream);
-    if (g_max_blocks == 0) {
-        int nb = 0, dev = 0, nsm = 0;
-        cudaError_t e = cudaGetDevice(&dev);
-        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, alm_fused_kernel, AT, 0);
+    std::lock_guard<std::mutex> lock(g_state.mu);
+    int dev = 0;
+    FusedDevState* S = g_state.current(&dev);
+    if (S == nullptr) return CL_EARG;
+    if (S->max_blocks == 0) {
+        int nb = 0, nsm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, alm_fused_kernel, AT, 0);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         if (e != cudaSuccess) return (int)e;
-        g_max_blocks = nb * nsm;
-        if (g_max_blocks > AMAXB) g_max_blocks = AMAXB;
-        if (g_max_blocks < 1) return CL_EARG;
+        int mb = nb * nsm;
+        if (mb > AMAXB) mb = AMAXB;
+        if (mb < 1) return CL_EARG;
+        S->max_blocks = mb;
     }
     const int64_t need = 5 * (int64_t)(a->rec_cap > 0 ? a->rec_cap : 1);
-    if (need > g_scratch_cap) {   // stream-ordered: no device-wide synchronize
-        if (g_scratch) cudaFreeAsync(g_scratch, st);
-        g_scratch = nullptr;
-        g_scratch_cap = 0;
+    if (need > S->scratch_cap) {   // this device's trace scratch; stream-ordered, no device-wide synchronize
+        if (S->scratch) cudaFreeAsync(S->scratch, st);
+        S->scratch = nullptr;
+        S->scratch_cap = 0;
         const int64_t cap = need < 4096 ? 4096 : need;
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&g_scratch), sizeof(double) * (size_t)cap, st);
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&S->scratch), sizeof(double) * (size_t)cap, st);
         if (e != cudaSuccess) return (int)e;
-        g_scratch_cap = cap;
+        S->scratch_cap = cap;
     }
     Az z;
     z.a = *a;
     z.h2 = a->ld / 2;
     z.G = lanes_for(z.h2);
-    z.rec = g_scratch;
-    z.bar_base = g_bar_base;
-    z.gnorms = g_scratch + 4 * (int64_t)(a->rec_cap > 0 ? a->rec_cap : 1);
+    z.rec = S->scratch;
+    z.bar_base = S->bar_base;
+    z.gnorms = S->scratch + 4 * (int64_t)(a->rec_cap > 0 ? a->rec_cap : 1);
     int64_t nb = (a->n * z.G + AT - 1) / AT;   // one row per lane group
-    if (nb > g_max_blocks) nb = g_max_blocks;
+    if (nb > S->max_blocks) nb = S->max_blocks;
     if (nb < 1) nb = 1;
     const double h0 = host_now();
     void* args[] = {&z};
@@ -754,12 +756,13 @@ extern "C" int cl_alm_inner_diag_fused(const cl_alm_inner_args* a, cl_alm_inner_
     if (e != cudaSuccess) return (int)e;
     AOut o;
     memcpy(&o, a->host, sizeof(o));
-    g_bar_base = o.ctr;
+    S->bar_base = o.ctr;
     if (o.err) {
         AOut zz;
         memset(&zz, 0, sizeof(zz));
-        cudaMemcpyToSymbol(a_out, &zz, sizeof(zz));
-        g_bar_base = 0;
+        cudaMemcpyToSymbolAsync(a_out, &zz, sizeof(zz), 0, cudaMemcpyHostToDevice, st);
+        cudaStreamSynchronize(st);
+        S->bar_base = 0;
         return CL_EARG + 1;
     }
     const int nrec = o.n_records < a->rec_cap ? o.n_records : a->rec_cap;

@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include "culorads.h"
+#include "fused_state.cuh"
 #include "grid_bar.cuh"
 
 namespace {
@@ -276,8 +277,7 @@ __global__ void __launch_bounds__(LT) lanczos_fused_kernel(Lz z) {
     if (blockIdx.x == 0 && threadIdx.x == 0) lz_out.k = k;
 }
 
-int lz_max_blocks = 0;
-unsigned long long lz_bar_base = 0;
+FusedState lz_state;
 
 }  // namespace
 
@@ -289,27 +289,30 @@ extern "C" int cl_lanczos_loop_fused(const cl_lanczos_args* a, int32_t* k_out) {
     const size_t smem = sizeof(double) * (size_t)a->k_max;
     if (smem > 32 * 1024) return CL_EARG;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(a->stream);
-    if (lz_max_blocks == 0) {
-        int nb = 0, dev = 0, nsm = 0;
-        cudaError_t e = cudaGetDevice(&dev);
-        if (e == cudaSuccess)
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lanczos_fused_kernel, LT, 32 * 1024);
+    std::lock_guard<std::mutex> lock(lz_state.mu);
+    int dev = 0;
+    FusedDevState* S = lz_state.current(&dev);
+    if (S == nullptr) return CL_EARG;
+    if (S->max_blocks == 0) {
+        int nb = 0, nsm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lanczos_fused_kernel, LT, 32 * 1024);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         if (e != cudaSuccess) return (int)e;
-        lz_max_blocks = nb * nsm;
-        if (lz_max_blocks > CL_RED_BLOCKS) lz_max_blocks = CL_RED_BLOCKS;
-        if (lz_max_blocks < 1) return CL_EARG;
+        int mb = nb * nsm;
+        if (mb > CL_RED_BLOCKS) mb = CL_RED_BLOCKS;
+        if (mb < 1) return CL_EARG;
+        S->max_blocks = mb;
     }
     Lz z;
     z.n = a->n; z.k_max = a->k_max; z.breakdown = a->breakdown; z.Q = a->Q; z.ldq = a->ldq;
     z.u = a->u; z.r = a->r; z.h = a->h;
     z.indptr = a->S.indptr; z.indices = a->S.indices; z.vals = a->S.cv;
     z.alpha = a->dalpha; z.beta = a->dbeta; z.ws = a->ws;
-    z.bar_base = lz_bar_base;
+    z.bar_base = S->bar_base;
     // one row per thread, and at least 128 warps for the projections
     int64_t nb = (a->n + LT - 1) / LT;
     if (nb < 16) nb = 16;
-    if (nb > lz_max_blocks) nb = lz_max_blocks;
+    if (nb > S->max_blocks) nb = S->max_blocks;
     void* args[] = {&z};
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)lanczos_fused_kernel, dim3((unsigned)nb), dim3(LT), args,
                                                 smem, st);
@@ -318,12 +321,13 @@ extern "C" int cl_lanczos_loop_fused(const cl_lanczos_args* a, int32_t* k_out) {
     if (e != cudaSuccess) return (int)e;
     LzOut o;
     memcpy(&o, a->host, sizeof(o));
-    lz_bar_base = o.ctr;
+    S->bar_base = o.ctr;
     if (o.err) {
         LzOut zz;
         memset(&zz, 0, sizeof(zz));
-        cudaMemcpyToSymbol(lz_out, &zz, sizeof(zz));
-        lz_bar_base = 0;
+        cudaMemcpyToSymbolAsync(lz_out, &zz, sizeof(zz), 0, cudaMemcpyHostToDevice, st);
+        cudaStreamSynchronize(st);
+        S->bar_base = 0;
         return CL_EARG + 1;
     }
     const int k = o.k;

@@ -418,12 +418,23 @@ def solve_sharded(p, cfg=None, *, group=None, dev=None):
     1-GPU solve does); the report's U/V/lam are then this rank's block in that labelling
     and ``report.perm`` maps it back (row k is the caller's row perm[k])."""
     from . import driver
-    from .device import default_device
+    from .device import Device
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    dev = dev or default_device()
+    # a dedicated device context (never the process-wide default one): its scalar fetches
+    # all-reduce over the group and its solve skips the 1-GPU-only native loops; a caller's
+    # context gets its own world/group back on exit
+    dev = dev or Device()
+    saved = (dev.world, dev.group)
     dev.world, dev.group = world, group
+    try:
+        return _solve_sharded(p, cfg, group, dev, world, rank, driver)
+    finally:
+        dev.world, dev.group = saved
+
+
+def _solve_sharded(p, cfg, group, dev, world, rank, driver):
     cfg = cfg or driver.SolverConfig()
     solve_p, perm = p, None
     if cfg.reorder:

@@ -75,6 +75,8 @@ def _lanczos_native(op, n, k_max, Q, u, r, h, dev, alphas, betas):
         rc = dev.lib.cl_lanczos_loop_fused(ctypes.byref(a), ctypes.byref(k))
         if _lib.coop_refused(rc, "cl_lanczos_loop_fused"):
             FUSED = fused = False
+        elif _lib.barrier_timeout(rc, "cl_lanczos_loop_fused"):
+            FUSED = fused = False       # Q[0] (the start vector) was only read: rerun
         else:
             dev.launches += 1
             _lib.check(rc, "cl_lanczos_loop_fused")
