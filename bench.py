@@ -54,6 +54,10 @@ def parse():
     ap.add_argument("--no-completion", action="store_true",
                     help="skip the matrix-completion operator rates (configs[3] at one GPU's share)")
     ap.add_argument("--n-g1", type=int, default=800)
+    ap.add_argument("--no-solve", action="store_true",
+                    help="skip the full solves of configs[1] and configs[2] (metric's solve-seconds clause)")
+    ap.add_argument("--solve-limit", type=float, default=60.0,
+                    help="time limit (s) of each full solve; 60 s is the north_star target at n=1e7")
     ap.add_argument("--graph", choices=("random", "delaunay"), default="random",
                     help="random: BASELINE configs[2] (default); delaunay: mesh-like graph of degree 6")
     ap.add_argument("--reorder", action="store_true", help="relabel rows by the solver's RCM locality order")
@@ -193,7 +197,7 @@ def cpu_measure(n, deg, seed, budget_s, warmup=1, max_steps=None):
                 bytes=nbytes, n=n)
 
 
-def solver_rates(ops, dev, R, n, r, ld, n_g1):
+def solver_rates(ops, dev, R, n, r, ld, n_g1, peak):
     """Solver-level numbers beside the operator bench (north_star: solve time and
     iterations/s): ALM inner iterations and ADMM steps on the bench instance, and a
     full solve of the G1-shaped instance (BASELINE configs[0]) on the device and,
@@ -201,6 +205,7 @@ def solver_rates(ops, dev, R, n, r, ld, n_g1):
     import torch
 
     from paper_2407_15049_b200 import admm, alm, driver, graphs, problem
+    from paper_2407_15049_b200 import roofline as RL
 
     out = {}
     rho = max(1.0, ops.problem.m / math.sqrt(max(ops.problem.nnz_a_full(), 1)))
@@ -216,6 +221,13 @@ def solver_rates(ops, dev, R, n, r, ld, n_g1):
     dt = time.perf_counter() - t
     out["alm_inner_ms_per_iter"] = 1e3 * dt / max(res.iterations, 1)
     out["alm_inner_iters_per_s"] = max(res.iterations, 1) / dt
+    p_ = ops.problem
+    nnz_c = int(ops.c_mat.cpat.indices.numel())
+    # bytes of the timed iterations: the history fills one pair per iteration up to 8
+    ab = sum(RL.alm_iteration_bytes(n, p_.m, nnz_c, ld, min(k, 8)) for k in range(res.iterations))
+    out["alm_iteration_GBps"] = ab / dt / 1e9
+    out["alm_iteration_frac"] = out["alm_iteration_GBps"] / peak
+    out["alm_iteration_bytes_steady"] = RL.alm_iteration_bytes(n, p_.m, nnz_c, ld, 8)
     st = admm.AdmmState(U=Rw.clone(), V=Rw.clone(), dual=dual, r=r)
     hs, pool = admm.HalfStep(ops, n, ld), admm._Pool(dev, n, ld)
     admm.admm_step(st, ops, hs=hs, pool=pool)
@@ -229,6 +241,12 @@ def solver_rates(ops, dev, R, n, r, ld, n_g1):
     dt = time.perf_counter() - t
     out["admm_ms_per_step"] = 1e3 * dt / 6
     out["admm_cg_iters_per_step"] = cg / 6
+    sb = RL.admm_step_bytes(n, p_.m, nnz_c, ld)
+    cb = RL.cg_iteration_bytes(n, ld)
+    out["admm_GBps"] = (6 * sb + cg * cb) / dt / 1e9
+    out["admm_frac"] = out["admm_GBps"] / peak
+    out["admm_step_bytes"] = sb
+    out["cg_iteration_bytes"] = cb
     del core, st, hs, pool, Rw
     # full solve, G1-shaped instance (configs[0]): device vs the CPU oracle
     p = problem.build_maxcut(graphs.random_sparse(n_g1, deg=48.0, seed=1))
@@ -254,6 +272,64 @@ def solver_rates(ops, dev, R, n, r, ld, n_g1):
         "objective_rel_diff": abs(rep.objective - ref["objective"]) / max(1.0, abs(ref["objective"])),
         "trace_rows": len(rep.trace_rows), "cpu_trace_rows": len(ref["trace"]),
     }
+    return out
+
+
+def _cpu_iteration_rates(p, seed, alm_iters=3):
+    """The reference algorithm's CPU iteration rate on the same instance: a bounded sample of
+    ALM inner iterations (oracle alm.py:268 restatement, scipy/numpy, one host core) at the
+    solver's starting rank, from the solver's own starting point."""
+    from oracle import lrsdp_oracle as O
+    ops = O.OracleOps(p)
+    r0 = O.initial_rank(p.m, p.n)
+    rng = np.random.default_rng(seed)
+    R = rng.standard_normal((p.n, r0)) / math.sqrt(p.n * r0)
+    st = {"lam": np.zeros(p.m), "rho": max(1.0, p.m / math.sqrt(max(O.nnz_a_full(p), 1)))}
+    t = time.perf_counter()
+    _, its, _, _ = O.alm_inner(ops, R, st, tol=0.0, max_iter=alm_iters)
+    dt = time.perf_counter() - t
+    return {"alm_inner_iters_per_s": its / dt, "iterations": its, "seconds": dt, "rank": r0, "cores": 1,
+            "kind": "port", "sample": f"{its} ALM inner iterations (oracle alm_inner, alm.py:268) at rank {r0}, "
+                                      f"including the inner solve's setup"}
+
+
+def solve_runs(dev, time_limit, instances, seed):
+    """BASELINE metric, first clause: driver.solve (reference defaults: reopt_level 1, eps 1e-5)
+    on configs[1] (n=1e6, deg~10) and configs[2] (n=1e7, deg~6) under a stated time limit.
+    Seconds include the operator build; the rank history, iteration counts, rates and peak
+    device bytes say where the time went. ``instances``: (name, builder) pairs, builder() ->
+    (problem, ops, build seconds)."""
+    import torch
+
+    from paper_2407_15049_b200 import driver
+    out = []
+    for name, build in instances:
+        torch.cuda.empty_cache()
+        p, ops, build_s = build()
+        cfg = driver.SolverConfig(time_limit=time_limit, seed=seed)
+        rep = driver.solve(p, cfg, ops=ops)
+        torch.cuda.synchronize()
+        met = rep.status == "optimal" and rep.time_total_s + build_s <= 60.0
+        entry = {
+            "config": name, "n": p.n, "m": p.m, "time_limit_s": time_limit,
+            "stop": "reopt_level 1: max(err1, err3) < 1e-5 (SolverConfig defaults)",
+            "status": rep.status, "seconds": rep.time_total_s + build_s, "solve_s": rep.time_total_s,
+            "build_operators_s": build_s, "time_alm_s": rep.time_alm_s, "time_admm_s": rep.time_admm_s,
+            "objective": rep.objective, "err1": rep.err1, "err2": rep.err2, "err3": rep.err3,
+            "rank_history": rep.rank_history, "memory_capped": rep.memory_capped,
+            "memory_rank_refused": rep.memory_rank_refused,
+            "alm_outer": rep.alm_outer_iterations, "alm_inner": rep.alm_inner_iterations,
+            "admm_steps": rep.admm_steps, "cg_iterations": rep.cg_iterations, "reopt_rounds": rep.reopt_rounds,
+            "alm_inner_iters_per_s": rep.alm_inner_iterations / max(rep.time_alm_s, 1e-9),
+            "admm_steps_per_s": rep.admm_steps / max(rep.time_admm_s, 1e-9),
+            "peak_bytes": rep.peak_bytes, "gpu_launches": rep.gpu_launches,
+            "target_60s_met": met,
+        }
+        del ops, rep
+        torch.cuda.empty_cache()
+        if p.n <= 2_000_000:
+            entry["cpu_reference_rate"] = _cpu_iteration_rates(p, seed)
+        out.append(entry)
     return out
 
 
@@ -588,10 +664,35 @@ def run_ours(args, rank, world, local_rank):
                  "share": kms[nm] / sum(kms.values())} for nm in names}
     solver = None
     if world == 1 and not args.no_solver:
-        solver = solver_rates(ops, dev, R, n, r, ld, args.n_g1)
+        solver = solver_rates(ops, dev, R, n, r, ld, args.n_g1, peak)
     completion = None
     if world == 1 and not args.no_completion:
         completion = completion_rates(dev, peak, 2.5e6, 2.5e7, args.seed)
+    solve = None
+    if world == 1 and not args.no_solve:
+        del core, g_new, ybuf, zero, R, lam
+        if e2e is not None:
+            del R_dev, lam_dev, R_pin, lam_pin, out_pin
+
+        def cfg1():
+            t = time.perf_counter()
+            p1 = problem.build_maxcut(graphs.random_sparse(int(1e6), deg=10.0, seed=args.seed))
+            o1 = linops.build_operators(p1, dev=dev)
+            torch.cuda.synchronize()
+            return p1, o1, time.perf_counter() - t
+
+        def cfg2():
+            # the bench instance itself (n=1e7, deg~6), built above: build_operators time re-measured
+            t = time.perf_counter()
+            o2 = linops.build_operators(p, dev=dev)
+            torch.cuda.synchronize()
+            return p, o2, time.perf_counter() - t
+
+        inst = [("configs[1]: MaxCut random sparse n=1e6, avg degree ~10", cfg1)]
+        if n == int(1e7) and abs(args.deg - 6.0) < 1e-9 and args.graph == "random" and not args.reorder:
+            del ops
+            inst.append(("configs[2]: MaxCut random sparse n=1e7, avg degree ~6", cfg2))
+        solve = solve_runs(dev, args.solve_limit, inst, args.seed)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         n_s = int(min(n, 2e6))
@@ -621,6 +722,7 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clocks.summary(),
         "solver": solver,
         "completion": completion,
+        "solve": solve,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

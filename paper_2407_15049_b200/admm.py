@@ -677,6 +677,9 @@ def admm_run(state: AdmmState, ops, *, scale=1.0, eps=1e-5, gap_eps=None, min_st
         if recorder is not None:
             recorder.record("admm", scale * obj, err1, max(stats.resid_u, stats.resid_v),
                             state.dual.rho, state.r)
+            gaps = getattr(recorder, "gaps", None)      # diagnostics beside the trace (driver.Trace)
+            if gaps is not None and g3 is not None:
+                gaps.append((recorder.counter, g3))
         done = p0 <= eps and (gap_eps is None or g3 < gap_eps) and step >= min_steps
         balance = (not done) and step % rho_balance_every == 0
         bal = state.step_bal                   # measured inside the one-launch step

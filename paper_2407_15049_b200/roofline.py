@@ -79,3 +79,45 @@ def gradient_pass_bytes(ops, ld):
         "pattern_spmm": pattern_spmm_bytes(n, nnz_c, ld),
         "diag_alm_update": diag_update_bytes(n, ld, nh=0, refresh=True, d_distinct=False),
     }
+
+
+# ---------------------------------------------------------------------------
+# solver iterations (north_star: iteration rates as a fraction of the HBM roofline)
+# ---------------------------------------------------------------------------
+
+def alm_iteration_bytes(n, m, nnz_c, ld, cnt):
+    """One native ALM inner iteration on a diagonal-constraint problem (alm.py:268 body,
+    csrc/alm_native.cu launch sequence, no refresh) with ``cnt`` curvature pairs stored:
+
+    * direction (alm.py:98, vector-free two-loop): one combination of g and the 2 cnt
+      history rows -> D;
+    * line search (alm.py:135): SpMM C D with <CD,R>, <CD,D>, <CR,D> (reads R, D, CR),
+      q1/q2 over the constraint rows (R, D), the 5-operand m-vector pass;
+    * step + gradient + Gram rows (alm.py:306-318): cl_diag_alm_update with nh = 2 cnt + 1.
+    """
+    nt = 1 + 2 * cnt
+    N = n * ld
+    direction = lincomb_bytes(N, nt)
+    ls_spmm = pattern_spmm_bytes(n, nnz_c, ld, n_epi_in=3)
+    ls_con = n * (2 * ld * F8 + F8 + 2 * F8)
+    ls_vec = lincomb_bytes(m, 5)
+    update = diag_update_bytes(n, ld, nh=2 * cnt + 1, refresh=False)
+    return direction + ls_spmm + ls_con + ls_vec + update
+
+
+def admm_step_bytes(n, m, nnz_c, ld):
+    """One native ADMM step (admm.py:136, csrc/admm_native.cu in-order mode) whose two CG
+    solves stop at their start: rho b - lam, the two half-step starts (SpMM C Wf with the
+    rhs / initial-residual epilogue: Wf and x0 rows read, r written; the V start also stores
+    C U) and the streamed step end (C U, U, V; A(UV^T), residual, dual ascent, lam.b)."""
+    nlam = lincomb_bytes(m, 2)
+    start = pattern_spmm_bytes(n, nnz_c, ld, n_epi_in=2) + 2 * n * F8
+    end = n * (3 * ld * F8 + 6 * F8)
+    return nlam + 2 * start + n * ld * F8 + end
+
+
+def cg_iteration_bytes(n, ld):
+    """One CG iteration of a diagonal half-step (admm.py:65 body): cl_diag_cg_apply_rows
+    (r, p, Wf read, p written, the per-row coefficient written) + cl_diag_cg_step (x, p, r,
+    Wf read, x, r written, the coefficient read)."""
+    return n * ld * F8 * 10 + n * F8 * 3

@@ -12,13 +12,10 @@ it further. The device solver is therefore held to:
   reference's own 1-ulp horizon;
 * final status among the statuses the perturbed reference reaches;
 * final objective inside the perturbed reference's spread, widened by 1e-6
-  relative (north_star: final objective to 1e-6), for runs that converge
-  ("optimal"); runs stopped by a step cap before converging ("best_effort")
-  end past the chaotic horizon and are held to twice the spread;
-* trace length at most 2x the perturbed reference's longest run (and at
-  least half its shortest unless the device run stopped "optimal": runs that
-  meet the stop criterion early are allowed to -- the perturbed reference's
-  own "optimal" runs end anywhere in its range).
+  relative (north_star: final objective to 1e-6), for converged ("optimal")
+  and capped ("best_effort") runs alike;
+* trace length between half the perturbed reference's shortest run and twice
+  its longest (a comparable iteration count).
 """
 
 import numpy as np
@@ -61,16 +58,13 @@ def test_solve_within_reference_envelope(case):
     assert rep.status in statuses
     lo, hi = objs.min(), objs.max()
     pad = 1e-6 * max(1.0, abs(hi), abs(lo))
-    if case != "random_sdp":          # unbounded instance: objective is ~1e33 noise
-        if rep.status == "optimal":
-            assert lo - pad <= rep.objective <= hi + pad
-        else:
-            # capped, non-converged run: its last iterate lies far past the chaotic horizon and
-            # five perturbed reference runs under-sample where it can end -- sanity bound only
-            assert lo - 2 * (hi - lo) <= rep.objective <= hi + 2 * (hi - lo)
-    assert len(got) <= 2.0 * rows.max()
-    if rep.status != "optimal":
-        assert len(got) >= 0.5 * rows.min()
+    if case != "random_sdp":
+        # optimal and capped (best_effort) runs alike: inside the perturbed reference's spread,
+        # widened by 1e-6 relative. random_sdp is unbounded below (dense random A_i, no trace
+        # constraint): its objective is ~-1e33 noise that the reference's own runs spread over 33
+        # orders of magnitude, so only its status and trace horizon are compared.
+        assert lo - pad <= rep.objective <= hi + pad
+    assert 0.5 * rows.min() <= len(got) <= 2.0 * rows.max()
 
 
 def test_final_errors_recomputed_honestly():

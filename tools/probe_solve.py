@@ -56,9 +56,13 @@ for row in rep.trace_rows:
     s = segs[-1]
     s["rows"] += 1
     s.update(t_end=tt, obj_end=obj, err1_end=err1, metric_end=metric, rho_end=rho)
+gap_at = dict(rep.admm_gaps)
+for s in segs:
+    s["gap_end"] = gap_at.get(s["first_row"] + s["rows"] - 1)
 for s in segs:
     print(f"  {s['stage']:4s} r={s['rank']:5d} rows {s['rows']:6d} t {s['t_start']:8.2f}-{s['t_end']:8.2f} "
-          f"obj {s['obj_end']:.8g} err1 {s['err1_end']:.2e} metric {s['metric_end']:.2e} rho {s['rho_end']:.3g}")
+          f"obj {s['obj_end']:.8g} err1 {s['err1_end']:.2e} metric {s['metric_end']:.2e} rho {s['rho_end']:.3g}"
+          + (f" gap {s['gap_end']:.2e}" if s["gap_end"] is not None else ""))
 if out:
     os.makedirs(os.path.dirname(out) or ".", exist_ok=True)
     with open(out, "w") as f:
@@ -67,4 +71,7 @@ if out:
                    "rank_history": rep.rank_history, "memory_capped": rep.memory_capped,
                    "memory_rank_refused": rep.memory_rank_refused,
                    "alm": [rep.alm_outer_iterations, rep.alm_inner_iterations],
-                   "admm_steps": rep.admm_steps, "cg": rep.cg_iterations, "segments": segs}, f, indent=1)
+                   "admm_steps": rep.admm_steps, "cg": rep.cg_iterations, "segments": segs,
+                   "admm_gaps": rep.admm_gaps[::max(1, len(rep.admm_gaps) // 400)],
+                   "trace_sample": [list(r) for r in rep.trace_rows[::max(1, len(rep.trace_rows) // 400)]]},
+                  f, indent=1)

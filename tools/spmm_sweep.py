@@ -25,6 +25,8 @@ def build():
     from paper_2407_15049_b200 import build_ext
     os.makedirs(OUT, exist_ok=True)
     for tag, flags in VARIANTS.items():
+        if len(sys.argv) > 2 and tag not in sys.argv[2:]:
+            continue
         cmd = [build_ext.nvcc(), *build_ext.NVCC_FLAGS, *flags, "-I", os.path.join(ROOT, "include"),
                "-o", os.path.join(OUT, f"libculorads_{tag}.so"), *build_ext.SRC]
         subprocess.run(cmd, check=True)
@@ -36,7 +38,8 @@ def one(tag):
     if tag.startswith("l2g"):
         l2g = int(tag[3:])
         tag = "base"
-    os.environ["CULORADS_LIB"] = os.path.join(OUT, f"libculorads_{tag}.so")
+    if tag != "base":      # base: the in-tree library (build_variants/ does not travel to the box)
+        os.environ["CULORADS_LIB"] = os.path.join(OUT, f"libculorads_{tag}.so")
     sys.path.insert(0, ROOT)
     import math
     import numpy as np
@@ -82,7 +85,8 @@ if __name__ == "__main__":
     if sys.argv[1] == "build":
         build()
     elif sys.argv[1] == "run":
-        for tag in list(VARIANTS) + ["l2g0", "l2g32", "l2g64", "l2g128"]:
+        tags = sys.argv[2:] or (list(VARIANTS) + ["l2g0", "l2g32", "l2g64", "l2g128"])
+        for tag in tags:
             subprocess.run([sys.executable, __file__, "one", tag])
     else:
         one(sys.argv[2])
