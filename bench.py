@@ -345,8 +345,14 @@ def completion_rates(dev, peak, n_total, m, seed):
 
     t0 = time.perf_counter()
     half = int(n_total) // 2
-    p = problem.build_matrix_completion(graphs.random_completion(half, int(n_total) - half, int(m), seed=seed))
+    obs = graphs.random_completion(half, int(n_total) - half, int(m), seed=seed)
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    p = problem.build_matrix_completion(obs)
+    t_prob = time.perf_counter() - t0
+    t0 = time.perf_counter()
     ops = linops.build_operators(p, dev=dev)
+    torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     r = driver.initial_rank(p.m, p.n)
     ld = padded_ld(r)
@@ -406,7 +412,8 @@ def completion_rates(dev, peak, n_total, m, seed):
     torch.cuda.synchronize()
     admm_ms = 1e3 * (time.perf_counter() - t) / 2
     return {"instance": f"matrix completion n={p.n}, m={p.m} sampled entries (BASELINE configs[3] at one "
-                        f"of 8 GPUs' share), rank {r}, ld {ld}", "build_s": t_build, "kernels": kern,
+                        f"of 8 GPUs' share), rank {r}, ld {ld}", "build_s": t_build, "build_problem_s": t_prob,
+            "generate_instance_s": t_gen, "kernels": kern,
             "alm_inner_ms_per_iter": alm_ms, "admm_ms_per_step": admm_ms, "admm_cg_iters_per_step": cg / 2}
 
 

@@ -14,14 +14,14 @@ from __future__ import annotations
 
 import numpy as np
 
-from .problem import GraphEdgeList
+from .problem import GraphEdgeList, unique_sorted
 
 
 def _finish(n, u, v, rng, target=None):
     a = np.minimum(u, v)
     b = np.maximum(u, v)
     keep = a != b
-    code = np.unique(a[keep] * n + b[keep])
+    code = unique_sorted(a[keep] * n + b[keep])
     if target is not None and code.size > target:
         code = np.sort(rng.choice(code, size=target, replace=False))
     return GraphEdgeList(n, code // n, code % n, np.ones(code.size))
@@ -57,8 +57,8 @@ def random_completion(n2, n1, m, rank=2, seed=0):
     from .problem import ObservationSet
     rng = np.random.default_rng(seed)
     draw = int(m * 1.1) + 16
-    code = np.unique(rng.integers(0, n2, size=draw, dtype=np.int64) * n1
-                     + rng.integers(0, n1, size=draw, dtype=np.int64))
+    code = unique_sorted(rng.integers(0, n2, size=draw, dtype=np.int64) * n1
+                         + rng.integers(0, n1, size=draw, dtype=np.int64))
     if code.size > m:
         code = np.sort(rng.choice(code, size=m, replace=False))
     i, j = code // n1, code % n1

@@ -252,13 +252,32 @@ class AdjointOperator:
     """Support-aligned transpose rows plus objective values (linops.py:153)."""
 
     def __init__(self, m, n, sup_i, sup_j, omega, apat, c_vals, dev):
+        """``sup_i``/``sup_j`` (host position arrays of Omega) may be None: they are then
+        derived from the device CSR on first use (inspection/toarray only -- the solve
+        never needs Omega's positions on the host)."""
         self.m, self.n = m, n
-        self.sup_i_host, self.sup_j_host = sup_i, sup_j
+        self._sup = (sup_i, sup_j) if sup_i is not None else None
         self.omega, self.apat = omega, apat
         self.c_vals = c_vals
         self.dev = dev
         self._atrows = DevicePattern(omega.nnz, omega.at_ptr, omega.at_con, omega.at_val,
                                      None, None, None)
+
+    def _support(self):
+        if self._sup is None:
+            om = self.omega
+            counts = (om.indptr[1:] - om.indptr[:-1]).to(I64)
+            rows = torch.repeat_interleave(torch.arange(om.nrows, device=counts.device, dtype=I64), counts)
+            self._sup = (rows.cpu().numpy(), om.indices[:om.nnz].to(I64).cpu().numpy())
+        return self._sup
+
+    @property
+    def sup_i_host(self):
+        return self._support()[0]
+
+    @property
+    def sup_j_host(self):
+        return self._support()[1]
 
     @property
     def sup_i(self):
@@ -446,7 +465,7 @@ def build_operators(p: SdpProblem, dense_c=None, dev=None) -> OperatorBundle:
     apat.single_a = single
 
     cop = CompressedOperator(m, n, K, imap.to(I32), jmap.to(I32), slot_a, con, dev)
-    adj = AdjointOperator(m, n, sup_i.cpu().numpy(), sup_j.cpu().numpy(), omega, apat, cv, dev)
+    adj = AdjointOperator(m, n, None, None, omega, apat, cv, dev)      # Omega stays on the device
 
     diag = None
     if (m == n and p.a_val.size == m and np.array_equal(p.a_con, np.arange(m))

@@ -32,6 +32,7 @@ gather kernel.
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -315,8 +316,88 @@ def slice_pattern(pat, lo, hi, bounds, rank, world, group, con_map=None, halo=Tr
     return out, plan
 
 
-def build_sharded_operators(p, rank, world, dev, group=None):
+def is_diag_problem(p):
+    """Constraint c is a_c e_c e_c^T for every c (MaxCut family): the check of
+    linops.build_operators' diagonal fast path."""
+    m = p.m
+    return (m == p.n and p.a_val.size == m and np.array_equal(p.a_con, np.arange(m))
+            and np.array_equal(p.a_row, p.a_con) and np.array_equal(p.a_col, p.a_con))
+
+
+def build_sharded_diag_operators(p, rank, world, dev, group=None):
+    """Rank-local operators of a diagonal-constraint problem (MaxCut family), built from
+    this rank's own rows only: no global operator build, so per-rank device memory and
+    setup time scale with the rank's share of C (BASELINE configs[4], n = 1.7e8 over 8).
+
+    Produces the same patterns, halo plan and constraint rows as slicing the single-device
+    operators (``build_sharded_operators``'s general path; tests/test_shard.py checks
+    equality): Omega's rows [lo, hi) are C's mirrored entries of those rows plus the
+    diagonal positions (the constraints), each diagonal slot carrying one adjoint entry
+    (local constraint i, a_c); Omega_A is the diagonal alone; constraint c is owned by the
+    rank of row c, so the owned constraints are the block's rows and no multiplier halo
+    is needed."""
+    from .linops import (AdjointOperator, CompressedOperator, ConstraintCSR, DevicePattern, ObjectiveMatrix,
+                         OperatorBundle, _csr_ptr, padded)
+
+    n = p.n
+    b = block_bounds(n, world)
+    lo, hi = b[rank], b[rank + 1]
+    nown = hi - lo
+    tdev = dev.dev
+    F64 = torch.float64
+    r, c, v = np.asarray(p.C.rows), np.asarray(p.C.cols), np.asarray(p.C.vals)
+    sel1 = (r >= lo) & (r < hi)
+    sel2 = (r != c) & (c >= lo) & (c < hi)                   # mirrored (c, r) of stored (r, c)
+    rows = torch.as_tensor(np.concatenate([r[sel1], c[sel2]]).astype(np.int64)).to(tdev)
+    cols = torch.as_tensor(np.concatenate([c[sel1], r[sel2]]).astype(np.int64)).to(tdev)
+    vals = torch.as_tensor(np.concatenate([v[sel1], v[sel2]]).astype(np.float64)).to(tdev)
+    ccodes = (rows - lo) * n + cols
+    o = torch.argsort(ccodes)
+    ccodes, vals = ccodes[o], vals[o]
+    ar = torch.arange(nown, dtype=I64, device=tdev)
+    dcodes = ar * n + (ar + lo)
+    sup = torch.unique(torch.cat([ccodes, dcodes]), sorted=True)
+    S = int(sup.numel())
+    slot_c = torch.searchsorted(sup, ccodes)
+    slot_d = torch.searchsorted(sup, dcodes)
+    cv = padded(torch.zeros(S, dtype=F64, device=tdev))
+    cv[slot_c] = vals
+    sup_r, sup_c = sup // n, sup % n
+    o_ptr = _csr_ptr(sup_r, nown)
+    plan = HaloPlan(lo, hi, o_ptr, sup_c, b, rank, world, group)
+    aval = torch.as_tensor(np.ascontiguousarray(p.a_val[lo:hi], dtype=np.float64)).to(tdev)
+    omega = DevicePattern(nown, o_ptr, padded(plan.local_indices), cv, _csr_ptr(slot_d, S),
+                          padded(ar.to(I32)), padded(aval.clone()))
+    cpat = DevicePattern(nown, _csr_ptr(ccodes // n, nown), padded(plan.remap(ccodes % n).to(I32)),
+                         padded(vals), None, None, None)
+    apat = DevicePattern(nown, _csr_ptr(ar, nown), padded(ar.to(I32)), None, _csr_ptr(ar, nown),
+                         padded(ar.to(I32)), padded(aval.clone()))
+    halo = plan if (world > 1 and sum(plan.counts) > 0) else None
+    omega.halo = cpat.halo = halo
+    apat.halo = None                                      # diagonal positions: row-local
+    con = ConstraintCSR(m=nown, indptr=_csr_ptr(ar, nown), colidx=padded((ar + lo).to(I32)),
+                        pi=ar.to(I32).contiguous(), pj=ar.to(I32).contiguous(), val=padded(aval.clone()),
+                        diag_aval=aval)
+    sp_ = ShardProblem(p, lo, hi)
+    ids = (ar + lo).to(I32)
+    cop = CompressedOperator(nown, nown, n, ids, ids, None, con, dev)
+    adj = AdjointOperator(nown, nown, None, None, omega, apat, omega.cv, dev)
+    n_diag_stored = int(np.count_nonzero(r == c))
+    omega_ref = n if p.dense_c else p.C.nnz_full + (n - n_diag_stored)
+    ops = OperatorBundle(problem=sp_, cop=cop, adj=adj, c_mat=ObjectiveMatrix(adj, cpat), dev=dev,
+                         b=torch.as_tensor(np.ascontiguousarray(p.b[lo:hi], dtype=np.float64)).to(tdev),
+                         diag_aval=aval, omega_size_ref=omega_ref)
+    ops.row_range = (lo, hi)
+    ops.con_range = (lo, hi)
+    return ops
+
+
+def build_sharded_operators(p, rank, world, dev, group=None, local=True):
     """Rank-local OperatorBundle of a row-sharded solve.
+
+    Diagonal-constraint problems (MaxCut family) are built from the rank's own rows
+    (``build_sharded_diag_operators``) unless ``local`` is False; other constraint
+    families go through the general path below.
 
     Rows [lo, hi) of the factors and of the C/Omega/Omega_A patterns live on
     this rank. A constraint is owned by the rank of the smallest row among its
@@ -330,6 +411,8 @@ def build_sharded_operators(p, rank, world, dev, group=None):
     from .linops import (AdjointOperator, CompressedOperator, ConstraintCSR, ObjectiveMatrix,
                          OperatorBundle, build_operators, padded)
 
+    if local and is_diag_problem(p):
+        return build_sharded_diag_operators(p, rank, world, dev, group)
     full = build_operators(p, dev=dev)
     tdev = full.b.device
     b = block_bounds(p.n, world)
@@ -401,7 +484,7 @@ def build_sharded_operators(p, rank, world, dev, group=None):
     sp.m = hi_m - lo_m
     cop = CompressedOperator(hi_m - lo_m, hi - lo, full.cop.ncols, full.cop.imap, full.cop.jmap,
                              full.cop.col_slot, con, dev)
-    adj = AdjointOperator(hi_m - lo_m, hi - lo, full.adj.sup_i_host, full.adj.sup_j_host, omega, apat,
+    adj = AdjointOperator(hi_m - lo_m, hi - lo, None, None, omega, apat,
                           omega.cv, dev)
     ops = OperatorBundle(problem=sp, cop=cop, adj=adj, c_mat=ObjectiveMatrix(adj, cpat), dev=dev,
                          b=full.b[owned].clone(), diag_aval=aval, omega_size_ref=full.omega_size_ref)

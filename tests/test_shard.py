@@ -134,3 +134,75 @@ def test_block_bounds_cover_rows():
     for n, w in [(10, 3), (7, 7), (1000, 8)]:
         b = shard.block_bounds(n, w)
         assert b[0] == 0 and b[-1] == n and all(b[k] <= b[k + 1] for k in range(w))
+
+
+class _CpuDev:
+    """The slice of device.Device the operator builders use (no kernels run)."""
+
+    def __init__(self):
+        self.dev = torch.device("cpu")
+
+    def put(self, a, dtype=torch.float64):
+        return torch.as_tensor(np.ascontiguousarray(a)).to(dtype=dtype)
+
+
+def _same(a, b):
+    if a is None or b is None:
+        return a is None and b is None
+    return a.dtype == b.dtype and torch.equal(a.cpu(), b.cpu())
+
+
+def _check_local_diag_build(rank, world, d, n, deg):
+    """The per-rank MaxCut build (no global operator build) equals slicing the global one."""
+    from paper_2407_15049_b200 import graphs, problem, shard
+    p = problem.build_maxcut(graphs.random_sparse(n, deg=deg, seed=5))
+    dev = _CpuDev()
+    a = shard.build_sharded_operators(p, rank, world, dev, None, local=False)
+    b = shard.build_sharded_operators(p, rank, world, dev, None, local=True)
+    for pa, pb in ((a.adj.omega, b.adj.omega), (a.adj.apat, b.adj.apat), (a.c_mat.cpat, b.c_mat.cpat)):
+        for f in ("indptr", "indices", "cv", "at_ptr", "at_con", "at_val"):
+            assert _same(getattr(pa, f), getattr(pb, f)), f
+        assert pa.nrows == pb.nrows
+        assert (pa.halo is None) == (pb.halo is None)
+        if pa.halo is not None:
+            assert pa.halo.counts == pb.halo.counts and torch.equal(pa.halo.publish, pb.halo.publish)
+        assert pa.mhalo is None and pb.mhalo is None
+    ca, cb = a.cop.con, b.cop.con
+    for f in ("indptr", "colidx", "pi", "pj", "val", "diag_aval"):
+        assert _same(getattr(ca, f), getattr(cb, f)), f
+    assert ca.halo is None and cb.halo is None
+    assert torch.equal(a.b, b.b) and torch.equal(a.diag_aval, b.diag_aval)
+    assert a.omega_size_ref == b.omega_size_ref and a.cop.ncols == b.cop.ncols
+    assert a.row_range == b.row_range and a.con_range == b.con_range
+    assert a.problem.m == b.problem.m and a.problem.n == b.problem.n
+
+
+@pytest.mark.parametrize("world,n,deg", [(2, 400, 6.0), (3, 301, 10.0)])
+def test_local_diag_build_matches_global_slice(world, n, deg):
+    _run(_check_local_diag_build, world, n, deg)
+
+
+def test_streamed_row_block_draw_matches_global_draw():
+    """A rank's block of the reference's global random draws (initial factor: divided by
+    sqrt(n r0); escalation noise: multiplied by 1e-3/sqrt(n)) is bit-identical to slicing
+    the full draw, and leaves the generator where the full draw leaves it."""
+    import math
+    from paper_2407_15049_b200 import driver
+    old = driver._DRAW_CHUNK
+    driver._DRAW_CHUNK = 7
+    try:
+        n, r = 50, 3
+        full = np.random.default_rng(4).standard_normal((n, r)) / math.sqrt(n * r)
+        full2 = np.random.default_rng(4).standard_normal((n, r)) * (1e-3 / math.sqrt(n))
+        for lo, hi in [(0, 50), (3, 20), (13, 14), (49, 50)]:
+            got = driver._draw(np.random.default_rng(4), n, r, rows=(lo, hi), div=math.sqrt(n * r))
+            assert np.array_equal(got, full[lo:hi])
+            got = driver._draw(np.random.default_rng(4), n, r, mult=1e-3 / math.sqrt(n), rows=(lo, hi))
+            assert np.array_equal(got, full2[lo:hi])
+        g1 = np.random.default_rng(4)
+        driver._draw(g1, n, r, rows=(3, 9), div=2.0)
+        g2 = np.random.default_rng(4)
+        g2.standard_normal((n, r))
+        assert np.array_equal(g1.standard_normal(5), g2.standard_normal(5))
+    finally:
+        driver._DRAW_CHUNK = old
