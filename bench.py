@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--graph", choices=("random", "delaunay"), default="random",
                     help="random: BASELINE configs[2] (default); delaunay: mesh-like graph of degree 6")
     ap.add_argument("--reorder", action="store_true", help="relabel rows by the solver's RCM locality order")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="weak: --nrows rows per GPU (default; N=1 is BASELINE configs[2]); strong: --nrows "
+                         "rows in total, split over the GPUs (configs[4]: --scaling strong --nrows 1.7e8)")
     ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
                     help="gloo: functional check of the N>1 path with ranks sharing one GPU (no timing value)")
     return ap.parse_args()
@@ -454,6 +457,15 @@ def _max_over_ranks(x):
     return float(t.item())
 
 
+def _sum_over_ranks(x):
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t)
+    return float(t.item())
+
+
 def _bind_near_gpu(index):
     """Bind this thread to the CPUs NVML reports as local to GPU ``index``; returns the
     previous affinity (to restore), or None when that is not possible here."""
@@ -490,9 +502,11 @@ def run_ours(args, rank, world, local_rank):
         else:
             dist.init_process_group("gloo")
     n = int(args.n)
+    strong = args.scaling == "strong"
+    n_global = n if strong else world * n
     dev = device.default_device()
     halo_bytes = 0
-    if world == 1:
+    if world == 1 and not strong:
         if args.graph == "delaunay":
             # the paper's 10^7-scale instances are Delaunay meshes: a triangulated lattice
             # with scrambled labels, optionally relabelled by the solver's RCM order
@@ -508,24 +522,26 @@ def run_ours(args, rank, world, local_rank):
         ops = linops.build_operators(p, dev=dev)
         r = driver.initial_rank(p.m, p.n)
     else:
-        # weak scaling: every rank owns n rows of one random graph on world*n vertices;
-        # remote factor rows arrive by the halo all-gather inside the SpMM (shard.py)
+        # weak scaling: every rank owns n rows of one random graph on world*n vertices; strong
+        # scaling: the ranks split one graph on n vertices. Remote factor rows arrive by the
+        # halo all-gather inside the SpMM (shard.py); the graph is generated on the device.
         if args.graph != "random" or args.reorder:
             if rank == 0:
-                print("bench: --graph/--reorder apply at N=1 only (the N>1 instance is generated "
-                      "per rank); running the random graph", file=sys.stderr)
+                print("bench: --graph/--reorder apply at N=1 weak scaling only (the sharded instance is "
+                      "generated per rank); running the random graph", file=sys.stderr)
             args.graph, args.reorder = "random", False
         from paper_2407_15049_b200 import shard
         dev.group, dev.world = None, world
-        ops = shard.sharded_maxcut_ops(world * n, args.deg, args.seed, rank, world, dev)
+        ops = shard.sharded_maxcut_ops(n_global, args.deg, args.seed, rank, world, dev)
         p = ops.problem
+        n = p.n                          # this rank's rows
         n_edges = ops.n_edges
-        r = driver.initial_rank(world * n, world * n)
+        r = driver.initial_rank(n_global, n_global)
     ld = device.padded_ld(r)
     rng = np.random.default_rng(args.seed + rank)
-    R_host = rng.standard_normal((n, r)) / math.sqrt(world * n * r)
+    R_host = rng.standard_normal((n, r)) / math.sqrt(n_global * r)
     lam_host = 0.1 * rng.standard_normal(p.m)
-    rho = max(1.0, world * n / math.sqrt(world * n))
+    rho = max(1.0, n_global / math.sqrt(n_global))
     if world > 1:
         halo_bytes = ops.plan.halo_bytes(ld)
     R = linops.to_factor(R_host, dev, ld)
@@ -583,11 +599,15 @@ def run_ours(args, rank, world, local_rank):
         ms = t0.elapsed_time(t1) / K
     if world > 1:
         ms = _max_over_ranks(ms)
-    value = world * step_bytes / (ms * 1e-3) / 1e9
+    # whole-job algorithmic bytes: every rank's share (equal shares up to one row)
+    step_bytes_all = world * step_bytes
+    if world > 1:
+        step_bytes_all = _sum_over_ranks(step_bytes)
+    value = step_bytes_all / (ms * 1e-3) / 1e9
 
     # end to end through the reference-facing API with host buffers
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and world == 1 and not strong:
         # Every step copies its inputs host->device and its result device->host; consecutive
         # steps are pipelined over two copy streams (H2D of step k+1 and D2H of step k overlap
         # the compute, as a data loader would), with double-buffered device inputs.
@@ -637,7 +657,7 @@ def run_ours(args, rank, world, local_rank):
             e_ms = (time.perf_counter() - te) * 1e3 / K
         if world > 1:
             e_ms = _max_over_ranks(e_ms)
-        e2e = {"value": world * step_bytes / (e_ms * 1e-3) / 1e9, "unit": UNIT,
+        e2e = {"value": step_bytes_all / (e_ms * 1e-3) / 1e9, "unit": UNIT,
                "ms_per_step": e_ms, "h2d_bytes_per_step": int(R_host.nbytes + lam_host.nbytes),
                "d2h_bytes_per_step": int(n * r * 8),
                "path": "alm.alm_gradient (reference alm.py:239 signature) on pinned host R, lam; "
@@ -670,13 +690,13 @@ def run_ours(args, rank, world, local_rank):
                  "GB/s": kbytes[nm] / (kms[nm] * 1e-3) / 1e9,
                  "share": kms[nm] / sum(kms.values())} for nm in names}
     solver = None
-    if world == 1 and not args.no_solver:
+    if world == 1 and not strong and not args.no_solver:
         solver = solver_rates(ops, dev, R, n, r, ld, args.n_g1, peak)
     completion = None
-    if world == 1 and not args.no_completion:
+    if world == 1 and not strong and not args.no_completion:
         completion = completion_rates(dev, peak, 2.5e6, 2.5e7, args.seed)
     solve = None
-    if world == 1 and not args.no_solve:
+    if world == 1 and not strong and not args.no_solve:
         del core, g_new, ybuf, zero, R, lam
         if e2e is not None:
             del R_dev, lam_dev, R_pin, lam_pin, out_pin
@@ -709,9 +729,9 @@ def run_ours(args, rank, world, local_rank):
                          f"deg~{args.deg:g}, {res['steps']} steps, {res['threads']} threads"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded random graph, random factor/multiplier)",
-        "config": {"workload": workload_name(world * n, args.deg, args.graph, args.reorder), "n": world * n,
+        "config": {"workload": workload_name(n_global, args.deg, args.graph, args.reorder), "n": n_global,
                    "n_per_gpu": n,
                    "edges": n_edges, "halo_bytes_per_spmm_per_rank": halo_bytes,
                    "rank": r, "ld": ld, "step": "BM gradient pass: SDDMM A(RR^T) + SpMM C R + fused 2 S R",

@@ -150,6 +150,9 @@ class HaloPlan:
         key = (ld, like.device, slot)
         b = self._bufs.get(key)
         if b is None:
+            # a new leading dimension (rank escalation): the old rank's buffers are dead
+            for k in [k for k in self._bufs if k[0] != ld]:
+                del self._bufs[k]
             send = torch.zeros((self.maxb, ld), dtype=like.dtype, device=like.device)
             recv = torch.zeros((self.world * self.maxb, ld), dtype=like.dtype, device=like.device)
             b = self._bufs[key] = (send, recv)
@@ -533,3 +536,59 @@ def _solve_sharded(p, cfg, group, dev, world, rank, driver):
     if perm is not None:
         ops.perm = perm
     return driver.solve(p, cfg, ops=ops)
+
+
+# ---------------------------------------------------------------------------
+# per-rank device memory of a row-sharded solve
+# ---------------------------------------------------------------------------
+
+def halo_buffer_rows(ops):
+    """Rows of halo receive/send buffers a rank's operators allocate per leading dimension:
+    every distinct plan (C/Omega row halos: one buffer slot per SpMM operand in flight; the
+    constraint halo of non-diagonal constraints: one slot per distinct operand of the line
+    search, R and D)."""
+    plans = {}
+    for pat, slots in ((ops.c_mat.cpat, 1), (ops.adj.omega, 1), (ops.adj.apat, 1)):
+        h = getattr(pat, "halo", None)
+        if h is not None:
+            plans[id(h)] = (h, max(slots, plans.get(id(h), (h, 0))[1]))
+    h = getattr(ops.cop.con, "halo", None)
+    if h is not None:
+        plans[id(h)] = (h, max(2, plans.get(id(h), (h, 0))[1]))
+    return sum(slots * (h.halo_rows + h.maxb) for h, slots in plans.values())
+
+
+def memory_model(n_global, world, r, nnz_c_per_row, m_global=None, nnz_a_per_con=1.0, halo_frac=1.0,
+                 memory=8, halo_slots=1):
+    """Per-rank device bytes of a row-sharded solve at rank r.
+
+    * stage buffers: driver.stage_factor_buffers(memory) factors of n_loc x ld fp64
+      (the ALM stage dominates: 2 memory + 11 = 27 at the default L-BFGS memory 8);
+    * halo: ``halo_slots`` receive buffers of world * maxb rows plus the send buffer,
+      maxb = halo_frac * n_loc published rows (random graphs: every row has a remote
+      neighbour, halo_frac ~ 1; locality-ordered meshes: only the block-boundary band);
+    * operators: C rows (int32 index + fp64 value per nonzero, int64 row pointer), Omega
+      (index, value, adjoint pointer per slot; constraint id + coefficient per adjoint
+      entry), Omega_A and the constraint rows;
+    * 16 m-vectors of the owned constraints.
+    Returns a dict of byte counts and their total."""
+    from .device import padded_ld
+    from .driver import stage_factor_buffers
+    m_global = n_global if m_global is None else m_global
+    ld = padded_ld(r)
+    n_loc = -(-n_global // world)
+    m_loc = -(-m_global // world)
+    nnz_c = n_loc * nnz_c_per_row
+    nnz_a = m_loc * nnz_a_per_con
+    factor = 8 * n_loc * ld
+    maxb = int(halo_frac * n_loc)
+    out = {
+        "n_per_rank": n_loc, "ld": ld, "factor_bytes": factor,
+        "stage_buffers": stage_factor_buffers(memory) * factor,
+        "halo": (halo_slots * (world * maxb) + maxb) * ld * 8 if world > 1 else 0,
+        "operators": (nnz_c * 12 + n_loc * 8) + (nnz_c + 2 * nnz_a) * 20 + nnz_a * 12 * 2 + nnz_a * 28
+                     + m_loc * 8 + 2 * n_loc * 8,
+        "m_vectors": 16 * 8 * m_loc,
+    }
+    out["total"] = sum(v for k, v in out.items() if k not in ("n_per_rank", "ld", "factor_bytes"))
+    return out

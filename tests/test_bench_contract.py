@@ -37,7 +37,8 @@ def test_reference_arm_line():
 
 @pytest.mark.gpu
 def test_device_arm_line():
-    d = _run("--steps", "2", "--warmup", "3", "--nrows", "200000", "--no-cpu-baseline", "--no-solver", "--no-completion")
+    d = _run("--steps", "2", "--warmup", "3", "--nrows", "200000", "--no-cpu-baseline", "--no-solver", "--no-completion",
+             "--no-solve")
     assert d["metric"] == _metric() and d["unit"] == "GB/s" and d["value"] > 0
     assert d["steps"] == 2 and d["warmup"] == 3 and d["dtype"] == "f64" and d["vs_baseline"] is None
     assert d["config"]["workload"] and "model" not in d["config"]
@@ -70,3 +71,23 @@ def test_device_arm_two_ranks_gloo():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
     assert d["config"]["halo_bytes_per_spmm_per_rank"] > 0
+
+
+@pytest.mark.gpu
+def test_device_arm_two_ranks_strong_scaling_gloo():
+    """--scaling strong: the two ranks split one graph of --nrows vertices."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--nrows", "300000", "--scaling", "strong",
+           "--no-cpu-baseline", "--no-e2e", "--dist-backend", "gloo"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["n"] == 300000 and d["config"]["n_per_gpu"] == 150000
