@@ -241,7 +241,7 @@ int cl_sddmm(int64_t K, const int32_t* imap, const int32_t* jmap, int32_t ld,
  * step update and gradient (alm.py:306-318) become row-local and fuse into one pass.
  *   R  += tau*D;  CR += tau*CD;  ax_out[c] = ax[c] + tau*q1[c] + tau^2*q2[c]
  *   w[c] = lam[c] + rho*(ax[c]-b[c]);  g_new = 2*(w[row]*a*R + scale*CR)
- *   y = g_new - g_old
+ *   y = g_new - g_old        (g_old NULL: 0, y = g_new -- the inner solve's first gradient)
  * plus dots: <CR,R>, <g_new,g_new>, <y, tau D>, lam·res, res·res and the
  * multi-dots of g_new and y against up to `nh` history vectors H[]:
  *   dots[0]=<CR,R> [1]=<g,g> [2]=<y,D> [3]=lam·res [4]=res·res [5]=<y,y>
@@ -358,7 +358,7 @@ typedef struct {
     double* q1;
     double* q2;
     double* wv;
-    const double* zero_g;
+    const double* zero_g;      /* g_old of the first gradient: NULL (= 0, no buffer) or a zero factor */
     int32_t nbuf;
     double* bufs[CL_ALM_MAXBUF];
     cl_pattern cpat;

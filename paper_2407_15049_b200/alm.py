@@ -513,8 +513,6 @@ def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory
     bufs = getattr(core, "native_bufs", None)
     if bufs is None or len(bufs) < nbuf:
         bufs = core.native_bufs = [dev.empty(n, ld) for _ in range(nbuf)]
-    if core.zero_g is None:
-        core.zero_g = dev.zeros(n, ld)
     a = _lib.AlmInnerArgs()
     a.n, a.ld, a.memory, a.max_iter = n, ld, memory, max_iter
     a.tol = float(tol)
@@ -524,7 +522,7 @@ def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory
     a.R, a.CR, a.CD = R.data_ptr(), core.CR.data_ptr(), core.CD.data_ptr()
     a.ax, a.ax2 = core.ax.data_ptr(), core.ax2.data_ptr()
     a.q1, a.q2, a.wv = core.q1.data_ptr(), core.q2.data_ptr(), core.wv.data_ptr()
-    a.zero_g = core.zero_g.data_ptr()
+    a.zero_g = None                 # g_old = 0 for the first gradient: no zero factor is held
     a.nbuf = nbuf
     for j in range(nbuf):
         a.bufs[j] = bufs[j].data_ptr()
@@ -709,17 +707,19 @@ def residual_norm(ops, ax, at=300):
 
 def alm_outer(R, dual: DualVector, ops, *, scale=1.0, switch_threshold=1e-3, outer_cap=50,
               inner_cap=500, inner_tol_floor=1e-8, lbfgs_memory=8, rho_growth=2.0, rho_max=1e8,
-              escalate=None, recorder=None, deadline=None, rank=None) -> AlmResult:
+              escalate=None, recorder=None, deadline=None, rank=None, own=False) -> AlmResult:
     """Inner solves + dual ascent until the primal switch threshold (alm.py:337).
 
     ``dual.lam`` is updated in place on the device when it is a device tensor.
     ``escalate(R_dev, r) -> (R_dev_new, r_new) or None`` raises the rank.
+    ``own``: the caller hands R over (the driver): it is iterated in place instead of
+    copied, saving one factor of HBM.
     """
     host = not isinstance(R, torch.Tensor)
     dev = ops.dev
     p = ops.problem
     Rd, ld = _prep(ops, R)
-    if Rd is R:
+    if Rd is R and not own:
         Rd = Rd.clone()
     r = R.shape[1] if rank is None else rank
     lam = _lam_dev(ops, dual.lam)

@@ -340,7 +340,7 @@ __device__ void update_pass(const Az& z, const Ctl& c, bool fresh, const double*
             double2 g;
             g.x = 2.0 * (wa * R.x + a.scale * CR.x);
             g.y = 2.0 * (wa * R.y + a.scale * CR.y);
-            const double2 go = ldcg2(gold + off);
+            const double2 go = gold != nullptr ? ldcg2(gold + off) : make_double2(0.0, 0.0);
             const double2 y = make_double2(g.x - go.x, g.y - go.y);
             st2(gn + off, g);
             st2(yv + off, y);
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(AT) alm_fused_kernel(Az z) {
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < AK; ++k) v[k] = 0.0;
-        update_pass(z, c, true, a.ax, a.ax, a.R, a.zero_g, v);
+        update_pass(z, c, true, a.ax, a.ax, a.R, a.zero_g, v);   // zero_g may be NULL: g_old = 0
         a_reduce(v, 7, ws, region);
         if (t0) {
             const int t = c.gscr;     // g now holds the gradient

@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(NT) diag_update_kernel(DiagDev a, double* ws, 
         double2 g;
         g.x = 2.0 * (wa * R.x + a.scale * CR.x);
         g.y = 2.0 * (wa * R.y + a.scale * CR.y);
-        const double2 go = ld2cs(a.g_old + off);
+        const double2 go = a.g_old != nullptr ? ld2cs(a.g_old + off) : make_double2(0.0, 0.0);   // NULL: g_old = 0
         const double2 y = make_double2(g.x - go.x, g.y - go.y);
         st2(a.g_new + off, g);
         st2(a.y + off, y);
