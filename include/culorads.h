@@ -270,6 +270,27 @@ int cl_basis_project(const double* Q, int64_t ldq, int32_t k_cnt, int64_t n, con
 int cl_basis_subtract(const double* Q, int64_t ldq, int32_t k_cnt, int64_t n, const double* h,
                       double* v, void* stream);
 
+/* Row-sharded solve (shard.py): the native loops below run on one rank's row
+ * block when `dist` is set. The caller (the Python host, over torch.distributed)
+ * supplies two hooks:
+ *   exchange  halo of a factor before a C product: packs this rank's published
+ *             rows of X (n_own x ld) and all-gathers them; returns the device
+ *             address of the ghost rows (pattern column j >= nown reads
+ *             ghost[j - nown]), NULL on failure;
+ *   reduce    combines slab[0:count) over the ranks (rank-ordered sum, identical
+ *             bits on every rank) into host[0:count) (pinned) after the stream's
+ *             queued work; 0 on success.
+ * Every reduction of the diagonal-constraint loops is a sum over rows, so with
+ * the hooks the loops take the same decisions as the single-GPU ones. CG steps
+ * then read <p, Q> before the update (alpha on the host), as the Python-driven
+ * sharded path does. NULL `dist`: single GPU. */
+typedef struct {
+    void* ctx;
+    const double* (*exchange)(void* ctx, const double* X, int32_t ld);
+    int32_t (*reduce)(void* ctx, double* slab, double* host, int32_t count, void* stream);
+    int64_t nown;
+} cl_dist_hooks;
+
 /* One ADMM step (admm.py:136 admm_step: U half-solve, V half-solve, dual
  * ascent) for diagonal constraints, with every scalar decision of the
  * reference (tolerance schedule, cg_solve's stop/curvature/finiteness
@@ -308,6 +329,7 @@ typedef struct {
     double* ws;                /* reduction workspace (CL_WS_ALLOC doubles) */
     void* stream;
     int32_t want_balance;      /* one-launch step: also return ||U_new-U||^2, ||V_new-V||^2 */
+    const cl_dist_hooks* dist; /* row-sharded solve (cl_admm_step_diag only), or NULL */
 } cl_admm_diag_args;
 
 typedef struct {
@@ -369,6 +391,7 @@ typedef struct {
     int32_t rec_cap;
     double* rec;               /* 4 * rec_cap host doubles */
     double* gnorms;            /* rec_cap host doubles */
+    const cl_dist_hooks* dist; /* row-sharded solve (cl_alm_inner_diag only), or NULL */
 } cl_alm_inner_args;
 
 typedef struct {

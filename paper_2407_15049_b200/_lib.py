@@ -95,6 +95,15 @@ class DiagUpdateArgs(ctypes.Structure):
                 ("nh", I32), ("H", P * CL_MAXIN), ("refresh", I32)]
 
 
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32)
+REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                             ctypes.c_void_p)
+
+
+class DistHooks(ctypes.Structure):
+    _fields_ = [("ctx", P), ("exchange", EXCHANGE_FN), ("reduce", REDUCE_FN), ("nown", I64)]
+
+
 class AdmmDiagArgs(ctypes.Structure):
     _fields_ = [("n", I64), ("ld", I32), ("aval", P), ("b", P), ("lam", P), ("lam_new", P), ("ax", P),
                 ("ax_valid", I32),
@@ -102,7 +111,7 @@ class AdmmDiagArgs(ctypes.Structure):
                 ("r", P), ("r_v", P), ("p", P), ("Q", P), ("cu", P), ("nlam", P), ("res", P),
                 ("cpat", Pattern), ("rho", D), ("scale", D), ("binf", D), ("rel_floor", D),
                 ("primal_coeff", D), ("cg_cap", I32), ("slab", P), ("host", P), ("ws", P), ("stream", P),
-                ("want_balance", I32)]
+                ("want_balance", I32), ("dist", ctypes.POINTER(DistHooks))]
 
 
 class AdmmStepStats(ctypes.Structure):
@@ -121,7 +130,8 @@ class AlmInnerArgs(ctypes.Structure):
                 ("rho", D), ("scale", D), ("b1", D), ("aval", P), ("b", P), ("lam", P), ("R", P), ("CR", P),
                 ("CD", P), ("ax", P), ("ax2", P), ("q1", P), ("q2", P), ("wv", P), ("zero_g", P),
                 ("nbuf", I32), ("bufs", P * CL_ALM_MAXBUF), ("cpat", Pattern), ("slab", P), ("host", P),
-                ("ws", P), ("stream", P), ("rec_cap", I32), ("rec", P), ("gnorms", P)]
+                ("ws", P), ("stream", P), ("rec_cap", I32), ("rec", P), ("gnorms", P),
+                ("dist", ctypes.POINTER(DistHooks))]
 
 
 class AlmInnerStats(ctypes.Structure):

@@ -319,7 +319,7 @@ def _resid(ops, ax, res, at):
     ops.dev.lincomb(res, [ax, ops.b], [1.0, -1.0], dots=[("out", "out")], at=at)
 
 
-NATIVE = True     # diagonal constraints, one device: run the step's control flow in C++
+NATIVE = True     # diagonal constraints: run the step's control flow in C++ (row-sharded: with hooks)
 # Problems with at most this many row-lanes (n times the lanes that share a factor row,
 # lanes_for(ld)) run each ADMM step as one cooperative launch (cl_admm_step_diag_fused):
 # there, latency rather than HBM bounds the step (measured crossover).
@@ -380,8 +380,12 @@ def _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, 
     a.want_balance = 1 if getattr(state, "want_balance", False) else 0
     a.rel_floor, a.primal_coeff, a.cg_cap = float(cg_rel_floor), float(cg_primal_coeff), int(cg_cap)
     global FUSED
+    if dev.world > 1 and not a.dist:         # row-sharded: halo exchanges and reductions via hooks
+        from .shard import native_hooks
+        hs.dist_hooks = native_hooks(dev, ops)
+        a.dist = hs.dist_hooks
     st = _lib.AdmmStepStats()
-    fused = FUSED and n >= 1 and n * lanes_for(ld) <= FUSED_MAX_LANES
+    fused = FUSED and dev.world == 1 and n >= 1 and n * lanes_for(ld) <= FUSED_MAX_LANES
     if fused:
         rc = dev.lib.cl_admm_step_diag_fused(ctypes.byref(a), ctypes.byref(st))
         if _lib.coop_refused(rc, "cl_admm_step_diag_fused"):
@@ -549,7 +553,7 @@ def admm_step(state: AdmmState, ops, *, scale=1.0, cg_cap=200, cg_rel_floor=1e-1
     if ops.is_diag:
         n, ld = state.U.shape
         hs = hs or HalfStep(ops, n, ld)
-        if NATIVE and dev.world == 1:
+        if NATIVE:
             return _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, hs, pool)
         return _admm_step_diag_py(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, hs, pool)
     p = ops.problem

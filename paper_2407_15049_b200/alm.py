@@ -496,7 +496,7 @@ class InnerResult:
     ax: object
 
 
-NATIVE = True     # diagonal constraints, one device: run the inner loop's control flow in C++
+NATIVE = True     # diagonal constraints: run the inner loop's control flow in C++ (row-sharded: with hooks)
 # Problems with n*ld at most this many doubles run the whole inner solve as one
 # cooperative launch (cl_alm_inner_diag_fused): latency, not HBM, bounds them.
 FUSED = os.environ.get("CULORADS_FUSED", "1") != "0"
@@ -536,8 +536,13 @@ def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory
     a.rec = rec.ctypes.data
     a.gnorms = gn.ctypes.data
     global FUSED
+    if dev.world > 1:                       # row-sharded: halo exchanges and reductions via hooks
+        if getattr(core, "dist_hooks", None) is None:
+            from .shard import native_hooks
+            core.dist_hooks = native_hooks(dev, ops)
+        a.dist = core.dist_hooks
     st = _lib.AlmInnerStats()
-    fused = FUSED and n >= 1 and n * ld <= FUSED_MAX_ELEMS
+    fused = FUSED and dev.world == 1 and n >= 1 and n * ld <= FUSED_MAX_ELEMS
     if fused:
         R_keep = R.clone()          # the one launch steps R in place; kept for a void launch
         rc = dev.lib.cl_alm_inner_diag_fused(ctypes.byref(a), ctypes.byref(st))
@@ -570,8 +575,7 @@ def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory
 def _inner(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory, recorder):
     """alm.py:268 on device buffers. R is updated in place."""
     dev, ops = core.dev, core.ops
-    if (NATIVE and ops.is_diag and dev.world == 1 and memory <= 8 and core.ld >= 2
-            and getattr(ops, "row_range", None) is None):
+    if NATIVE and ops.is_diag and memory <= 8 and core.ld >= 2:
         return _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory, recorder)
     b1 = ops.problem.b_norm1
     pool = core.pool

@@ -64,6 +64,14 @@ enum {
 
 bool fetch(Ctx& c, int lo, int cnt) {
     if (c.rc) return false;
+    if (c.a->dist != nullptr) {     // row-sharded: the partial sums are combined over the ranks
+        if (c.a->dist->reduce(c.a->dist->ctx, c.a->slab + lo, c.a->host + lo, cnt, (void*)c.st) != 0) {
+            c.rc = CL_EARG;
+            c.line = __LINE__;
+            return false;
+        }
+        return true;
+    }
     cudaError_t e = cudaMemcpyAsync(c.a->host + lo, c.a->slab + lo, cnt * sizeof(double), cudaMemcpyDeviceToHost,
                                     c.st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c.st);
@@ -120,6 +128,15 @@ void cg_init(Ctx& c, const double* x0, const double* Wf, double* r, int slot, do
     const cl_admm_diag_args* a = c.a;
     cl_pattern P = a->cpat;
     P.c_coeff = 1.0;
+    if (a->dist != nullptr && !c.rc) {      // row-sharded: C Wf reads Wf's halo
+        P.ghost = a->dist->exchange(a->dist->ctx, Wf, a->ld);
+        P.nown = a->dist->nown;
+        if (P.ghost == nullptr) {
+            c.rc = CL_EARG;
+            c.line = __LINE__;
+            return;
+        }
+    }
     CL_TRY(c, cl_diag_admm_cg_init(&P, Wf, x0, a->ld, a->scale, a->rho, a->nlam, a->aval, r, cw, a->slab + slot,
                                    a->ws, (void*)c.st));
 }
@@ -150,10 +167,23 @@ int cg_loop(Ctx& c, const double* x0, double* x, const double* Wf, double* r, do
         // (Q is never stored: its first n doubles hold the per-row coefficients it is rebuilt from)
         CL_TRY(c, cl_diag_cg_apply_rows(a->n, a->ld, a->aval, a->rho, beta, r, a->p, Wf, a->Q, a->slab + S_PQ,
                                         a->ws, (void*)c.st));
-        CL_TRY(c, cl_diag_cg_step(a->n, a->ld, a->rho, a->Q, Wf, 0.0, qr, a->slab + S_PQ, xs, x, a->p, r,
-                                  a->slab + S_QN, a->ws, (void*)c.st));
-        if (!fetch(c, S_PQ, 2)) return 0;
-        const double pq = H(c, S_PQ);
+        double pq;
+        if (a->dist == nullptr) {
+            CL_TRY(c, cl_diag_cg_step(a->n, a->ld, a->rho, a->Q, Wf, 0.0, qr, a->slab + S_PQ, xs, x, a->p, r,
+                                      a->slab + S_QN, a->ws, (void*)c.st));
+            if (!fetch(c, S_PQ, 2)) return 0;
+            pq = H(c, S_PQ);
+        } else {
+            // row-sharded: <p, Q> is a per-rank partial until combined -- read it, take alpha
+            // on the host, then update (the sequence of admm._admm_step_diag_py)
+            if (!fetch(c, S_PQ, 1)) return 0;
+            pq = H(c, S_PQ);
+            if (isfinite(pq) && pq > 0.0) {
+                CL_TRY(c, cl_diag_cg_step(a->n, a->ld, a->rho, a->Q, Wf, qr / pq, 0.0, nullptr, xs, x, a->p, r,
+                                          a->slab + S_QN, a->ws, (void*)c.st));
+                if (!fetch(c, S_QN, 1)) return 0;
+            }
+        }
         if (!isfinite(pq) || pq <= 0.0) {          // the device update was skipped
             *last_is_x = xs == x;
             *its_out = its;
@@ -227,7 +257,7 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
 
     // U start; at small n also the V start and the step end, speculatively assuming U (then V)
     // is kept, read at one synchronize
-    const bool spec = c.N <= SPEC_MAX_ELEMS;
+    const bool spec = c.N <= SPEC_MAX_ELEMS && a->dist == nullptr;
     cg_init(c, a->U, a->V, a->r, S_RHSU, nullptr);
     if (spec) {
         cg_init(c, a->V, a->U, a->r_v, S_RHSV, a->cu);

@@ -44,6 +44,15 @@ enum { S_DIR = 0, S_LS = 40, S_MV = 48, S_UPD = 64 };
 
 bool fetch(Ctx& c, int count) {
     if (c.rc) return false;
+    if (c.a->dist != nullptr) {     // row-sharded: the partial sums are combined over the ranks
+        const int rc = c.a->dist->reduce(c.a->dist->ctx, c.a->slab, c.a->host, count, (void*)c.st);
+        if (rc != 0) {
+            c.rc = CL_EARG;
+            c.line = __LINE__;
+            return false;
+        }
+        return true;
+    }
     cudaError_t e = cudaMemcpyAsync(c.a->host, c.a->slab, count * sizeof(double), cudaMemcpyDeviceToHost, c.st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c.st);
     if (e != cudaSuccess) {
@@ -217,10 +226,26 @@ void constraint_values(Ctx& c, const double* R, double* out) {
                                    (void*)c.st));
 }
 
+// C's pattern for a product with X; a row-sharded solve first exchanges X's halo
+bool c_pattern(Ctx& c, const double* X, cl_pattern* P) {
+    *P = c.a->cpat;
+    P->c_coeff = 1.0;
+    if (c.a->dist != nullptr && !c.rc) {
+        P->ghost = c.a->dist->exchange(c.a->dist->ctx, X, c.a->ld);
+        P->nown = c.a->dist->nown;
+        if (P->ghost == nullptr) {
+            c.rc = CL_EARG;
+            c.line = __LINE__;
+            return false;
+        }
+    }
+    return !c.rc;
+}
+
 void c_times(Ctx& c, const double* X, double* out) {
     const cl_alm_inner_args* a = c.a;
-    cl_pattern P = a->cpat;
-    P.c_coeff = 1.0;
+    cl_pattern P;
+    if (!c_pattern(c, X, &P)) return;
     TRY(c, cl_pattern_spmm(&P, X, a->ld, 1.0, nullptr, out, nullptr, nullptr, (void*)c.st));
 }
 
@@ -342,8 +367,8 @@ extern "C" int cl_alm_inner_diag(const cl_alm_inner_args* a, cl_alm_inner_stats*
         // ---- exact line search (AlmCore.line_search, alm.py:135) ----
         double* D = B(c, Dn);
         {
-            cl_pattern P = a->cpat;
-            P.c_coeff = 1.0;
+            cl_pattern P;
+            c_pattern(c, D, &P);
             cl_epilogue E;
             memset(&E, 0, sizeof(E));
             E.nz = 3;

@@ -592,3 +592,65 @@ def memory_model(n_global, world, r, nnz_c_per_row, m_global=None, nnz_a_per_con
     }
     out["total"] = sum(v for k, v in out.items() if k not in ("n_per_rank", "ld", "factor_bytes"))
     return out
+
+
+# ---------------------------------------------------------------------------
+# hooks of the native loops (cl_dist_hooks, include/culorads.h)
+# ---------------------------------------------------------------------------
+
+class _RawRows:
+    """A device factor known only by its address (what HaloPlan.exchange needs of it)."""
+
+    def __init__(self, addr, ld, like):
+        self.addr, self.ld = addr, ld
+        self.dtype, self.device = like.dtype, like.device
+
+    def reshape(self, *shape):
+        return self
+
+    def data_ptr(self):
+        return self.addr
+
+
+def native_hooks(dev, ops):
+    """cl_dist_hooks for cl_alm_inner_diag / cl_admm_step_diag on a row-sharded solve, or
+    None on one GPU. ``exchange`` is C's halo exchange (the only pattern with remote
+    columns in the diagonal-constraint loops); ``reduce`` is Device.fetch's rank-ordered
+    all-reduce of a slab range into the pinned host mirror."""
+    if dev.world == 1:
+        return None
+    import ctypes
+    import sys
+    import traceback
+
+    from . import _lib
+    plan = getattr(ops.c_mat.cpat, "halo", None)
+    slab0, host0 = dev.slab.data_ptr(), dev.host.data_ptr()
+
+    def exchange(ctx, xptr, ld):
+        try:
+            if plan is None:           # no remote column on any rank: the ghost block is never read
+                return xptr
+            return plan.exchange(_RawRows(xptr, ld, dev.slab), ld, dev.gather_rows).data_ptr()
+        except Exception:             # noqa: BLE001 -- reported, then surfaced as CL_EARG by the loop
+            traceback.print_exc(file=sys.stderr)
+            return None
+
+    def reduce(ctx, sptr, hptr, count, stream):
+        try:
+            so, ho = (sptr - slab0) // 8, (hptr - host0) // 8
+            red = all_reduce_sum(dev.slab[so:so + count].clone(), dev.group)
+            dev.host[ho:ho + count].copy_(red, non_blocking=True)
+            dev.stream.synchronize()
+            return 0
+        except Exception:             # noqa: BLE001
+            traceback.print_exc(file=sys.stderr)
+            return 1
+
+    h = _lib.DistHooks()
+    h.ctx = None
+    h.exchange = _lib.EXCHANGE_FN(exchange)
+    h.reduce = _lib.REDUCE_FN(reduce)
+    h.nown = plan.nown if plan is not None else int(ops.problem.n)
+    h._keep = (h.exchange, h.reduce)          # the callbacks live as long as the struct
+    return ctypes.pointer(h)

@@ -279,3 +279,48 @@ def test_sharded_locality_ordered_solve():
     # the ALM stage and the first ADMM steps agree to 1e-9; later rows part by chaos
     assert horizon >= min(len(ref), len(tr), 100)
     assert abs(res[0][2] - single.objective) <= 1e-3 * abs(single.objective)
+
+
+def _native_twin_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2407_15049_b200 import admm, alm, driver, shard
+        from paper_2407_15049_b200.device import Device
+        from tests._golden import cfg_of, load, problem_from
+        z = load("solve_g1_like.npz")
+        cfg = dict(cfg_of(z))
+        cfg.update(admm_step_cap=60, max_reopts=1)
+        p = problem_from(z)
+        out = []
+        for native in (True, False):
+            alm.NATIVE = admm.NATIVE = native
+            rep = shard.solve_sharded(p, driver.SolverConfig(**cfg), dev=Device())
+            out.append((np.array([r[2:7] for r in rep.trace_rows], dtype=float), rep.objective, rep.gpu_launches))
+        q.put((rank, out))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_native_loops_match_python_twins():
+    """Row-sharded solves run the native C++ ALM inner loop and ADMM step with the
+    distributed hooks (halo exchange + rank-ordered slab reduction as callbacks,
+    include/culorads.h cl_dist_hooks): bit-identical trace to the Python-driven loops."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = 2
+    pc = mp.spawn(_native_twin_worker, args=(world, _free_port(), q), nprocs=world, join=False)
+    res = [q.get(timeout=900) for _ in range(world)]
+    while not pc.join():
+        pass
+    for rank, out in res:
+        assert not isinstance(out, str), out
+        (tn, on, ln), (tp, op, lp) = out
+        print(f"rank {rank}: rows {len(tn)} objective {on!r} launches native {ln} python {lp}")
+        assert len(tn) == len(tp) and np.array_equal(tn, tp) and on == op

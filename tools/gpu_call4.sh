@@ -1,0 +1,18 @@
+#!/bin/bash
+# round-2 profiling call: gather probe, completion kernels and one-launch kernels under ncu, default bench
+O=gpurun_out/r2
+mkdir -p $O
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/gputests.txt 2>&1
+tail -5 $O/gputests.txt
+./tools/micro/gather_probe > $O/gather_plain.txt 2>&1
+timeout 300 ncu --metrics dram__bytes_read.sum,gpu__time_duration.sum,lts__t_sectors_op_read.sum --csv \
+  ./tools/micro/gather_probe > $O/gather_ncu.csv 2>&1
+for k in constraint_kernel single_entry_apply_kernel assemble_kernel spmm_tiled_kernel; do
+  timeout 400 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -f -o $O/completion_$k \
+    python tools/probe_completion.py 1.25e6 1.25e6 2.5e7 > $O/completion_ncu_$k.log 2>&1
+done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"fused" -c 3 -f -o $O/fused \
+  python tools/g1_solve.py > $O/fused_ncu.log 2>&1
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
+tail -3 $O/bench.err
