@@ -12,7 +12,12 @@ for k in constraint_kernel single_entry_apply_kernel assemble_kernel spmm_tiled_
   timeout 400 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -f -o $O/completion_$k \
     python tools/probe_completion.py 1.25e6 1.25e6 2.5e7 > $O/completion_ncu_$k.log 2>&1
 done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"fused" -c 3 -f -o $O/fused \
-  python tools/g1_solve.py > $O/fused_ncu.log 2>&1
+for k in alm_fused_kernel admm_step_fused_kernel lanczos_fused_kernel; do
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -f -o $O/fused_$k \
+    python tools/g1_solve.py > $O/fused_ncu_$k.log 2>&1
+done
+timeout 300 python tools/profile_alm.py 1e6 10 20 6 822 > $O/highrank_plain.txt 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv \
+  python tools/profile_alm.py 1e6 10 6 3 822 > $O/highrank_launches.csv 2>&1
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
 tail -3 $O/bench.err
