@@ -206,3 +206,20 @@ def test_streamed_row_block_draw_matches_global_draw():
         assert np.array_equal(g1.standard_normal(5), g2.standard_normal(5))
     finally:
         driver._DRAW_CHUNK = old
+
+
+def test_memory_model_configs():
+    """DESIGN.md's per-rank memory table: configs[3] fits 8 ranks with room to escalate;
+    configs[4] fits 8 ranks at r0 for a locality-ordered graph, not for a uniformly
+    random one (its halo is the whole remote factor)."""
+    from paper_2407_15049_b200 import driver, shard
+    budget = 0.94 * 180e9
+    c3 = shard.memory_model(int(2e7), 8, 29, 0, m_global=int(2e8), nnz_a_per_con=2, halo_slots=2)
+    assert c3["total"] < budget / 4
+    assert shard.memory_model(int(2e7), 8, 150, 0, m_global=int(2e8), nnz_a_per_con=2, halo_slots=2)["total"] < budget
+    mesh = shard.memory_model(int(1.7e8), 8, 29, 7, halo_frac=0.002)
+    rand = shard.memory_model(int(1.7e8), 8, 29, 7)
+    assert mesh["total"] < budget < rand["total"]
+    assert mesh["stage_buffers"] == driver.stage_factor_buffers(8) * mesh["factor_bytes"]
+    # the driver's guard counts the same stage buffers
+    assert driver.factor_bytes_needed(100, 100, 29, 8) >= driver.stage_factor_buffers(8) * 100 * 30 * 8
