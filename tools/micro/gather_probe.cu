@@ -22,12 +22,13 @@
         }                                                                           \
     } while (0)
 
-template <int LD>
+template <int LD, int LANES = 16>
 __global__ void __launch_bounds__(256) ldg_gather(const double* __restrict__ X, const int* __restrict__ idx,
                                                    int64_t G, int ncols, double* out) {
-    const int lane = threadIdx.x & 15;
-    const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4;
-    const int64_t ngrp = (gridDim.x * (int64_t)blockDim.x) >> 4;
+    constexpr int SH = LANES == 32 ? 5 : 4;
+    const int lane = threadIdx.x & (LANES - 1);
+    const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> SH;
+    const int64_t ngrp = (gridDim.x * (int64_t)blockDim.x) >> SH;
     double2 acc = make_double2(0.0, 0.0);
     const bool act = 2 * lane < ncols;
     for (int64_t k = grp * 8; k < G; k += ngrp * 8) {
@@ -112,10 +113,10 @@ int main(int argc, char** argv) {
     double* X;
     int* idx;
     double* out;
-    CK(cudaMalloc(&X, sizeof(double) * n * 32 + 4096));
+    CK(cudaMalloc(&X, sizeof(double) * n * 52 + 4096));
     CK(cudaMalloc(&idx, sizeof(int) * G));
     CK(cudaMalloc(&out, 64));
-    CK(cudaMemset(X, 0, sizeof(double) * n * 32));
+    CK(cudaMemset(X, 0x3F, sizeof(double) * n * 52));   // non-zero data (no compression shortcuts)
     int* h = (int*)malloc(sizeof(int) * G);
     uint64_t s = 88172645463325252ull;
     for (int64_t k = 0; k < G; ++k) {
@@ -150,6 +151,9 @@ int main(int argc, char** argv) {
     run("ldg28", 224, [&] { ldg_gather<28><<<grid, 256>>>(X, idx, G, 28, out); });
     run("ldg32_26", 208, [&] { ldg_gather<32><<<grid, 256>>>(X, idx, G, 26, out); });
     run("ldg32", 256, [&] { ldg_gather<32><<<grid, 256>>>(X, idx, G, 32, out); });
+    run("ldg52", 416, [&] { ldg_gather<52, 32><<<grid, 256>>>(X, idx, G, 52, out); });
+    run("2x ldg26", 416, [&] { ldg_gather<26><<<grid, 256>>>(X, idx, G, 26, out);
+                               ldg_gather<26><<<grid, 256>>>(X + (int64_t)n * 26, idx, G, 26, out); });
     run("bulk26", 208, [&] { bulk_gather<<<nsm * 12, 128>>>(X, idx, G, out); });
     CK(cudaDeviceSynchronize());
     return 0;
