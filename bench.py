@@ -69,6 +69,18 @@ def parse():
     return ap.parse_args()
 
 
+def bench_config(n_global, n, deg, edges, r, ld, step_bytes, world=1, halo_bytes=0, graph="random",
+                 reorder=False):
+    """The line's ``config`` -- the same dict on the device arm and the reference arm for
+    the same workload."""
+    return {"workload": workload_name(n_global, deg, graph, reorder), "n": n_global, "n_per_gpu": n,
+            "edges": edges, "halo_bytes_per_spmm_per_rank": halo_bytes,
+            "rank": r, "ld": ld, "step": "BM gradient pass: SDDMM A(RR^T) + SpMM C R + fused 2 S R",
+            "bytes_per_step": step_bytes,
+            "l2": f"inputs larger than L2 (factor {n * ld * 8 / 1e9:.2f} GB >> 126 MB)",
+            "parallelism": f"rows x{world}" if world > 1 else "single GPU"}
+
+
 def workload_name(n, deg, graph="random", reorder=False):
     if graph == "delaunay":
         return (f"MaxCut Delaunay-like mesh n={n:.2e}, degree 6, scrambled labels"
@@ -196,8 +208,10 @@ def cpu_measure(n, deg, seed, budget_s, warmup=1, max_steps=None):
             if time.perf_counter() - t_all > budget_s or (max_steps and len(times) >= max_steps):
                 break
     sec = sum(times) / len(times)
+    p = st["p"]
     return dict(value=nbytes / sec / 1e9, sec=sec, steps=len(times), threads=threads,
-                bytes=nbytes, n=n)
+                bytes=nbytes, n=n, rank=st["r"], ld=st["r"] + (st["r"] & 1),
+                edges=int(np.count_nonzero(p.C.rows != p.C.cols)))
 
 
 def solver_rates(ops, dev, R, n, r, ld, n_g1, peak):
@@ -423,19 +437,18 @@ def completion_rates(dev, peak, n_total, m, seed):
 def run_reference(args, rank):
     if rank != 0:
         return
-    n_s = int(min(args.n, 2e6))
-    # one step = one bounded gradient pass (~1-2 s of CPU work at 2e6 rows)
+    n_s = int(args.n)
+    # one step = one full gradient pass of the bench workload (~2-4 s of CPU work at 1e7 rows)
     res = cpu_measure(n_s, args.deg, args.seed, budget_s=1e9, warmup=args.warmup,
                       max_steps=args.steps)
-    sample = (f"oracle/lrsdp_oracle.py gradient pass (reference alm.py:239) on the same synthetic "
-              f"family at n={n_s:.0e}, deg~{args.deg:g} (row-rate identical per row; full n=1e7 "
-              f"oracle setup alone exceeds the run budget), {res['threads']} threads over row blocks")
+    sample = (f"oracle/lrsdp_oracle.py gradient pass (reference alm.py:239) on the bench workload itself "
+              f"(n={n_s:.0e}, deg~{args.deg:g}), {res['threads']} threads over row blocks of the SpMM")
     line = {
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
         "steps": res["steps"], "warmup": args.warmup, "ms_per_step": 1e3 * res["sec"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": workload_name(args.n, args.deg), "sample_n": n_s},
+        "config": bench_config(n_s, n_s, args.deg, res["edges"], res["rank"], res["ld"], res["bytes"]),
         "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": res["threads"],
                          "kind": "port", "sample": sample},
         "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -731,13 +744,8 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded random graph, random factor/multiplier)",
-        "config": {"workload": workload_name(n_global, args.deg, args.graph, args.reorder), "n": n_global,
-                   "n_per_gpu": n,
-                   "edges": n_edges, "halo_bytes_per_spmm_per_rank": halo_bytes,
-                   "rank": r, "ld": ld, "step": "BM gradient pass: SDDMM A(RR^T) + SpMM C R + fused 2 S R",
-                   "bytes_per_step": step_bytes,
-                   "l2": f"inputs larger than L2 (factor {n * ld * 8 / 1e9:.2f} GB >> 126 MB)",
-                   "parallelism": f"rows x{world}" if world > 1 else "single GPU"},
+        "config": bench_config(n_global, n, args.deg, n_edges, r, ld, step_bytes, world, halo_bytes, args.graph,
+                               args.reorder),
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src,

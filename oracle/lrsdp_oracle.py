@@ -83,6 +83,43 @@ def _mirror(n, tag, r, c, v):
             np.concatenate([v, v[o]]))
 
 
+# Set operations of the reference's linops.py:139 compress, by explicit sorts: the same
+# arrays as np.unique / np.union1d / np.searchsorted, which on this numpy (2.3, hash-based
+# unique; random-order binary searches) take minutes at the bench's 10^7 rows.
+
+def _unique_inverse(a):
+    """np.unique(a, return_inverse=True)."""
+    a = np.asarray(a)
+    order = np.argsort(a, kind="stable")
+    s = a[order]
+    flag = np.empty(s.size, dtype=bool)
+    flag[:1] = True
+    np.not_equal(s[1:], s[:-1], out=flag[1:])
+    inv = np.empty(a.size, dtype=np.intp)
+    inv[order] = np.cumsum(flag) - 1
+    return s[flag], inv
+
+
+def _union_sorted(a, b):
+    """np.union1d(a, b)."""
+    s = np.sort(np.concatenate([np.ravel(a), np.ravel(b)]))
+    if s.size == 0:
+        return s
+    flag = np.empty(s.size, dtype=bool)
+    flag[0] = True
+    np.not_equal(s[1:], s[:-1], out=flag[1:])
+    return s[flag]
+
+
+def _searchsorted(sorted_arr, q):
+    """np.searchsorted(sorted_arr, q) with the queries visited in sorted order."""
+    q = np.asarray(q)
+    order = np.argsort(q, kind="stable")
+    out = np.empty(q.size, dtype=np.intp)
+    out[order] = np.searchsorted(sorted_arr, q[order])
+    return out
+
+
 def c_dense(p):
     M = np.zeros((p.n, p.n))
     M[p.C.rows, p.C.cols] = p.C.vals
@@ -121,7 +158,7 @@ class OracleOps:
         if dense_c is None:
             dense_c = is_dense_c(p)
         codes, cons, vals = _mirror(n, p.a_con, p.a_row, p.a_col, p.a_val)
-        uniq, colidx = np.unique(codes, return_inverse=True)
+        uniq, colidx = _unique_inverse(codes)
         self.K = len(uniq)
         self.rows = sp.csr_matrix((vals, (cons, colidx)), shape=(m, self.K))
         self.imap, self.jmap = uniq // n, uniq % n
@@ -134,11 +171,11 @@ class OracleOps:
         else:
             ccodes, _, cv = _mirror(n, np.zeros(len(p.C.vals), dtype=np.int64),
                                     p.C.rows, p.C.cols, p.C.vals)
-            sup = np.union1d(uniq, ccodes)
-            self.slot = np.searchsorted(sup, uniq)
+            sup = _union_sorted(uniq, ccodes)
+            self.slot = _searchsorted(sup, uniq)
             self.At = sp.csr_matrix((vals, (self.slot[colidx], cons)), shape=(len(sup), m))
             self.cvals = np.zeros(len(sup))
-            self.cvals[np.searchsorted(sup, ccodes)] = cv
+            self.cvals[_searchsorted(sup, ccodes)] = cv
             self.dense = None
         self.sup_i, self.sup_j = sup // n, sup % n
         self.indptr = np.zeros(n + 1, dtype=np.int64)
