@@ -395,8 +395,22 @@ __device__ __forceinline__ double group_dot_rows(const double* __restrict__ x, c
     return p;
 }
 
+// Resident CTAs per SM the constraint kernel (A(UV^T)) and the single-entry ADMM operator
+// are compiled for (a register cap). Unset: the compiler's own choice -- note that an
+// explicit minBlocks of 1 is NOT the same (it lets ptxas spend up to 86 registers).
+#ifdef CK_MINB
+#define CK_BOUNDS(NP) __launch_bounds__(NT, (NP) == 1 ? CK_MINB : 1)
+#else
+#define CK_BOUNDS(NP) __launch_bounds__(NT)
+#endif
+#ifdef SE_MINB
+#define SE_BOUNDS __launch_bounds__(NT, SE_MINB)
+#else
+#define SE_BOUNDS __launch_bounds__(NT)
+#endif
+
 template <int G, int VEC, int NP>    // NP = 1: X1 Y1 only (A(UV^T)); 3: up to three products
-__global__ void __launch_bounds__(NT) constraint_kernel(int64_t m, const int64_t* __restrict__ indptr,
+__global__ void CK_BOUNDS(NP) constraint_kernel(int64_t m, const int64_t* __restrict__ indptr,
                                                         const int32_t* __restrict__ pi,
                                                         const int32_t* __restrict__ pj,
                                                         const double* __restrict__ val, int ld,
@@ -691,7 +705,7 @@ struct DiagDev {
 // One thread per double2 of the flat n*ld factor; every thread of a row
 // recomputes the row's constraint scalars from the (read-only) m-vectors and
 // the row owner (first double2 of the row) writes ax_out and adds the m-dots.
-template <int NH>
+template <int NH, bool GOLD = true>   // GOLD false: g_old = 0 (the inner solve's first gradient)
 __global__ void __launch_bounds__(NT) diag_update_kernel(DiagDev a, double* ws, double* dots_out) {
     constexpr int ND = 7 + 2 * NH;
     double acc[ND];
@@ -728,7 +742,7 @@ __global__ void __launch_bounds__(NT) diag_update_kernel(DiagDev a, double* ws, 
         double2 g;
         g.x = 2.0 * (wa * R.x + a.scale * CR.x);
         g.y = 2.0 * (wa * R.y + a.scale * CR.y);
-        const double2 go = a.g_old != nullptr ? ld2cs(a.g_old + off) : make_double2(0.0, 0.0);   // NULL: g_old = 0
+        const double2 go = GOLD ? ld2cs(a.g_old + off) : make_double2(0.0, 0.0);
         const double2 y = make_double2(g.x - go.x, g.y - go.y);
         st2(a.g_new + off, g);
         st2(a.y + off, y);
@@ -1209,7 +1223,7 @@ void sp_dispatch_epi(const SpDev& a, const EpiDev& E, double* ws, double* dots, 
 // twice instead of being stored and re-read; dots[0] = <W, out>. One column chunk per
 // row (ld <= 2G): lanes share the slot indices by shuffles and reduce the dots.
 template <int G>
-__global__ void __launch_bounds__(NT) single_entry_apply_kernel(int64_t nrows, const int64_t* __restrict__ indptr,
+__global__ void SE_BOUNDS single_entry_apply_kernel(int64_t nrows, const int64_t* __restrict__ indptr,
                                                                 const int32_t* __restrict__ indices,
                                                                 const double* __restrict__ slot_a, int ld,
                                                                 const double* __restrict__ W,
@@ -2093,7 +2107,11 @@ int cl_diag_alm_update(const cl_diag_update_args* a, double* dots_out, double* w
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int64_t n2 = a->n * (a->ld / 2);
 #define CL_DU(NHH) diag_update_kernel<NHH><<<occ_grid((const void*)diag_update_kernel<NHH>, n2), NT, 0, st>>>(d, ws, dots_out)
-    if (a->nh == 0) CL_DU(0);
+    if (a->g_old == nullptr) {
+        if (a->nh != 0) return CL_EARG;        // the first gradient has no history
+        diag_update_kernel<0, false><<<occ_grid((const void*)diag_update_kernel<0, false>, n2), NT, 0, st>>>(
+            d, ws, dots_out);
+    } else if (a->nh == 0) CL_DU(0);
     else if (a->nh <= 4) CL_DU(4);
     else if (a->nh <= 10) CL_DU(10);
     else CL_DU(CL_MAXIN);
