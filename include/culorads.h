@@ -171,6 +171,19 @@ int cl_gather_rows(const int32_t* idx, int64_t count, int32_t ld, const double* 
 int cl_single_entry_apply(int64_t nrows, const int64_t* indptr, const int32_t* indices, const double* slot_a,
                           int32_t ld, const double* W, const double* Wf, double rho, double* out, double* dots_out,
                           double* ws, void* stream);
+/* The same operator with W and Wf interleaved in one pair buffer P (n x 2ld, row i =
+ * [W_i | Wf_i]): each slot gathers one contiguous 2ld run instead of two ld runs, which
+ * touches fewer 128-byte DRAM lines (random 208-byte rows cost 2.4 lines each, a 416-byte
+ * pair 3.9; tools/micro/gather_probe.cu). Same arithmetic, same thread mapping:
+ * bit-identical to cl_single_entry_apply. */
+int cl_single_entry_apply_pair(int64_t nrows, const int64_t* indptr, const int32_t* indices, const double* slot_a,
+                               int32_t ld, const double* P, double rho, double* out, double* dots_out, double* ws,
+                               void* stream);
+/* P[i, half*ld : (half+1)*ld] = X[i, :] for a pair buffer P (n x 2ld). */
+int cl_pair_pack(int64_t n, int32_t ld, const double* X, double* P, int32_t half, void* stream);
+/* CG direction update of the pair path: p = r + beta p (cl_lincomb's arithmetic), written
+ * to p (n x ld) and to P's first half. */
+int cl_cg_direction_pair(int64_t n, int32_t ld, double beta, const double* r, double* p, double* P, void* stream);
 
 /* Fused SpMM passes of the ADMM step for diagonal constraints:
  *   cl_diag_admm_cg_init: rhs = -scale C Wf + rho Wf + diag(a nlam) Wf (admm.py:52,

@@ -56,7 +56,7 @@ def barrier_timeout(rc, what):
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint_eval_halo",
            "cl_diag_constraint_eval", "cl_sddmm",
            "cl_gather_rows", "cl_diag_cg_apply", "cl_diag_cg_apply_rows", "cl_diag_cg_step", "cl_cg_step", "cl_cg_step_dev", "cl_admm_step_diag", "cl_admm_step_diag_fused", "cl_alm_inner_diag", "cl_alm_inner_diag_fused",
-           "cl_diag_admm_cg_init", "cl_diag_admm_step_end", "cl_diag_admm_step_end_rows", "cl_single_entry_apply", "cl_lanczos_loop", "cl_lanczos_loop_fused",
+           "cl_diag_admm_cg_init", "cl_diag_admm_step_end", "cl_diag_admm_step_end_rows", "cl_single_entry_apply", "cl_single_entry_apply_pair", "cl_pair_pack", "cl_cg_direction_pair", "cl_lanczos_loop", "cl_lanczos_loop_fused",
            "cl_pattern_assemble", "cl_lanczos_update",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
            "cl_set_l2_fetch_granularity", "cl_get_l2_fetch_granularity", "cl_version", "cl_device_ok")
@@ -172,6 +172,9 @@ def _declare(lib):
     lib.cl_diag_admm_step_end_rows.argtypes = [I64, I32, P, P, P, P, P, P, D, P, P, P, P, P]
     lib.cl_diag_admm_step_end.argtypes = [ctypes.POINTER(Pattern), P, P, I32, P, P, P, D, P, P, P, P, P]
     lib.cl_single_entry_apply.argtypes = [I64, P, P, P, I32, P, P, D, P, P, P, P]
+    lib.cl_single_entry_apply_pair.argtypes = [I64, P, P, P, I32, P, D, P, P, P, P]
+    lib.cl_pair_pack.argtypes = [I64, I32, P, P, I32, P]
+    lib.cl_cg_direction_pair.argtypes = [I64, I32, D, P, P, P, P]
     lib.cl_pattern_assemble.argtypes = [ctypes.POINTER(Pattern), P, P]
     lib.cl_lanczos_loop.argtypes = [ctypes.POINTER(LanczosArgs), ctypes.POINTER(I32)]
     lib.cl_lanczos_loop_fused.argtypes = [ctypes.POINTER(LanczosArgs), ctypes.POINTER(I32)]

@@ -120,9 +120,21 @@ class HalfStep:
         if rnorm <= eps:
             return 0, rnorm
         dev.lincomb(p, [r], [1.0])
+        apat = self.ops.adj.apat
+        # single-entry constraints: the CG direction and Wf share one pair buffer [p_i | Wf_i],
+        # so each operator slot gathers one 2 ld run (bit-identical to the two-operand kernel)
+        pair = (PAIR and apat.single_a is not None and apat.halo is None and self.ld <= 64)
+        if pair:
+            if getattr(self, "P2", None) is None:
+                self.P2 = dev.empty(self.n, 2 * self.ld)
+            dev.pair_pack(Wf, self.ld, self.P2, 1)
+            dev.pair_pack(p, self.ld, self.P2, 0)
         its = 0
         for k in range(max_iter):
-            self.apply(p, Wf, rho, Q, dot_with=p, at=A + 1)
+            if pair:
+                dev.single_entry_apply_pair(apat, self.ld, self.P2, rho, Q, at=A + 1)
+            else:
+                self.apply(p, Wf, rho, Q, dot_with=p, at=A + 1)
             if dev.world == 1:
                 # x += alpha p; r -= alpha Q; <r, r> with alpha = qr / <p, Q> taken on the device,
                 # so <p, Q> and <r, r> come back in one read (a rejected curvature skips the update)
@@ -144,7 +156,10 @@ class HalfStep:
             its = k + 1
             if rnorm <= eps:
                 break
-            dev.lincomb(p, [r, p], [1.0, qn / qr])
+            if pair:
+                dev.cg_direction_pair(self.ld, qn / qr, r, p, self.P2)
+            else:
+                dev.lincomb(p, [r, p], [1.0, qn / qr])
             qr = qn
         dev.lincomb(None, [x], [0.0], dots=[(0, 0)], at=A + 3)
         if not math.isfinite(float(dev.fetch(A + 4)[A + 3])):
@@ -319,6 +334,8 @@ def _resid(ops, ax, res, at):
     ops.dev.lincomb(res, [ax, ops.b], [1.0, -1.0], dots=[("out", "out")], at=at)
 
 
+# single-entry constraints: CG operator on the pair buffer [p | Wf] (cl_single_entry_apply_pair)
+PAIR = os.environ.get("CULORADS_PAIR", "1") != "0"
 NATIVE = True     # diagonal constraints: run the step's control flow in C++ (row-sharded: with hooks)
 # Problems with at most this many row-lanes (n times the lanes that share a factor row,
 # lanes_for(ld)) run each ADMM step as one cooperative launch (cl_admm_step_diag_fused):

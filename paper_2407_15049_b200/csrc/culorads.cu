@@ -1222,6 +1222,9 @@ void sp_dispatch_epi(const SpDev& a, const EpiDev& E, double* ws, double* dots, 
 // association on both rows of c, so each constraint value is computed bit-identically
 // twice instead of being stored and re-read; dots[0] = <W, out>. One column chunk per
 // row (ld <= 2G): lanes share the slot indices by shuffles and reduce the dots.
+// ``sw``: row stride of W and Wf -- ld for separate factors, 2 ld for a pair buffer
+// [W_i | Wf_i] (cl_single_entry_apply_pair), where one 16-byte-aligned 2 ld run per row holds
+// both gathered operands (fewer 128-byte DRAM lines per slot, tools/micro/gather_probe.cu).
 template <int G>
 __global__ void SE_BOUNDS single_entry_apply_kernel(int64_t nrows, const int64_t* __restrict__ indptr,
                                                                 const int32_t* __restrict__ indices,
@@ -1229,7 +1232,7 @@ __global__ void SE_BOUNDS single_entry_apply_kernel(int64_t nrows, const int64_t
                                                                 const double* __restrict__ W,
                                                                 const double* __restrict__ Wf, double rho,
                                                                 double* __restrict__ out, double* ws,
-                                                                double* dots_out) {
+                                                                double* dots_out, int64_t sw) {
     double dacc[1] = {0.0};
     const int lane = threadIdx.x & 31;
     const int gl = lane % G;
@@ -1240,8 +1243,8 @@ __global__ void SE_BOUNDS single_entry_apply_kernel(int64_t nrows, const int64_t
     const double2 zr = make_double2(0.0, 0.0);
     for (int64_t row = ((int64_t)blockIdx.x * NT + threadIdx.x) / G; row < nrows; row += groups_total) {
         const int64_t s0 = __ldg(indptr + row), s1 = __ldg(indptr + row + 1);
-        const double2 wi = active ? ld2(W + row * ld + col) : zr;
-        const double2 fi = active ? ld2(Wf + row * ld + col) : zr;
+        const double2 wi = active ? ld2(W + row * sw + col) : zr;
+        const double2 fi = active ? ld2(Wf + row * sw + col) : zr;
         double2 acc = zr;
         for (int64_t base = s0; base < s1; base += G) {
             const int64_t s = base + gl;
@@ -1255,8 +1258,8 @@ __global__ void SE_BOUNDS single_entry_apply_kernel(int64_t nrows, const int64_t
             for (int u = 0; u < cnt; ++u) {
                 const int j = __shfl_sync(gmask, jj, (lane - gl) + u);
                 const double av = __shfl_sync(gmask, aa, (lane - gl) + u);
-                const double2 wj = active ? ld2(W + (int64_t)j * ld + col) : zr;
-                const double2 fj = active ? ld2(Wf + (int64_t)j * ld + col) : zr;
+                const double2 wj = active ? ld2(W + (int64_t)j * sw + col) : zr;
+                const double2 fj = active ? ld2(Wf + (int64_t)j * sw + col) : zr;
                 const bool lo_is_i = row <= j;
                 double t1 = dot2(lo_is_i ? wi : wj, lo_is_i ? fj : fi);   // W_lo . Wf_hi
                 double t2 = dot2(lo_is_i ? wj : wi, lo_is_i ? fi : fj);   // W_hi . Wf_lo
@@ -1538,6 +1541,60 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
+
+namespace {
+int single_entry_launch(int64_t nrows, const int64_t* indptr, const int32_t* indices, const double* slot_a,
+                        int32_t ld, const double* W, const double* Wf, int64_t sw, double rho, double* out,
+                        double* dots_out, double* ws, void* stream) {
+    if (nrows < 0 || ld < 2 || (ld & 1) || ld > 64 || indptr == nullptr || W == nullptr || Wf == nullptr ||
+        out == nullptr || dots_out == nullptr || ws == nullptr)
+        return CL_EARG;
+    if (!aligned16(W) || !aligned16(Wf) || !aligned16(out)) return CL_EARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (nrows == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double), st);
+    const int G = ld <= 2 ? 1 : ld <= 4 ? 2 : ld <= 8 ? 4 : ld <= 16 ? 8 : ld <= 32 ? 16 : 32;
+    const int grid = red_grid(nrows * G);
+#define CL_SE(GG) single_entry_apply_kernel<GG><<<grid, NT, 0, st>>>(nrows, indptr, indices, slot_a, ld, W, Wf, rho, \
+                                                                   out, ws, dots_out, sw)
+    switch (G) {
+        case 1: CL_SE(1); break;
+        case 2: CL_SE(2); break;
+        case 4: CL_SE(4); break;
+        case 8: CL_SE(8); break;
+        case 16: CL_SE(16); break;
+        default: CL_SE(32); break;
+    }
+#undef CL_SE
+    return (int)cudaGetLastError();
+}
+
+// Pair buffer rows: P[i, half*ld : half*ld+ld] = X[i, :]   (flat row-major n x ld source)
+__global__ void __launch_bounds__(NT) pair_pack_kernel(int64_t n, int h2, const double* __restrict__ X,
+                                                       double* __restrict__ P, int half) {
+    const int64_t total = n * h2;
+    for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < total; k += (int64_t)gridDim.x * NT) {
+        const int64_t i = k / h2;
+        const int q = (int)(k - i * h2);
+        st2(P + 2 * (i * 2 * h2 + half * h2 + q), ld2cs(X + 2 * k));
+    }
+}
+
+// CG direction update of the pair path: p = r + beta p (cl_lincomb's arithmetic:
+// fma(beta, p, fma(1, r, 0))), written to p and to the pair buffer's first half
+__global__ void __launch_bounds__(NT) cg_direction_pair_kernel(int64_t n, int h2, double beta,
+                                                               const double* __restrict__ r, double* __restrict__ p,
+                                                               double* __restrict__ P) {
+    const int64_t total = n * h2;
+    for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < total; k += (int64_t)gridDim.x * NT) {
+        const int64_t i = k / h2;
+        const int q = (int)(k - i * h2);
+        double2 o = axpy2(1.0, ld2cs(r + 2 * k), make_double2(0.0, 0.0));
+        o = axpy2(beta, ld2cs(p + 2 * k), o);
+        st2(p + 2 * k, o);
+        st2(P + 2 * (i * 2 * h2 + q), o);
+    }
+}
+}  // namespace
 
 extern "C" {
 
@@ -2038,25 +2095,39 @@ int cl_diag_admm_step_end_rows(int64_t n, int32_t ld, const double* CU, const do
     return (int)cudaGetLastError();
 }
 
+
 int cl_single_entry_apply(int64_t nrows, const int64_t* indptr, const int32_t* indices, const double* slot_a,
                           int32_t ld, const double* W, const double* Wf, double rho, double* out, double* dots_out,
                           double* ws, void* stream) {
-    if (nrows < 0 || ld < 2 || (ld & 1) || ld > 64 || indptr == nullptr || W == nullptr || Wf == nullptr ||
-        out == nullptr || dots_out == nullptr || ws == nullptr)
-        return CL_EARG;
-    if (!aligned16(W) || !aligned16(Wf) || !aligned16(out)) return CL_EARG;
+    return single_entry_launch(nrows, indptr, indices, slot_a, ld, W, Wf, ld, rho, out, dots_out, ws, stream);
+}
+
+int cl_single_entry_apply_pair(int64_t nrows, const int64_t* indptr, const int32_t* indices, const double* slot_a,
+                               int32_t ld, const double* P, double rho, double* out, double* dots_out, double* ws,
+                               void* stream) {
+    if (P == nullptr) return CL_EARG;
+    return single_entry_launch(nrows, indptr, indices, slot_a, ld, P, P + ld, 2 * (int64_t)ld, rho, out, dots_out,
+                               ws, stream);
+}
+
+int cl_pair_pack(int64_t n, int32_t ld, const double* X, double* P, int32_t half, void* stream) {
+    if (n < 0 || ld < 2 || (ld & 1) || (half != 0 && half != 1) || X == nullptr || P == nullptr) return CL_EARG;
+    if (!aligned16(X) || !aligned16(P)) return CL_EARG;
+    if (n == 0) return CL_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (nrows == 0) return (int)cudaMemsetAsync(dots_out, 0, sizeof(double), st);
-    const int G = ld <= 2 ? 1 : ld <= 4 ? 2 : ld <= 8 ? 4 : ld <= 16 ? 8 : ld <= 32 ? 16 : 32;
-    const int grid = red_grid(nrows * G);
-    switch (G) {
-        case 1: single_entry_apply_kernel<1><<<grid, NT, 0, st>>>(nrows, indptr, indices, slot_a, ld, W, Wf, rho, out, ws, dots_out); break;
-        case 2: single_entry_apply_kernel<2><<<grid, NT, 0, st>>>(nrows, indptr, indices, slot_a, ld, W, Wf, rho, out, ws, dots_out); break;
-        case 4: single_entry_apply_kernel<4><<<grid, NT, 0, st>>>(nrows, indptr, indices, slot_a, ld, W, Wf, rho, out, ws, dots_out); break;
-        case 8: single_entry_apply_kernel<8><<<grid, NT, 0, st>>>(nrows, indptr, indices, slot_a, ld, W, Wf, rho, out, ws, dots_out); break;
-        case 16: single_entry_apply_kernel<16><<<grid, NT, 0, st>>>(nrows, indptr, indices, slot_a, ld, W, Wf, rho, out, ws, dots_out); break;
-        default: single_entry_apply_kernel<32><<<grid, NT, 0, st>>>(nrows, indptr, indices, slot_a, ld, W, Wf, rho, out, ws, dots_out); break;
-    }
+    const int64_t work = n * (ld / 2);
+    pair_pack_kernel<<<occ_grid((const void*)pair_pack_kernel, work), NT, 0, st>>>(n, ld / 2, X, P, half);
+    return (int)cudaGetLastError();
+}
+
+int cl_cg_direction_pair(int64_t n, int32_t ld, double beta, const double* r, double* p, double* P, void* stream) {
+    if (n < 0 || ld < 2 || (ld & 1) || r == nullptr || p == nullptr || P == nullptr) return CL_EARG;
+    if (!aligned16(r) || !aligned16(p) || !aligned16(P)) return CL_EARG;
+    if (n == 0) return CL_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t work = n * (ld / 2);
+    cg_direction_pair_kernel<<<occ_grid((const void*)cg_direction_pair_kernel, work), NT, 0, st>>>(n, ld / 2, beta, r,
+                                                                                                    p, P);
     return (int)cudaGetLastError();
 }
 

@@ -260,6 +260,26 @@ class Device:
         self.launches += 1
         check(rc, "cl_single_entry_apply")
 
+    def single_entry_apply_pair(self, apat, ld, P2, rho, out, at=0):
+        """single_entry_apply with W and Wf interleaved in the pair buffer P2 (n x 2ld)."""
+        rc = self.lib.cl_single_entry_apply_pair(int(apat.nrows), ptr(apat.indptr), ptr(apat.indices),
+                                                 ptr(apat.single_a), int(ld), ptr(P2), float(rho), ptr(out),
+                                                 self.slot(at), ptr(self.ws), self.sp)
+        self.launches += 1
+        check(rc, "cl_single_entry_apply_pair")
+
+    def pair_pack(self, X, ld, P2, half):
+        """P2[:, half*ld:(half+1)*ld] = X."""
+        rc = self.lib.cl_pair_pack(int(X.shape[0]), int(ld), ptr(X), ptr(P2), int(half), self.sp)
+        self.launches += 1
+        check(rc, "cl_pair_pack")
+
+    def cg_direction_pair(self, ld, beta, r, p, P2):
+        """p = r + beta p, also into P2's first half."""
+        rc = self.lib.cl_cg_direction_pair(int(p.shape[0]), int(ld), float(beta), ptr(r), ptr(p), ptr(P2), self.sp)
+        self.launches += 1
+        check(rc, "cl_cg_direction_pair")
+
     def cg_step_dev(self, qr, pq_at, x_in, x_out, p, r, Q, at=0):
         """x_out = x_in + alpha p; r -= alpha Q with alpha = qr / slab[pq_at] on the device;
         <r, r> -> slab[at] (update skipped for a non-finite or non-positive curvature)."""

@@ -269,6 +269,66 @@ def test_single_entry_apply_matches_generic_operator(dev, r):
     assert abs(d_fused - d_gen) <= 1e-12 * (1 + abs(d_gen))
 
 
+@pytest.mark.parametrize("r", [3, 8, 25, 50])
+def test_single_entry_pair_buffer_bit_identical(dev, r):
+    """cl_single_entry_apply_pair on the pair buffer [W | Wf] (cl_pair_pack) equals the
+    two-operand kernel bit for bit, output and <W, out>; cl_cg_direction_pair equals the
+    lincomb p = r + beta p and mirrors it into the pair buffer."""
+    import torch
+    from paper_2407_15049_b200 import admm, graphs, linops, problem
+    from paper_2407_15049_b200.device import padded_ld
+    p = problem.build_matrix_completion(graphs.random_completion(400, 350, 9000, seed=r))
+    ops = linops.build_operators(p)
+    apat = ops.adj.apat
+    ld = padded_ld(r)
+    rng = np.random.default_rng(r)
+    W = linops.to_factor(rng.standard_normal((p.n, r)), dev, ld)
+    Wf = linops.to_factor(rng.standard_normal((p.n, r)), dev, ld)
+    a, b = torch.empty_like(W), torch.empty_like(W)
+    dev.single_entry_apply(apat, ld, W, Wf, 1.3, a, at=30)
+    da = float(dev.fetch(31)[30])
+    P2 = dev.empty(p.n, 2 * ld)
+    dev.pair_pack(W, ld, P2, 0)
+    dev.pair_pack(Wf, ld, P2, 1)
+    assert torch.equal(P2[:, :ld], W) and torch.equal(P2[:, ld:], Wf)
+    dev.single_entry_apply_pair(apat, ld, P2, 1.3, b, at=30)
+    db = float(dev.fetch(31)[30])
+    assert a.cpu().numpy().tobytes() == b.cpu().numpy().tobytes() and da == db
+    rr = linops.to_factor(rng.standard_normal((p.n, r)), dev, ld)
+    p1, p2 = W.clone(), W.clone()
+    dev.lincomb(p1, [rr, p1], [1.0, 0.37])
+    dev.cg_direction_pair(ld, 0.37, rr, p2, P2)
+    assert torch.equal(p1, p2) and torch.equal(P2[:, :ld], p2) and torch.equal(P2[:, ld:], Wf)
+
+
+def test_pair_cg_matches_two_operand_cg(dev):
+    """A whole completion half-step CG on the pair buffer: the same iterates, residuals and
+    iteration count as the two-operand path (admm.PAIR off)."""
+    from paper_2407_15049_b200 import admm, alm, graphs, linops, problem
+    from paper_2407_15049_b200.device import padded_ld
+    p = problem.build_matrix_completion(graphs.random_completion(500, 400, 12000, seed=9))
+    ops = linops.build_operators(p)
+    r = 12
+    ld = padded_ld(r)
+    rng = np.random.default_rng(3)
+    U = linops.to_factor(rng.standard_normal((p.n, r)) / 20, dev, ld)
+    V = linops.to_factor(rng.standard_normal((p.n, r)) / 20, dev, ld)
+    out = []
+    for pair in (True, False):
+        admm.PAIR = pair
+        try:
+            st = admm.AdmmState(U=U.clone(), V=V.clone(), dual=alm.DualVector(lam=dev.zeros(p.m), rho=2.0), r=r)
+            hs = admm.HalfStep(ops, p.n, ld)
+            stats = [admm.admm_step(st, ops, hs=hs) for _ in range(3)]
+        finally:
+            admm.PAIR = True
+        out.append((st.U.cpu().numpy(), st.V.cpu().numpy(), [(s.cg_iters_u, s.cg_iters_v, s.resid_u, s.resid_v)
+                                                             for s in stats]))
+    (u1, v1, s1), (u2, v2, s2) = out
+    assert sum(a + b for a, b, _, _ in s1) > 0          # the CGs iterate
+    assert s1 == s2 and u1.tobytes() == u2.tobytes() and v1.tobytes() == v2.tobytes()
+
+
 def test_single_entry_detection_rejects_general_constraints(dev):
     from paper_2407_15049_b200 import linops
     from tests._golden import load, problem_from

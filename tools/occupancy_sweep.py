@@ -16,7 +16,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "variants_so")     # travels to the GPU box (not in .gpurunignore); *.so git-ignored
 VARIANTS = {
     "base": [],
+    "ck5_se5": ["-DCK_MINB=5", "-DSE_MINB=5"],
     "ck6_se6": ["-DCK_MINB=6", "-DSE_MINB=6"],
+    "ck7": ["-DCK_MINB=7"],
     "ck8_se8": ["-DCK_MINB=8", "-DSE_MINB=8"],
     "sp5": ["-DSP_MINB0=5"],
     "sp6": ["-DSP_MINB0=6"],
@@ -69,6 +71,16 @@ def one(tag):
     hs = admm.HalfStep(ops, p.n, ld)
     res["A(UV^T)_ms"] = timeit(dev, lambda: dev.constraint_eval(ops.cop.con, ld, U, V, y))
     res["single_entry_apply_ms"] = timeit(dev, lambda: hs.apply(U, V, 1.5, out, dot_with=U, at=0))
+    if hasattr(dev.lib, "cl_single_entry_apply_pair"):
+        P2 = dev.empty(p.n, 2 * ld)
+        dev.pair_pack(U, ld, P2, 0)
+        dev.pair_pack(V, ld, P2, 1)
+        res["single_entry_apply_pair_ms"] = timeit(
+            dev, lambda: dev.single_entry_apply_pair(ops.adj.apat, ld, P2, 1.5, out, at=0))
+        res["pair_pack_ms"] = timeit(dev, lambda: dev.pair_pack(U, ld, P2, 0))
+        del P2
+    res["A(RD+DR, DD)_line_search_ms"] = timeit(dev, lambda: dev.constraint_eval(ops.cop.con, ld, U, V, y, X2=V, Y2=U,
+                                                                               X3=V, Y3=V, out2=out.view(-1)[:p.m]))
     del ops, hs, U, V, y, out
     torch.cuda.empty_cache()
     # MaxCut C R at configs[2]
