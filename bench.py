@@ -396,6 +396,9 @@ def completion_rates(dev, peak, n_total, m, seed):
     om = ops.adj.omega
     apat = ops.adj.apat
     hs = admm.HalfStep(ops, p.n, ld)
+    P2 = dev.empty(p.n, 2 * ld)
+    dev.pair_pack(U, ld, P2, 0)
+    dev.pair_pack(V, ld, P2, 1)
     kern = {}
     for name, fn, nbytes in (
             ("constraint_eval A(UV^T)", lambda: dev.constraint_eval(con, ld, U, V, y),
@@ -403,7 +406,11 @@ def completion_rates(dev, peak, n_total, m, seed):
             ("adjoint SpMM (C + A*(lam)) V", lambda: dev.spmm(om, V, ld, out=out, c_coeff=1.0, w1=lam),
              RL.pattern_spmm_bytes(p.n, om.nnz, ld, at_entries=int(om.at_con.numel()) if om.at_con is not None
                                    else 0)),
-            ("ADMM operator (single-entry fused)", lambda: hs.apply(U, V, 1.5, out, dot_with=U, at=0),
+            ("ADMM operator (single-entry fused, two operands)", lambda: hs.apply(U, V, 1.5, out, dot_with=U, at=0),
+             p.n * (RL.I8 + 3 * ld * RL.F8) + apat.nnz * (RL.I4 + RL.F8 + 2 * ld * RL.F8)),
+            # what the CG runs: p and Wf interleaved in one pair buffer (same algorithmic bytes)
+            ("ADMM operator (single-entry fused, pair buffer: the CG's)",
+             lambda: dev.single_entry_apply_pair(apat, ld, P2, 1.5, out, at=0),
              p.n * (RL.I8 + 3 * ld * RL.F8) + apat.nnz * (RL.I4 + RL.F8 + 2 * ld * RL.F8))):
         ms = timeit(fn)
         gbs = nbytes / (ms * 1e-3) / 1e9
