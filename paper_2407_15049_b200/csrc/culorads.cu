@@ -142,13 +142,15 @@ struct LcDev {
 };
 
 // MODE 0: up to 7 inputs, <= 8 arbitrary pair dots (operand 7 = out)
-// MODE 1: up to CL_MAXIN inputs, dots out·in[j] (j < nin) then out·out
-// MODE 2: up to CL_MAXIN inputs (no out), dots in0·in[j] (j < nin) then in1·in[j] (1 <= j < nin)
-template <int MODE>
+// MODE 1: up to KIN inputs, dots out·in[j] (j < nin) then out·out (at nin)
+// MODE 2: up to KIN inputs (no out), dots in0·in[j] (j < nin) then in1·in[j] (1 <= j < nin)
+// KIN is the input capacity the instance is compiled for (the host picks the smallest that
+// holds nin): every input and accumulator lives in registers, so capacity costs occupancy --
+// a 20-input instance needs 191 registers (one CTA per SM), a 2-input one 40.
+template <int MODE, int KIN = (MODE == 0 ? 7 : CL_MAXIN)>
 __global__ void __launch_bounds__(NT) lincomb_kernel(LcDev a, int64_t n2, int tail, double* ws,
                                                      double* dots_out) {
-    constexpr int KIN = MODE == 0 ? 7 : CL_MAXIN;
-    constexpr int ND = MODE == 0 ? 8 : (MODE == 1 ? CL_MAXIN + 1 : 2 * CL_MAXIN - 1);
+    constexpr int ND = MODE == 0 ? 8 : (MODE == 1 ? KIN + 1 : 2 * KIN - 1);
     double acc[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) acc[d] = 0.0;
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(NT) lincomb_kernel(LcDev a, int64_t n2, int ta
 #pragma unroll
             for (int j = 0; j < KIN; ++j)
                 if (j < nin) acc[j] += dot2(o, v[j]);
-            acc[ND - 1] += dot2(o, o);
+            acc[KIN] += dot2(o, o);
         } else {
 #pragma unroll
             for (int j = 0; j < KIN; ++j)
@@ -201,8 +203,22 @@ __global__ void __launch_bounds__(NT) lincomb_kernel(LcDev a, int64_t n2, int ta
                 if (j < nin) acc[KIN + j - 1] += dot2(v[1], v[j]);
         }
     }
-    // MODE 2 output layout is fixed: [j] = in0·in_j, [CL_MAXIN + j - 1] = in1·in_j
-    if (a.ndot > 0) reduce_and_finish<ND>(acc, a.ndot, ws, dots_out);
+    if (a.ndot > 0) {
+        if (MODE == 1) {
+            // out·out sits after the nin input dots: move it there (unused slots hold 0)
+            if (nin < KIN) {
+#pragma unroll
+                for (int j = 0; j < KIN; ++j)
+                    if (j == nin) acc[j] = acc[KIN];
+            }
+            reduce_and_finish<ND>(acc, a.ndot, ws, dots_out);
+        } else if (MODE == 2) {
+            // fixed output layout: [j] = in0·in_j, [CL_MAXIN + j - 1] = in1·in_j
+            reduce_and_finish<ND>(acc, a.ndot, ws, dots_out, KIN, CL_MAXIN - KIN);
+        } else {
+            reduce_and_finish<ND>(acc, a.ndot, ws, dots_out);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -401,7 +417,10 @@ __device__ __forceinline__ double group_dot_rows(const double* __restrict__ x, c
 #ifndef CK_MINB
 #define CK_MINB 6           // A(UV^T): 40 registers, 6 CTAs/SM: 5.77 -> 4.49 ms at configs[3]'s share
 #endif
-#define CK_BOUNDS(NP) __launch_bounds__(NT, (NP) == 1 ? CK_MINB : 0)   // 0: the compiler's choice
+#ifndef CK3_MINB
+#define CK3_MINB 0          // the line search's three-product variant: the compiler's choice
+#endif
+#define CK_BOUNDS(NP) __launch_bounds__(NT, (NP) == 1 ? CK_MINB : CK3_MINB)   // 0: the compiler's choice
 #ifdef SE_MINB
 #define SE_BOUNDS __launch_bounds__(NT, SE_MINB)
 #else
@@ -623,6 +642,9 @@ __global__ void __launch_bounds__(NT, 4) diag_constraint_kernel(DiagCon a) {
 #define CL_SMALLN 1         // small problems: spread rows over at least FLAT_MIN_BLK blocks / one tile per CTA
 #endif
 #define FLAT_MIN_BLK (2 * NSM)
+#ifndef DCF_MAXH2
+#define DCF_MAXH2 32        // widest row (double2 units) the flat diagonal-constraint kernel takes
+#endif
 
 // Rows per block iteration of the flat row kernels: NT*DC_U double2 units, or fewer when
 // that would leave SMs idle (small n), so every SM has work and each thread few units.
@@ -1647,10 +1669,15 @@ int cl_lincomb(const cl_lincomb_args* args, int64_t N, double* dots_out, double*
     if (mode < 0 || mode > 2) return CL_EARG;
     if (mode == 0 && args->ndot == 0 && args->nin > 7) mode = 1;   // plain wide combination
     if (mode == 0 && (args->nin > 7 || args->ndot > 8)) return CL_EARG;
+    // input capacity of the instance (registers scale with it)
+    const int nin = args->nin;
+    const int kin = nin <= 2 ? 2 : nin <= 4 ? 4 : nin <= 8 ? 8 : nin <= 12 ? 12 : nin <= 17 ? 17 : CL_MAXIN;
     if (mode == 1) d.ndot = args->ndot > 0 ? args->nin + 1 : 0;
     if (mode == 2) {
         if (args->out != nullptr || args->nin < 2) return CL_EARG;
-        d.ndot = args->ndot > 0 ? 2 * CL_MAXIN - 1 : 0;
+        d.ndot = args->ndot > 0 ? 2 * kin - 1 : 0;
+        if (d.ndot > 0) cudaMemsetAsync(dots_out, 0, sizeof(double) * (2 * CL_MAXIN - 1),
+                                        reinterpret_cast<cudaStream_t>(stream));   // the unused layout slots
     }
     if (d.ndot > 0 && (dots_out == nullptr || ws == nullptr)) return CL_EARG;
     const int64_t n2 = N / 2;
@@ -1660,17 +1687,32 @@ int cl_lincomb(const cl_lincomb_args* args, int64_t N, double* dots_out, double*
         return CL_OK;
     }
     switch (mode) {
+#define CL_LC(M, K) lincomb_kernel<M, K><<<occ_grid((const void*)lincomb_kernel<M, K>, n2 + tail), NT, 0, st>>>( \
+    d, n2, tail, ws, dots_out)
         case 0:
-            lincomb_kernel<0><<<occ_grid((const void*)lincomb_kernel<0>, n2 + tail), NT, 0, st>>>(d, n2, tail, ws,
-                                                                                                   dots_out);
+            if (nin <= 3) CL_LC(0, 3);
+            else CL_LC(0, 7);
             break;
         case 1:
-            lincomb_kernel<1><<<occ_grid((const void*)lincomb_kernel<1>, n2 + tail), NT, 0, st>>>(d, n2, tail, ws,
-                                                                                                   dots_out);
+            switch (kin) {
+                case 2: CL_LC(1, 2); break;
+                case 4: CL_LC(1, 4); break;
+                case 8: CL_LC(1, 8); break;
+                case 12: CL_LC(1, 12); break;
+                case 17: CL_LC(1, 17); break;
+                default: CL_LC(1, CL_MAXIN); break;
+            }
             break;
         default:
-            lincomb_kernel<2><<<occ_grid((const void*)lincomb_kernel<2>, n2 + tail), NT, 0, st>>>(d, n2, tail, ws,
-                                                                                                   dots_out);
+            switch (kin) {
+                case 2:
+                case 4: CL_LC(2, 4); break;
+                case 8: CL_LC(2, 8); break;
+                case 12: CL_LC(2, 12); break;
+                case 17: CL_LC(2, 17); break;
+                default: CL_LC(2, CL_MAXIN); break;
+            }
+#undef CL_LC
             break;
     }
     return (int)cudaGetLastError();
@@ -1875,7 +1917,9 @@ int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const dou
         }
         d.pidx[k] = f;
     }
-    if (ld >= 2 && ld / 2 <= NT * DC_U && aligned16(X1) && aligned16(Y1) && (X2 == nullptr || aligned16(X2)) &&
+    // flat rows while a row's fold is short (one thread folds a row's ld/2 unit products);
+    // wide rows (high rank) go to the lane-group kernel: a warp per row, a shuffle tree
+    if (ld >= 2 && ld / 2 <= DCF_MAXH2 && aligned16(X1) && aligned16(Y1) && (X2 == nullptr || aligned16(X2)) &&
         (Y2 == nullptr || aligned16(Y2)) && (X3 == nullptr || aligned16(X3)) && (Y3 == nullptr || aligned16(Y3))) {
         const int rb = flat_rows(n, ld / 2);
         const int64_t nblk = (n + rb - 1) / rb;

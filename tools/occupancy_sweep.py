@@ -20,6 +20,8 @@ VARIANTS = {
     "ck6_se6": ["-DCK_MINB=6", "-DSE_MINB=6"],
     "ck7": ["-DCK_MINB=7"],
     "ck8_se8": ["-DCK_MINB=8", "-DSE_MINB=8"],
+    "ck3_4": ["-DCK3_MINB=4"],
+    "ck3_5": ["-DCK3_MINB=5"],
     "sp5": ["-DSP_MINB0=5"],
     "sp6": ["-DSP_MINB0=6"],
 }

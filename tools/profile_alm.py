@@ -40,6 +40,8 @@ print(f"n={n} r={r} ld={ld}: {res.iterations} ALM inner iterations in {dt:.3f}s 
       f"{1e3 * dt / max(res.iterations, 1):.2f} ms/iter, {(dev.launches - l0) / max(res.iterations, 1):.1f} launches/iter",
       flush=True)
 if steps:
+    del core, res
+    torch.cuda.empty_cache()
     st = admm.AdmmState(U=R.clone(), V=R.clone(), dual=dual, r=r)
     hs = admm.HalfStep(ops, n, ld)
     pool = admm._Pool(dev, n, ld)
