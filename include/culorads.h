@@ -240,6 +240,14 @@ int cl_diag_cg_step(int64_t n, int32_t ld, double rho, const double* coef, const
 /* cl_constraint_eval for a row block of a row-sharded solve: factor row
  * index >= nown of operand k (X1, Y1, X2, Y2, X3, Y3) reads ghosts[k][row-nown]
  * (the halo rows gathered from the other ranks). */
+/* The line search's products (alm.py:153-154) with R and D interleaved in one pair buffer
+ * P (n x 2ld, row i = [R_i | D_i]): out1 = A(R D^T + D R^T), out2 = A(D D^T) -- the
+ * cl_constraint_eval call with X1=R, Y1=D, X2=D, Y2=R, X3=Y3=D, bit for bit, with each
+ * position's rows gathered as one 2ld run (fewer 128-byte DRAM lines). */
+int cl_constraint_eval_pair(int64_t m, const int64_t* indptr, const int32_t* pi, const int32_t* pj,
+                            const double* val, int32_t ld, const double* P, double* out1, double* out2,
+                            void* stream);
+
 int cl_constraint_eval_halo(int64_t m, const int64_t* indptr, const int32_t* pi, const int32_t* pj,
                             const double* val, int32_t ld, const double* X1, const double* Y1, const double* X2,
                             const double* Y2, double* out1, const double* X3, const double* Y3, double* out2,

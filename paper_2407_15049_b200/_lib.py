@@ -53,7 +53,7 @@ def barrier_timeout(rc, what):
                   RuntimeWarning, stacklevel=3)
     return True
 
-EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint_eval_halo",
+EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint_eval_halo", "cl_constraint_eval_pair",
            "cl_diag_constraint_eval", "cl_sddmm",
            "cl_gather_rows", "cl_diag_cg_apply", "cl_diag_cg_apply_rows", "cl_diag_cg_step", "cl_cg_step", "cl_cg_step_dev", "cl_admm_step_diag", "cl_admm_step_diag_fused", "cl_alm_inner_diag", "cl_alm_inner_diag_fused",
            "cl_diag_admm_cg_init", "cl_diag_admm_step_end", "cl_diag_admm_step_end_rows", "cl_single_entry_apply", "cl_single_entry_apply_pair", "cl_pair_pack", "cl_cg_direction_pair", "cl_lanczos_loop", "cl_lanczos_loop_fused",
@@ -159,6 +159,7 @@ def _declare(lib):
                                     P, P, P, P]
     lib.cl_constraint_eval.argtypes = [I64, P, P, P, P, I32, P, P, P, P, P, P, P, P, P]
     lib.cl_constraint_eval_halo.argtypes = [I64, P, P, P, P, I32, P, P, P, P, P, P, P, P, P, I64, P]
+    lib.cl_constraint_eval_pair.argtypes = [I64, P, P, P, P, I32, P, P, P, P]
     lib.cl_diag_constraint_eval.argtypes = [I64, P, I32, P, P, P, P, P, P, P, P, P]
     lib.cl_diag_cg_apply.argtypes = [I64, I32, P, D, D, P, P, P, P, P, P, P]
     lib.cl_cg_step.argtypes = [I64, D, P, P, P, P, P, P, P, P]

@@ -406,8 +406,18 @@ class AlmCore:
         dev.spmm(ops.c_mat.cpat, D, self.ld, out=self.CD, Z=[R, D, self.CR],
                  dots=[("out", ("z", 0)), ("out", ("z", 1)), (("z", 2), ("z", 1))], at=self.S_LS,
                  c_coeff=1.0)
-        dev.constraint_eval(ops.cop.con, self.ld, R, D, self.q1, X2=D, Y2=R, X3=D, Y3=D,
-                            out2=self.q2)
+        con = ops.cop.con
+        if PAIR and con.diag_aval is None and getattr(con, "halo", None) is None and self.ld <= 64 \
+                and ops.adj.apat.single_a is not None:
+            # single-entry constraints: R and D interleaved in one pair buffer, so each
+            # position's four rows come as two 2 ld runs (bit-identical products)
+            if getattr(self, "P2", None) is None:
+                self.P2 = dev.empty(self.n, 2 * self.ld)
+            dev.pair_pack(R, self.ld, self.P2, 0)
+            dev.pair_pack(D, self.ld, self.P2, 1)
+            dev.constraint_eval_pair(con, self.ld, self.P2, self.q1, self.q2)
+        else:
+            dev.constraint_eval(con, self.ld, R, D, self.q1, X2=D, Y2=R, X3=D, Y3=D, out2=self.q2)
         # w = -lam + rho*(b - ax)
         dev.lincomb(self.wv, [lam, ops.b, self.ax, self.q1, self.q2], [-1.0, rho, -rho, 0.0, 0.0],
                     dots=[(4, 4), (3, 4), ("out", 4), (3, 3), ("out", 3)], at=self.S_MV)
@@ -496,6 +506,8 @@ class InnerResult:
     ax: object
 
 
+# single-entry constraints: the line search reads R and D from a pair buffer (cl_constraint_eval_pair)
+PAIR = os.environ.get("CULORADS_PAIR", "1") != "0"
 NATIVE = True     # diagonal constraints: run the inner loop's control flow in C++ (row-sharded: with hooks)
 # Problems with n*ld at most this many doubles run the whole inner solve as one
 # cooperative launch (cl_alm_inner_diag_fused): latency, not HBM, bounds them.

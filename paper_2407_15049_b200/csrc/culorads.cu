@@ -392,10 +392,12 @@ __device__ __forceinline__ double group_dot(const double* __restrict__ X, const 
 struct ConGhost {
     const double* g[6];
     int64_t nown;
+    int64_t sx;           // row stride of the local operands (ld; 2 ld for a pair buffer)
 };
 
-__device__ __forceinline__ const double* grow(const double* X, const double* Xg, int64_t i, int64_t nown, int ld) {
-    return (nown < 0 || i < nown) ? X + i * ld : Xg + (i - nown) * ld;
+__device__ __forceinline__ const double* grow(const double* X, const double* Xg, int64_t i, int64_t nown, int ld,
+                                              int64_t sx) {
+    return (nown < 0 || i < nown) ? X + i * sx : Xg + (i - nown) * ld;
 }
 
 template <int G, int VEC>
@@ -459,26 +461,26 @@ __global__ void CK_BOUNDS(NP) constraint_kernel(int64_t m, const int64_t* __rest
                 double2 x1a = z2, y1a = z2, x1b = z2, y1b = z2, x2a = z2, y2a = z2, x2b = z2, y2b = z2;
                 double2 x3a = z2, y3a = z2, x3b = z2, y3b = z2;
                 if (act) {
-                    x1a = ld2(grow(X1, gh.g[0], i0, nw, ld) + col);
-                    y1a = ld2(grow(Y1, gh.g[1], j0, nw, ld) + col);
+                    x1a = ld2(grow(X1, gh.g[0], i0, nw, ld, gh.sx) + col);
+                    y1a = ld2(grow(Y1, gh.g[1], j0, nw, ld, gh.sx) + col);
                     if (two) {
-                        x1b = ld2(grow(X1, gh.g[0], i1, nw, ld) + col);
-                        y1b = ld2(grow(Y1, gh.g[1], j1, nw, ld) + col);
+                        x1b = ld2(grow(X1, gh.g[0], i1, nw, ld, gh.sx) + col);
+                        y1b = ld2(grow(Y1, gh.g[1], j1, nw, ld, gh.sx) + col);
                     }
                     if (NP > 1 && X2 != nullptr) {
-                        x2a = ld2(grow(X2, gh.g[2], i0, nw, ld) + col);
-                        y2a = ld2(grow(Y2, gh.g[3], j0, nw, ld) + col);
+                        x2a = ld2(grow(X2, gh.g[2], i0, nw, ld, gh.sx) + col);
+                        y2a = ld2(grow(Y2, gh.g[3], j0, nw, ld, gh.sx) + col);
                         if (two) {
-                            x2b = ld2(grow(X2, gh.g[2], i1, nw, ld) + col);
-                            y2b = ld2(grow(Y2, gh.g[3], j1, nw, ld) + col);
+                            x2b = ld2(grow(X2, gh.g[2], i1, nw, ld, gh.sx) + col);
+                            y2b = ld2(grow(Y2, gh.g[3], j1, nw, ld, gh.sx) + col);
                         }
                     }
                     if (NP > 1 && X3 != nullptr) {
-                        x3a = ld2(grow(X3, gh.g[4], i0, nw, ld) + col);
-                        y3a = ld2(grow(Y3, gh.g[5], j0, nw, ld) + col);
+                        x3a = ld2(grow(X3, gh.g[4], i0, nw, ld, gh.sx) + col);
+                        y3a = ld2(grow(Y3, gh.g[5], j0, nw, ld, gh.sx) + col);
                         if (two) {
-                            x3b = ld2(grow(X3, gh.g[4], i1, nw, ld) + col);
-                            y3b = ld2(grow(Y3, gh.g[5], j1, nw, ld) + col);
+                            x3b = ld2(grow(X3, gh.g[4], i1, nw, ld, gh.sx) + col);
+                            y3b = ld2(grow(Y3, gh.g[5], j1, nw, ld, gh.sx) + col);
                         }
                     }
                 }
@@ -529,14 +531,14 @@ __global__ void CK_BOUNDS(NP) constraint_kernel(int64_t m, const int64_t* __rest
         for (int64_t t = t0; t < t1; ++t) {
             const int64_t i = __ldg(pi + t), j = __ldg(pj + t);
             const double v = __ldg(val + t);
-            double x = group_dot_rows<G, VEC>(grow(X1, gh.g[0], i, nw, ld), grow(Y1, gh.g[1], j, nw, ld), ld, gl,
+            double x = group_dot_rows<G, VEC>(grow(X1, gh.g[0], i, nw, ld, gh.sx), grow(Y1, gh.g[1], j, nw, ld, gh.sx), ld, gl,
                                               gmask);
             if (X2 != nullptr)
-                x += group_dot_rows<G, VEC>(grow(X2, gh.g[2], i, nw, ld), grow(Y2, gh.g[3], j, nw, ld), ld, gl,
+                x += group_dot_rows<G, VEC>(grow(X2, gh.g[2], i, nw, ld, gh.sx), grow(Y2, gh.g[3], j, nw, ld, gh.sx), ld, gl,
                                             gmask);
             a1 += v * x;
             if (X3 != nullptr)
-                a2 += v * group_dot_rows<G, VEC>(grow(X3, gh.g[4], i, nw, ld), grow(Y3, gh.g[5], j, nw, ld), ld, gl,
+                a2 += v * group_dot_rows<G, VEC>(grow(X3, gh.g[4], i, nw, ld, gh.sx), grow(Y3, gh.g[5], j, nw, ld, gh.sx), ld, gl,
                                                  gmask);
         }
         if (gl == 0) {
@@ -856,6 +858,9 @@ __global__ void __launch_bounds__(NT) basis_subtract_kernel(const double* __rest
 #ifndef SP_UNROLL
 #define SP_UNROLL 8         // gathers in flight per lane
 #endif
+#ifndef SP_MINB1
+#define SP_MINB1 3          // resident CTAs per SM the epilogue variants are compiled for
+#endif
 #ifndef SP_MINB0
 #define SP_MINB0 4          // resident CTAs per SM the plain-epilogue variant is compiled for
 #endif
@@ -944,7 +949,7 @@ __device__ __forceinline__ void sp_issue(const SpDev& a, SpTile* T, int64_t (*me
 }
 
 template <int G, int VEC, int EPI, int GHOST>
-__global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : 3) spmm_tiled_kernel(SpDev a, EpiDev E, double* ws,
+__global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : SP_MINB1) spmm_tiled_kernel(SpDev a, EpiDev E, double* ws,
                                                                                      double* dots_out) {
     constexpr int NG = NT / G;
     // epilogue operand set of the tiled path: Y0, Y1, out, Z0, Z1, Z2
@@ -1368,12 +1373,28 @@ __global__ void __launch_bounds__(NT) diag_cg_apply_kernel(DiagCg a, double* ws,
             }
         }
         __syncthreads();
-        for (int rr = threadIdx.x; rr < nr; rr += NT) {
-            double sdot = 0.0;
-            for (int q = 0; q < h2; ++q) sdot += part[rr * h2 + q];
-            const double av = __ldg(a.aval + r0 + rr);
-            coef[rr] = a.rho * (av * (av * sdot));      // rho * a_c * y_c
-            if (a.coef_g != nullptr) a.coef_g[r0 + rr] = coef[rr];
+        if (h2 <= DCF_MAXH2) {
+            // short rows: one thread folds a row's unit products in order
+            for (int rr = threadIdx.x; rr < nr; rr += NT) {
+                double sdot = 0.0;
+                for (int q = 0; q < h2; ++q) sdot += part[rr * h2 + q];
+                const double av = __ldg(a.aval + r0 + rr);
+                coef[rr] = a.rho * (av * (av * sdot));      // rho * a_c * y_c
+                if (a.coef_g != nullptr) a.coef_g[r0 + rr] = coef[rr];
+            }
+        } else {
+            // wide rows (high rank): a warp per row, lane-strided partial sums and a shuffle tree
+            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+            for (int rr = wid; rr < nr; rr += NWARP) {
+                double sdot = 0.0;
+                for (int q = lane; q < h2; q += 32) sdot += part[rr * h2 + q];
+                sdot = warp_sum(sdot);
+                if (lane == 0) {
+                    const double av = __ldg(a.aval + r0 + rr);
+                    coef[rr] = a.rho * (av * (av * sdot));
+                    if (a.coef_g != nullptr) a.coef_g[r0 + rr] = coef[rr];
+                }
+            }
         }
         __syncthreads();
 #pragma unroll
@@ -1845,13 +1866,42 @@ int cl_constraint_eval(int64_t m, const int64_t* indptr, const int32_t* pi, cons
                                    stream);
 }
 
+namespace {
+int constraint_eval_impl(int64_t m, const int64_t* indptr, const int32_t* pi, const int32_t* pj, const double* val,
+                         int32_t ld, const double* X1, const double* Y1, const double* X2, const double* Y2,
+                         double* out1, const double* X3, const double* Y3, double* out2, const double* const* ghosts,
+                         int64_t nown, int64_t sx, void* stream);
+}
+
 int cl_constraint_eval_halo(int64_t m, const int64_t* indptr, const int32_t* pi, const int32_t* pj,
                             const double* val, int32_t ld, const double* X1, const double* Y1, const double* X2,
                             const double* Y2, double* out1, const double* X3, const double* Y3, double* out2,
                             const double* const* ghosts, int64_t nown, void* stream) {
+    return constraint_eval_impl(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2, ghosts, nown, 0,
+                                stream);
+}
+
+int cl_constraint_eval_pair(int64_t m, const int64_t* indptr, const int32_t* pi, const int32_t* pj,
+                            const double* val, int32_t ld, const double* P, double* out1, double* out2,
+                            void* stream) {
+    if (P == nullptr || ld < 2) return CL_EARG;
+    const double* R = P;
+    const double* D = P + ld;
+    return constraint_eval_impl(m, indptr, pi, pj, val, ld, R, D, D, R, out1, D, D, out2, nullptr, -1,
+                                2 * (int64_t)ld, stream);
+}
+
+}  // extern "C"
+
+namespace {
+int constraint_eval_impl(int64_t m, const int64_t* indptr, const int32_t* pi, const int32_t* pj, const double* val,
+                         int32_t ld, const double* X1, const double* Y1, const double* X2, const double* Y2,
+                         double* out1, const double* X3, const double* Y3, double* out2, const double* const* ghosts,
+                         int64_t nown, int64_t sx, void* stream) {
     ConGhost gh;
     for (int k = 0; k < 6; ++k) gh.g[k] = ghosts != nullptr ? ghosts[k] : nullptr;
     gh.nown = ghosts != nullptr ? nown : -1;
+    gh.sx = sx > 0 ? sx : ld;
     if (m == 0) return CL_OK;
     if (m < 0 || ld < 1 || (ld > 1 && (ld & 1)) || X1 == nullptr || Y1 == nullptr || out1 == nullptr) return CL_EARG;
     if ((X2 == nullptr) != (Y2 == nullptr) || (X3 == nullptr) != (Y3 == nullptr)) return CL_EARG;
@@ -1885,6 +1935,9 @@ int cl_constraint_eval_halo(int64_t m, const int64_t* indptr, const int32_t* pi,
 #undef CL_CK
     return (int)cudaGetLastError();
 }
+}  // namespace
+
+extern "C" {
 
 int cl_diag_constraint_eval(int64_t n, const double* aval, int32_t ld, const double* X1, const double* Y1,
                             const double* X2, const double* Y2, double* out1, const double* X3, const double* Y3,

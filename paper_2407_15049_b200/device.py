@@ -268,6 +268,13 @@ class Device:
         self.launches += 1
         check(rc, "cl_single_entry_apply_pair")
 
+    def constraint_eval_pair(self, con, ld, P2, out1, out2):
+        """Line-search products from the pair buffer P2 = [R | D]: out1 = A(RD^T + DR^T), out2 = A(DD^T)."""
+        rc = self.lib.cl_constraint_eval_pair(int(con.m), ptr(con.indptr), ptr(con.pi), ptr(con.pj), ptr(con.val),
+                                              int(ld), ptr(P2), ptr(out1), ptr(out2), self.sp)
+        self.launches += 1
+        check(rc, "cl_constraint_eval_pair")
+
     def pair_pack(self, X, ld, P2, half):
         """P2[:, half*ld:(half+1)*ld] = X."""
         rc = self.lib.cl_pair_pack(int(X.shape[0]), int(ld), ptr(X), ptr(P2), int(half), self.sp)

@@ -559,11 +559,12 @@ def halo_buffer_rows(ops):
 
 
 def memory_model(n_global, world, r, nnz_c_per_row, m_global=None, nnz_a_per_con=1.0, halo_frac=1.0,
-                 memory=8, halo_slots=1):
+                 memory=8, halo_slots=1, pair=False):
     """Per-rank device bytes of a row-sharded solve at rank r.
 
-    * stage buffers: driver.stage_factor_buffers(memory) factors of n_loc x ld fp64
-      (the ALM stage dominates: 2 memory + 11 = 27 at the default L-BFGS memory 8);
+    * stage buffers: driver.stage_factor_buffers(memory, pair) factors of n_loc x ld fp64
+      (the ALM stage dominates: 2 memory + 8 = 24 at the default L-BFGS memory 8, + 2 for
+      the pair buffer of single-entry constraints);
     * halo: ``halo_slots`` receive buffers of world * maxb rows plus the send buffer,
       maxb = halo_frac * n_loc published rows (random graphs: every row has a remote
       neighbour, halo_frac ~ 1; locality-ordered meshes: only the block-boundary band);
@@ -584,7 +585,7 @@ def memory_model(n_global, world, r, nnz_c_per_row, m_global=None, nnz_a_per_con
     maxb = int(halo_frac * n_loc)
     out = {
         "n_per_rank": n_loc, "ld": ld, "factor_bytes": factor,
-        "stage_buffers": stage_factor_buffers(memory) * factor,
+        "stage_buffers": stage_factor_buffers(memory, pair) * factor,
         "halo": (halo_slots * (world * maxb) + maxb) * ld * 8 if world > 1 else 0,
         "operators": (nnz_c * 12 + n_loc * 8) + (nnz_c + 2 * nnz_a) * 20 + nnz_a * 12 * 2 + nnz_a * 28
                      + m_loc * 8 + 2 * n_loc * 8,

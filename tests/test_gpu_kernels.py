@@ -329,6 +329,53 @@ def test_pair_cg_matches_two_operand_cg(dev):
     assert s1 == s2 and u1.tobytes() == u2.tobytes() and v1.tobytes() == v2.tobytes()
 
 
+@pytest.mark.parametrize("r", [3, 25, 50])
+def test_constraint_eval_pair_bit_identical(dev, r):
+    """cl_constraint_eval_pair on [R | D] equals the line search's three-product
+    cl_constraint_eval (X1=R, Y1=D, X2=D, Y2=R, X3=Y3=D) bit for bit."""
+    from paper_2407_15049_b200 import graphs, linops, problem
+    from paper_2407_15049_b200.device import padded_ld
+    p = problem.build_matrix_completion(graphs.random_completion(300, 260, 7000, seed=r))
+    ops = linops.build_operators(p)
+    con = ops.cop.con
+    ld = padded_ld(r)
+    rng = np.random.default_rng(r)
+    R = linops.to_factor(rng.standard_normal((p.n, r)), dev, ld)
+    D = linops.to_factor(rng.standard_normal((p.n, r)), dev, ld)
+    q1, q2, s1, s2 = dev.empty(p.m), dev.empty(p.m), dev.empty(p.m), dev.empty(p.m)
+    dev.constraint_eval(con, ld, R, D, q1, X2=D, Y2=R, X3=D, Y3=D, out2=q2)
+    P2 = dev.empty(p.n, 2 * ld)
+    dev.pair_pack(R, ld, P2, 0)
+    dev.pair_pack(D, ld, P2, 1)
+    dev.constraint_eval_pair(con, ld, P2, s1, s2)
+    assert q1.cpu().numpy().tobytes() == s1.cpu().numpy().tobytes()
+    assert q2.cpu().numpy().tobytes() == s2.cpu().numpy().tobytes()
+
+
+def test_pair_line_search_alm_matches(dev):
+    """A completion ALM inner solve with the pair-buffer line search (alm.PAIR) follows
+    the two-operand line search bit for bit."""
+    from paper_2407_15049_b200 import alm, graphs, linops, problem
+    from paper_2407_15049_b200.device import padded_ld
+    p = problem.build_matrix_completion(graphs.random_completion(400, 300, 9000, seed=4))
+    ops = linops.build_operators(p)
+    r = 10
+    ld = padded_ld(r)
+    R0 = linops.to_factor(np.random.default_rng(1).standard_normal((p.n, r)) / 10, dev, ld)
+    out = []
+    for pair in (True, False):
+        alm.PAIR = pair
+        try:
+            core = alm.AlmCore(ops, p.n, ld)
+            R = R0.clone()
+            res = alm._inner(core, R, dev.zeros(p.m), 3.0, 1.0, 0.0, 25, None, 8, alm._RankRecorder(None, r))
+        finally:
+            alm.PAIR = True
+        out.append((R.cpu().numpy(), res.iterations, res.grad_norms))
+    assert out[0][1] == out[1][1] > 0 and out[0][2] == out[1][2]
+    assert out[0][0].tobytes() == out[1][0].tobytes()
+
+
 def test_single_entry_detection_rejects_general_constraints(dev):
     from paper_2407_15049_b200 import linops
     from tests._golden import load, problem_from

@@ -214,9 +214,10 @@ def test_memory_model_configs():
     random one (its halo is the whole remote factor)."""
     from paper_2407_15049_b200 import driver, shard
     budget = 0.94 * 180e9
-    c3 = shard.memory_model(int(2e7), 8, 29, 0, m_global=int(2e8), nnz_a_per_con=2, halo_slots=2)
+    c3 = shard.memory_model(int(2e7), 8, 29, 0, m_global=int(2e8), nnz_a_per_con=2, halo_slots=2, pair=True)
     assert c3["total"] < budget / 4
-    assert shard.memory_model(int(2e7), 8, 150, 0, m_global=int(2e8), nnz_a_per_con=2, halo_slots=2)["total"] < budget
+    assert shard.memory_model(int(2e7), 8, 140, 0, m_global=int(2e8), nnz_a_per_con=2, halo_slots=2,
+                              pair=True)["total"] < budget
     mesh = shard.memory_model(int(1.7e8), 8, 29, 7, halo_frac=0.002)
     rand = shard.memory_model(int(1.7e8), 8, 29, 7)
     assert mesh["total"] < budget < rand["total"]

@@ -22,6 +22,9 @@ VARIANTS = {
     "ck8_se8": ["-DCK_MINB=8", "-DSE_MINB=8"],
     "ck3_4": ["-DCK3_MINB=4"],
     "ck3_5": ["-DCK3_MINB=5"],
+    "sp1_4": ["-DSP_MINB1=4"],
+    "spu12": ["-DSP_UNROLL=12"],
+    "spu4": ["-DSP_UNROLL=4"],
     "sp5": ["-DSP_MINB0=5"],
     "sp6": ["-DSP_MINB0=6"],
 }
@@ -94,6 +97,22 @@ def one(tag):
     R = linops.to_factor(np.random.default_rng(0).standard_normal((n, r)) / math.sqrt(n * r), dev, ld)
     core = alm.AlmCore(ops, n, ld)
     res["maxcut_CR_ms"] = timeit(dev, lambda: core.c_times(R, core.CR), reps=20)
+    D = R.clone()
+    ls = lambda: dev.spmm(ops.c_mat.cpat, D, ld, out=core.CD, Z=[R, D, core.CR],  # noqa: E731
+                          dots=[("out", ("z", 0)), ("out", ("z", 1)), (("z", 2), ("z", 1))], at=40, c_coeff=1.0)
+    res["maxcut_linesearch_spmm_ms"] = timeit(dev, ls, reps=20)
+    del ops, core, R, D
+    torch.cuda.empty_cache()
+    # high rank (configs[1] after its escalations): n = 1e6, r = 822
+    n = int(1e6)
+    p = problem.build_maxcut(graphs.random_sparse(n, deg=10.0, seed=0))
+    ops = linops.build_operators(p, dev=dev)
+    ld = 822
+    R = linops.to_factor(np.random.default_rng(0).standard_normal((n, ld)) / math.sqrt(n * ld), dev, ld)
+    core = alm.AlmCore(ops, n, ld)
+    D = R.clone()
+    res["hr_CR_ms"] = timeit(dev, lambda: core.c_times(R, core.CR), reps=5)
+    res["hr_linesearch_spmm_ms"] = timeit(dev, ls, reps=5)
     print(json.dumps(res), flush=True)
 
 
