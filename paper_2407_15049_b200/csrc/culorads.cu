@@ -856,7 +856,16 @@ __global__ void __launch_bounds__(NT) basis_subtract_kernel(const double* __rest
 #endif
 #define SP_PTRMAX 264       // row pointers per tile: TR + 1 + alignment slack, TR <= 256
 #ifndef SP_UNROLL
-#define SP_UNROLL 8         // gathers in flight per lane
+#define SP_UNROLL 8         // gathers in flight per lane (epilogue variants)
+#endif
+// Plain-store variant: more gathers in flight for narrow rows (12: 4.32 -> 4.12 ms for C R at
+// n = 1e7, ld 26), fewer for wide rows where one group already covers 512 bytes per gather
+// (4: 13.3 -> 12.6 ms at ld 822); the epilogue variants lose registers to more (occupancy_sweep).
+#ifndef SP_UNROLL0
+#define SP_UNROLL0 12
+#endif
+#ifndef SP_UNROLL0_WIDE
+#define SP_UNROLL0_WIDE 4
 #endif
 #ifndef SP_MINB1
 #define SP_MINB1 3          // resident CTAs per SM the epilogue variants are compiled for
@@ -952,6 +961,7 @@ template <int G, int VEC, int EPI, int GHOST>
 __global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : SP_MINB1) spmm_tiled_kernel(SpDev a, EpiDev E, double* ws,
                                                                                      double* dots_out) {
     constexpr int NG = NT / G;
+    constexpr int SPU = EPI == 0 ? (G == 32 ? SP_UNROLL0_WIDE : SP_UNROLL0) : SP_UNROLL;
     // epilogue operand set of the tiled path: Y0, Y1, out, Z0, Z1, Z2
     constexpr int NOPS = SP_NY + 1 + SP_NZ;
     __shared__ __align__(128) SpTile T[2];
@@ -1028,18 +1038,18 @@ __global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : SP_MIN
                 const bool active = col < ld;
                 double2 acc = make_double2(0.0, 0.0);
                 if (!heavy) {
-                    for (int64_t s = s0; s < s1; s += SP_UNROLL) {
-                        int jv[SP_UNROLL];
-                        double cv[SP_UNROLL];
-                        double2 xv[SP_UNROLL];
+                    for (int64_t s = s0; s < s1; s += SPU) {
+                        int jv[SPU];
+                        double cv[SPU];
+                        double2 xv[SPU];
 #pragma unroll
-                        for (int u = 0; u < SP_UNROLL; ++u) {
+                        for (int u = 0; u < SPU; ++u) {
                             const bool ok = s + u < s1;
                             jv[u] = ok ? B.idx[s + u - ib] : 0;
                             cv[u] = ok ? B.val[s + u - vb] : 0.0;
                         }
 #pragma unroll
-                        for (int u = 0; u < SP_UNROLL; ++u) {
+                        for (int u = 0; u < SPU; ++u) {
                             if (active && s + u < s1) {
                                 const double* src = (!GHOST || jv[u] < a.nown) ? X + (int64_t)jv[u] * ld
                                                                                : a.Xg + (int64_t)(jv[u] - a.nown) * ld;
@@ -1050,7 +1060,7 @@ __global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : SP_MIN
                             }
                         }
 #pragma unroll
-                        for (int u = 0; u < SP_UNROLL; ++u) {
+                        for (int u = 0; u < SPU; ++u) {
                             if (s + u < s1) {
                                 acc.x = fma(cv[u], xv[u].x, acc.x);
                                 acc.y = fma(cv[u], xv[u].y, acc.y);
