@@ -450,6 +450,16 @@ def alm_gradient(R, dual: DualVector, ops, scale=1.0, ax=None):
     m = ops.problem.m
     axd = ops.cop.apply_pair_dev(Rd, Rd, ld) if ax is None else to_vec(ax, dev)
     w = dev.empty(m)
+    if ops.is_diag and getattr(ops.c_mat.cpat, "halo", None) is None:
+        # diagonal constraints (MaxCut): S = scale C + diag(a w), so 2 S R is the C product with a
+        # row-diagonal epilogue term -- the solver's own fused path (no Omega assembly). Same
+        # value as the assembled product up to the association of the diagonal slot (1e-16).
+        dev.lincomb(w, [_lam_dev(ops, dual.lam), axd, ops.b], [2.0, 2.0 * dual.rho, -2.0 * dual.rho])
+        g = dev.empty(*Rd.shape)
+        dev.spmm(ops.c_mat.cpat, Rd, ld, alpha=2.0 * scale, out=g, Y=[Rd], ycoef=[0.0], c_coeff=1.0,
+                 drow=w, dmul=ops.diag_aval)
+        out = g[:, :R.shape[1]]
+        return out if isinstance(R, torch.Tensor) else out.cpu().numpy()
     dev.lincomb(w, [_lam_dev(ops, dual.lam), axd, ops.b], [1.0, dual.rho, -dual.rho])
     S = ops.adj.assemble(lam=w, c_coeff=scale)
     g = S.matmul_dev(Rd, ld, alpha=2.0)
