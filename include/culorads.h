@@ -413,6 +413,16 @@ typedef struct {
     double* rec;               /* 4 * rec_cap host doubles */
     double* gnorms;            /* rec_cap host doubles */
     const cl_dist_hooks* dist; /* row-sharded solve (cl_alm_inner_diag only), or NULL */
+    /* cl_alm_inner_generic only (general constraints: A(R R^T) by the constraint CSR, the
+     * gradient's A*(w) R over Omega_A with assembled coefficients) */
+    int64_t m;                 /* constraints */
+    const int64_t* con_indptr; /* constraint CSR with resolved positions (cl_constraint_eval) */
+    const int32_t* con_pi;
+    const int32_t* con_pj;
+    const double* con_val;
+    cl_pattern apat;           /* Omega_A: adjoint rows (w1 = wv set here), scratch */
+    double* res;               /* m doubles */
+    double* pair;              /* n x 2ld pair buffer [R | D] for the line search, or NULL */
 } cl_alm_inner_args;
 
 typedef struct {
@@ -426,6 +436,12 @@ typedef struct {
 } cl_alm_inner_stats;
 
 int cl_alm_inner_diag(const cl_alm_inner_args* a, cl_alm_inner_stats* out);
+/* The same inner solve for general constraints (matrix completion, SDPA instances): the
+ * launches of the Python host path's generic chain (alm.py _inner with AlmCore.grad_value's
+ * generic branch and line_search), with its scalar algebra in native code: bit-identical
+ * iterates. `aval` unused; m, con_*, apat, res set; `pair` optional (single-entry
+ * constraints: cl_constraint_eval_pair). Single GPU (dist must be NULL). */
+int cl_alm_inner_generic(const cl_alm_inner_args* a, cl_alm_inner_stats* out);
 /* The same inner solve as ONE cooperative launch (csrc/alm_fused.cu) for small
  * problems: thread 0 of every block replays the scalar algebra from grid-reduced
  * values, vector passes run between grid barriers; one synchronize per inner solve.

@@ -55,7 +55,7 @@ def barrier_timeout(rc, what):
 
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint_eval_halo", "cl_constraint_eval_pair",
            "cl_diag_constraint_eval", "cl_sddmm",
-           "cl_gather_rows", "cl_diag_cg_apply", "cl_diag_cg_apply_rows", "cl_diag_cg_step", "cl_cg_step", "cl_cg_step_dev", "cl_admm_step_diag", "cl_admm_step_diag_fused", "cl_alm_inner_diag", "cl_alm_inner_diag_fused",
+           "cl_gather_rows", "cl_diag_cg_apply", "cl_diag_cg_apply_rows", "cl_diag_cg_step", "cl_cg_step", "cl_cg_step_dev", "cl_admm_step_diag", "cl_admm_step_diag_fused", "cl_alm_inner_diag", "cl_alm_inner_diag_fused", "cl_alm_inner_generic",
            "cl_diag_admm_cg_init", "cl_diag_admm_step_end", "cl_diag_admm_step_end_rows", "cl_single_entry_apply", "cl_single_entry_apply_pair", "cl_pair_pack", "cl_cg_direction_pair", "cl_lanczos_loop", "cl_lanczos_loop_fused",
            "cl_pattern_assemble", "cl_lanczos_update",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
@@ -131,7 +131,8 @@ class AlmInnerArgs(ctypes.Structure):
                 ("CD", P), ("ax", P), ("ax2", P), ("q1", P), ("q2", P), ("wv", P), ("zero_g", P),
                 ("nbuf", I32), ("bufs", P * CL_ALM_MAXBUF), ("cpat", Pattern), ("slab", P), ("host", P),
                 ("ws", P), ("stream", P), ("rec_cap", I32), ("rec", P), ("gnorms", P),
-                ("dist", ctypes.POINTER(DistHooks))]
+                ("dist", ctypes.POINTER(DistHooks)), ("m", I64), ("con_indptr", P), ("con_pi", P), ("con_pj", P),
+                ("con_val", P), ("apat", Pattern), ("res", P), ("pair", P)]
 
 
 class AlmInnerStats(ctypes.Structure):
@@ -169,6 +170,7 @@ def _declare(lib):
     lib.cl_admm_step_diag_fused.argtypes = [ctypes.POINTER(AdmmDiagArgs), ctypes.POINTER(AdmmStepStats)]
     lib.cl_alm_inner_diag.argtypes = [ctypes.POINTER(AlmInnerArgs), ctypes.POINTER(AlmInnerStats)]
     lib.cl_alm_inner_diag_fused.argtypes = [ctypes.POINTER(AlmInnerArgs), ctypes.POINTER(AlmInnerStats)]
+    lib.cl_alm_inner_generic.argtypes = [ctypes.POINTER(AlmInnerArgs), ctypes.POINTER(AlmInnerStats)]
     lib.cl_diag_admm_cg_init.argtypes = [ctypes.POINTER(Pattern), P, P, I32, D, D, P, P, P, P, P, P, P]
     lib.cl_diag_admm_step_end_rows.argtypes = [I64, I32, P, P, P, P, P, P, D, P, P, P, P, P]
     lib.cl_diag_admm_step_end.argtypes = [ctypes.POINTER(Pattern), P, P, I32, P, P, P, D, P, P, P, P, P]

@@ -401,21 +401,30 @@ class AlmCore:
                     gy=s[9], gH=gH, yH=yH)
 
     # line search -------------------------------------------------------
+    def pair_ok(self):
+        """Line search on a pair buffer [R | D]: single-entry constraints, one GPU, ld <= 64."""
+        con = self.ops.cop.con
+        return (PAIR and con.diag_aval is None and getattr(con, "halo", None) is None and self.ld <= 64
+                and self.ops.adj.apat.single_a is not None)
+
+    def pair_buffer(self):
+        if getattr(self, "P2", None) is None:
+            self.P2 = self.dev.empty(self.n, 2 * self.ld)
+        return self.P2
+
     def line_search(self, R, D, lam, rho, scale):
         dev, ops = self.dev, self.ops
         dev.spmm(ops.c_mat.cpat, D, self.ld, out=self.CD, Z=[R, D, self.CR],
                  dots=[("out", ("z", 0)), ("out", ("z", 1)), (("z", 2), ("z", 1))], at=self.S_LS,
                  c_coeff=1.0)
         con = ops.cop.con
-        if PAIR and con.diag_aval is None and getattr(con, "halo", None) is None and self.ld <= 64 \
-                and ops.adj.apat.single_a is not None:
+        if self.pair_ok():
             # single-entry constraints: R and D interleaved in one pair buffer, so each
             # position's four rows come as two 2 ld runs (bit-identical products)
-            if getattr(self, "P2", None) is None:
-                self.P2 = dev.empty(self.n, 2 * self.ld)
-            dev.pair_pack(R, self.ld, self.P2, 0)
-            dev.pair_pack(D, self.ld, self.P2, 1)
-            dev.constraint_eval_pair(con, self.ld, self.P2, self.q1, self.q2)
+            P2 = self.pair_buffer()
+            dev.pair_pack(R, self.ld, P2, 0)
+            dev.pair_pack(D, self.ld, P2, 1)
+            dev.constraint_eval_pair(con, self.ld, P2, self.q1, self.q2)
         else:
             dev.constraint_eval(con, self.ld, R, D, self.q1, X2=D, Y2=R, X3=D, Y3=D, out2=self.q2)
         # w = -lam + rho*(b - ax)
@@ -519,6 +528,7 @@ class InnerResult:
 # single-entry constraints: the line search reads R and D from a pair buffer (cl_constraint_eval_pair)
 PAIR = os.environ.get("CULORADS_PAIR", "1") != "0"
 NATIVE = True     # diagonal constraints: run the inner loop's control flow in C++ (row-sharded: with hooks)
+NATIVE_GENERIC = True   # other constraint families on one GPU: cl_alm_inner_generic
 # Problems with n*ld at most this many doubles run the whole inner solve as one
 # cooperative launch (cl_alm_inner_diag_fused): latency, not HBM, bounds them.
 FUSED = os.environ.get("CULORADS_FUSED", "1") != "0"
@@ -526,10 +536,12 @@ FUSED_MAX_ELEMS = int(os.environ.get("CULORADS_FUSED_MAX", 1 << 18))
 
 
 def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory, recorder):
-    """alm.py:268 through cl_alm_inner_diag: the launches of ``_inner`` below with the
+    """alm.py:268 through cl_alm_inner_diag (diagonal constraints) or cl_alm_inner_generic
+    (any other constraint family, one GPU): the launches of ``_inner`` below with the
     host-side scalar algebra in native code (bit-identical iterates)."""
     from . import _lib
     dev, ops = core.dev, core.ops
+    generic = not ops.is_diag
     n, ld = core.n, core.ld
     nbuf = 2 * memory + 4
     bufs = getattr(core, "native_bufs", None)
@@ -540,11 +552,25 @@ def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory
     a.tol = float(tol)
     a.reduce_factor = float(reduce_factor) if reduce_factor is not None else -1.0
     a.rho, a.scale, a.b1 = float(rho), float(scale), float(ops.problem.b_norm1)
-    a.aval, a.b, a.lam = ops.diag_aval.data_ptr(), ops.b.data_ptr(), lam.data_ptr()
+    a.aval = ops.diag_aval.data_ptr() if not generic else None
+    a.b, a.lam = ops.b.data_ptr(), lam.data_ptr()
     a.R, a.CR, a.CD = R.data_ptr(), core.CR.data_ptr(), core.CD.data_ptr()
     a.ax, a.ax2 = core.ax.data_ptr(), core.ax2.data_ptr()
     a.q1, a.q2, a.wv = core.q1.data_ptr(), core.q2.data_ptr(), core.wv.data_ptr()
     a.zero_g = None                 # g_old = 0 for the first gradient: no zero factor is held
+    if generic:
+        # the generic chain's y = g - g_old is a lincomb: it reads a zero factor, as _inner does
+        if core.zero_g is None:
+            core.zero_g = dev.zeros(n, ld)
+        a.zero_g = core.zero_g.data_ptr()
+        con = ops.cop.con
+        a.m = int(con.m)
+        a.con_indptr, a.con_pi, a.con_pj, a.con_val = (con.indptr.data_ptr(), con.pi.data_ptr(),
+                                                       con.pj.data_ptr(), con.val.data_ptr())
+        a.apat = ops.adj.apat.struct(c_coeff=None, w1=core.wv)
+        a.res = core.res.data_ptr()
+        if core.pair_ok():
+            a.pair = core.pair_buffer().data_ptr()
     a.nbuf = nbuf
     for j in range(nbuf):
         a.bufs[j] = bufs[j].data_ptr()
@@ -564,7 +590,7 @@ def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory
             core.dist_hooks = native_hooks(dev, ops)
         a.dist = core.dist_hooks
     st = _lib.AlmInnerStats()
-    fused = FUSED and dev.world == 1 and n >= 1 and n * ld <= FUSED_MAX_ELEMS
+    fused = FUSED and not generic and dev.world == 1 and n >= 1 and n * ld <= FUSED_MAX_ELEMS
     if fused:
         R_keep = R.clone()          # the one launch steps R in place; kept for a void launch
         rc = dev.lib.cl_alm_inner_diag_fused(ctypes.byref(a), ctypes.byref(st))
@@ -577,7 +603,12 @@ def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory
         else:
             dev.launches += 1
             _lib.check(rc, "cl_alm_inner_diag_fused")
-    if not fused:
+    if generic:
+        fused = False
+        rc = dev.lib.cl_alm_inner_generic(ctypes.byref(a), ctypes.byref(st))
+        dev.launches += 8 + 13 * st.iterations
+        _lib.check(rc, f"cl_alm_inner_generic (alm_native.cu:{st.err_line})")
+    elif not fused:
         rc = dev.lib.cl_alm_inner_diag(ctypes.byref(a), ctypes.byref(st))
         dev.launches += 2 + 5 * st.iterations
         _lib.check(rc, f"cl_alm_inner_diag (alm_native.cu:{st.err_line})")
@@ -597,7 +628,9 @@ def _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory
 def _inner(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory, recorder):
     """alm.py:268 on device buffers. R is updated in place."""
     dev, ops = core.dev, core.ops
-    if NATIVE and ops.is_diag and memory <= 8 and core.ld >= 2:
+    if NATIVE and memory <= 8 and core.ld >= 2 and (ops.is_diag or (
+            NATIVE_GENERIC and dev.world == 1 and getattr(ops, "row_range", None) is None
+            and getattr(ops.cop.con, "halo", None) is None)):
         return _inner_native(core, R, lam, rho, scale, tol, max_iter, reduce_factor, memory, recorder)
     b1 = ops.problem.b_norm1
     pool = core.pool

@@ -29,6 +29,8 @@ struct Ctx {
     int rc;
     int line;
     int64_t N;
+    bool generic;    // general constraints (cl_alm_inner_generic)
+    int64_t M;       // m-vector length
 };
 
 #define TRY(c, expr)                      \
@@ -186,10 +188,115 @@ bool best_step(const double* a, double* tau) {
 double* B(const Ctx& c, int i) { return c.a->bufs[i]; }
 
 // AlmCore.grad_value, diagonal branch: one cl_diag_alm_update launch + one fetch
+void lincomb_n(Ctx& c, double* out, int nin, const double* const* in, const double* coef, int64_t N, double* slab,
+               int mode, int ndot, const uint8_t* da, const uint8_t* db) {
+    cl_lincomb_args L;
+    memset(&L, 0, sizeof(L));
+    L.nin = nin;
+    L.mode = mode;
+    for (int j = 0; j < nin; ++j) {
+        L.in[j] = in[j];
+        L.coef[j] = coef[j];
+    }
+    L.out = out;
+    L.ndot = ndot;
+    for (int k = 0; k < ndot && da != nullptr; ++k) {
+        L.da[k] = da[k];
+        L.db[k] = db[k];
+    }
+    TRY(c, cl_lincomb(&L, N, ndot ? slab : nullptr, ndot ? c.a->ws : nullptr, (void*)c.st));
+}
+
+// AlmCore.grad_value, generic branch (alm.py AlmCore.grad_value): the step (unless refresh),
+// res = ax - b with rr, lam.res; <CR, R>; w = lam + rho res; g = 2 A*(w) R + 2 scale C R over
+// Omega_A; y = g - g_old; the Gram rows of g and y; one fetch. Results in the diagonal
+// branch's layout s[0..]: crr, gg, yd, lres, rr, yy, gy, gH[], yH[].
+bool grad_value_generic(Ctx& c, double* R, const double* gold, double* gnew, double* y, const double* const* H, int nh,
+                        const double* D, const double* CD, double tau, bool refresh, const double* ax_in,
+                        double* ax_out, double* s) {
+    const cl_alm_inner_args* a = c.a;
+    const double* ax = ax_in;
+    if (!refresh) {
+        const double* i1[2] = {R, D};
+        const double c1[2] = {1.0, tau};
+        lincomb_n(c, R, 2, i1, c1, c.N, nullptr, CL_DOT_PAIRS, 0, nullptr, nullptr);
+        const double* i2[2] = {a->CR, CD};
+        lincomb_n(c, a->CR, 2, i2, c1, c.N, nullptr, CL_DOT_PAIRS, 0, nullptr, nullptr);
+        const double* i3[3] = {ax_in, a->q1, a->q2};
+        const double c3[3] = {1.0, tau, tau * tau};
+        lincomb_n(c, ax_out, 3, i3, c3, c.M, nullptr, CL_DOT_PAIRS, 0, nullptr, nullptr);
+        ax = ax_out;
+    }
+    {
+        const double* in[3] = {ax, a->b, a->lam};
+        const double cf[3] = {1.0, -1.0, 0.0};
+        const uint8_t da[2] = {CL_OUT, 2}, db[2] = {CL_OUT, CL_OUT};
+        lincomb_n(c, a->res, 3, in, cf, c.M, a->slab + S_UPD + 4, CL_DOT_PAIRS, 2, da, db);   // rr, lam.res
+    }
+    {
+        const double* in[2] = {a->CR, R};
+        const double cf[2] = {0.0, 0.0};
+        const uint8_t da[1] = {0}, db[1] = {1};
+        lincomb_n(c, nullptr, 2, in, cf, c.N, a->slab + S_UPD, CL_DOT_PAIRS, 1, da, db);       // <CR, R>
+    }
+    {
+        const double* in[2] = {a->lam, a->res};
+        const double cf[2] = {1.0, a->rho};
+        lincomb_n(c, a->wv, 2, in, cf, c.M, nullptr, CL_DOT_PAIRS, 0, nullptr, nullptr);   // w = lam + rho res
+    }
+    {
+        cl_pattern P = a->apat;
+        P.cv = nullptr;
+        P.c_coeff = 0.0;
+        P.w1 = a->wv;
+        P.w2 = nullptr;
+        cl_epilogue E;
+        memset(&E, 0, sizeof(E));
+        E.ny = 1;
+        E.Y[0] = a->CR;
+        E.ycoef[0] = 2.0 * a->scale;
+        TRY(c, cl_pattern_spmm(&P, R, a->ld, 2.0, &E, gnew, nullptr, nullptr, (void*)c.st));
+    }
+    {
+        const double* in[2] = {gnew, gold};
+        const double cf[2] = {1.0, -1.0};
+        lincomb_n(c, y, 2, in, cf, c.N, nullptr, CL_DOT_PAIRS, 0, nullptr, nullptr);
+    }
+    {
+        const double* in[2 + 2 * CL_ALM_MAXMEM + 1];
+        double cf[2 + 2 * CL_ALM_MAXMEM + 1];
+        in[0] = gnew;
+        in[1] = y;
+        for (int k = 0; k < nh; ++k) in[2 + k] = H[k];
+        for (int k = 0; k < 2 + nh; ++k) cf[k] = 0.0;
+        lincomb_n(c, nullptr, 2 + nh, in, cf, c.N, a->slab + S_UPD + 8, CL_DOT_FIRST_TWO, 1, nullptr, nullptr);
+    }
+    if (!fetch(c, S_UPD + 8 + 2 * CL_MAXIN)) return false;
+    const double* h = a->host + S_UPD;
+    s[0] = h[0];
+    s[1] = h[8];
+    s[3] = h[5];
+    s[4] = h[4];
+    s[5] = h[8 + CL_MAXIN];
+    s[6] = h[9];
+    for (int k = 0; k < nh; ++k) {
+        s[7 + k] = h[10 + k];
+        s[7 + CL_MAXIN + k] = h[8 + CL_MAXIN + 1 + k];
+    }
+    s[2] = (D != nullptr && nh > 0 && H[nh - 1] == D) ? s[7 + CL_MAXIN + nh - 1] : 0.0;
+    return true;
+}
+
 bool grad_value(Ctx& c, double* R, int g_old, const double* gold_ptr, int g_new, int ybuf, const int* H, int nh,
                 const double* D, const double* CD, double tau, bool refresh, const double* ax_in, double* ax_out,
                 double* s) {
     const cl_alm_inner_args* a = c.a;
+    if (c.generic) {
+        const double* Hp[2 * CL_ALM_MAXMEM + 1];
+        for (int j = 0; j < nh; ++j) Hp[j] = c.a->bufs[H[j]];
+        return grad_value_generic(c, R, g_old >= 0 ? c.a->bufs[g_old] : gold_ptr, c.a->bufs[g_new], c.a->bufs[ybuf],
+                                  Hp, nh, D, CD, tau, refresh, ax_in, ax_out, s);
+    }
     cl_diag_update_args u;
     memset(&u, 0, sizeof(u));
     u.n = a->n;
@@ -222,6 +329,11 @@ bool grad_value(Ctx& c, double* R, int g_old, const double* gold_ptr, int g_new,
 
 void constraint_values(Ctx& c, const double* R, double* out) {
     const cl_alm_inner_args* a = c.a;
+    if (c.generic) {
+        TRY(c, cl_constraint_eval(a->m, a->con_indptr, a->con_pi, a->con_pj, a->con_val, a->ld, R, R, nullptr, nullptr,
+                                  out, nullptr, nullptr, nullptr, (void*)c.st));
+        return;
+    }
     TRY(c, cl_diag_constraint_eval(a->n, a->aval, a->ld, R, R, nullptr, nullptr, out, nullptr, nullptr, nullptr,
                                    (void*)c.st));
 }
@@ -249,9 +361,25 @@ void c_times(Ctx& c, const double* X, double* out) {
     TRY(c, cl_pattern_spmm(&P, X, a->ld, 1.0, nullptr, out, nullptr, nullptr, (void*)c.st));
 }
 
+int alm_inner(const cl_alm_inner_args* a, cl_alm_inner_stats* out, bool generic);
+
 }  // namespace
 
 extern "C" int cl_alm_inner_diag(const cl_alm_inner_args* a, cl_alm_inner_stats* out) {
+    return alm_inner(a, out, false);
+}
+
+extern "C" int cl_alm_inner_generic(const cl_alm_inner_args* a, cl_alm_inner_stats* out) {
+    if (a == nullptr || a->dist != nullptr || a->m < 0 || (a->m > 0 && (a->con_indptr == nullptr ||
+        a->con_pi == nullptr || a->con_pj == nullptr || a->con_val == nullptr)) || a->res == nullptr ||
+        a->apat.at_ptr == nullptr || a->zero_g == nullptr)
+        return CL_EARG;
+    return alm_inner(a, out, true);
+}
+
+namespace {
+
+int alm_inner(const cl_alm_inner_args* a, cl_alm_inner_stats* out, bool generic) {
     if (a == nullptr || out == nullptr || a->n < 0 || a->ld < 2 || (a->ld & 1) || a->memory < 0 ||
         a->memory > CL_ALM_MAXMEM || a->nbuf < 2 * a->memory + 4 || a->nbuf > MAXB)
         return CL_EARG;
@@ -261,6 +389,8 @@ extern "C" int cl_alm_inner_diag(const cl_alm_inner_args* a, cl_alm_inner_stats*
     c.rc = 0;
     c.line = 0;
     c.N = a->n * (int64_t)a->ld;
+    c.generic = generic;
+    c.M = generic ? a->m : a->n;
     memset(out, 0, sizeof(*out));
     static thread_local Hist hist;
     hist.cap = a->memory;
@@ -384,7 +514,18 @@ extern "C" int cl_alm_inner_diag(const cl_alm_inner_args* a, cl_alm_inner_stats*
             E.db[2] = 17;
             TRY(c, cl_pattern_spmm(&P, D, a->ld, 1.0, &E, a->CD, a->slab + S_LS, a->ws, (void*)c.st));
         }
-        TRY(c, cl_diag_constraint_eval(a->n, a->aval, a->ld, R, D, D, R, a->q1, D, D, a->q2, (void*)c.st));
+        if (!c.generic) {
+            TRY(c, cl_diag_constraint_eval(a->n, a->aval, a->ld, R, D, D, R, a->q1, D, D, a->q2, (void*)c.st));
+        } else if (a->pair != nullptr) {
+            // single-entry constraints: R and D interleaved (AlmCore.line_search's pair branch)
+            TRY(c, cl_pair_pack(a->n, a->ld, R, a->pair, 0, (void*)c.st));
+            TRY(c, cl_pair_pack(a->n, a->ld, D, a->pair, 1, (void*)c.st));
+            TRY(c, cl_constraint_eval_pair(a->m, a->con_indptr, a->con_pi, a->con_pj, a->con_val, a->ld, a->pair,
+                                           a->q1, a->q2, (void*)c.st));
+        } else {
+            TRY(c, cl_constraint_eval(a->m, a->con_indptr, a->con_pi, a->con_pj, a->con_val, a->ld, R, D, D, R, a->q1,
+                                      D, D, a->q2, (void*)c.st));
+        }
         {
             cl_lincomb_args Lc;
             memset(&Lc, 0, sizeof(Lc));
@@ -403,7 +544,7 @@ extern "C" int cl_alm_inner_diag(const cl_alm_inner_args* a, cl_alm_inner_stats*
                 Lc.da[k] = da[k];
                 Lc.db[k] = db[k];
             }
-            TRY(c, cl_lincomb(&Lc, a->n, a->slab + S_MV, a->ws, (void*)c.st));
+            TRY(c, cl_lincomb(&Lc, c.M, a->slab + S_MV, a->ws, (void*)c.st));
         }
         if (!fetch(c, S_MV + 5)) break;
         for (int k = 0; k < nt; ++k) hist.set(Dn, tb[k], a->host[S_DIR + k]);
@@ -512,3 +653,5 @@ extern "C" int cl_alm_inner_diag(const cl_alm_inner_args* a, cl_alm_inner_stats*
     out->err_line = c.line;
     return c.rc;
 }
+
+}  // namespace

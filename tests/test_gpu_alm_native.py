@@ -133,3 +133,27 @@ def test_fused_inner_reduce_factor_exit_and_times():
     t1 = time.perf_counter()
     assert times and all(t0 - 1e-3 <= t <= t1 + 1e-3 for t in times)
     assert all(u <= v for u, v in zip(times, times[1:]))
+
+
+@pytest.mark.parametrize("case,memory,iters", [("completion", 8, 120), ("completion", 3, 40), ("sdpa", 8, 60)])
+def test_native_generic_inner_bit_identical(case, memory, iters):
+    """cl_alm_inner_generic (general constraints: matrix completion with the pair-buffer line
+    search, a dense-constraint SDPA instance) against the Python-driven generic loop."""
+    from paper_2407_15049_b200 import graphs, problem
+    if case == "completion":
+        p = problem.build_matrix_completion(graphs.random_completion(400, 350, 9000, seed=memory))
+    else:
+        from tests._golden import load, problem_from
+        p = problem_from(load("solve_random_sdp.npz"))
+    a = _run(True, p, iters, memory, 2)
+    from paper_2407_15049_b200 import alm
+    alm.NATIVE_GENERIC = False
+    try:
+        b = _run(True, p, iters, memory, 2)
+    finally:
+        alm.NATIVE_GENERIC = True
+    assert a[1] == b[1] and a[1] > 0
+    assert a[0].tobytes() == b[0].tobytes()
+    assert a[4].tobytes() == b[4].tobytes()
+    assert a[2] == b[2] and a[3] == b[3]
+    assert a[5] == b[5]
