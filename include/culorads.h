@@ -372,6 +372,51 @@ typedef struct {
 
 int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats* out);
 
+/* One ADMM step (admm.py:136) for general constraints (matrix completion, SDPA
+ * instances), single GPU: the launches of the Python host path (admm.admm_step's
+ * generic branch with HalfStep.rhs / .cg / .apply: the right-hand side over Omega with
+ * assembled coefficients, CG with the single-entry operator -- on the pair buffer when
+ * `pair` is set -- or constraint pass + Omega_A product, the dual ascent in place), with
+ * its scalar decisions in native code: bit-identical iterates. Writes U_new, V_new (always:
+ * a CG that stops at its start copies the start), ax_new = A(U_new V_new^T) and lam (in
+ * place). Stats as cl_admm_step_diag (status 1: non-finite curvature, 2: non-positive
+ * curvature, 3: non-finite iterate; bad_half 0/1 = U/V). */
+typedef struct {
+    int64_t n, m;
+    int32_t ld;
+    const double* b;
+    double* lam;               /* updated in place: lam + rho (A(U_new V_new^T) - b) */
+    const double* ax;          /* A(U V^T) of the step start, or NULL (recomputed into ax_new) */
+    double* ax_new;
+    const double* U;
+    const double* V;
+    double* U_new;
+    double* V_new;
+    double* rhs;               /* n x ld */
+    double* r;                 /* CG vectors, n x ld */
+    double* p;
+    double* Q;
+    double* y;                 /* m-vector scratch (residual; the operator's constraint values) */
+    double* nlam;              /* m-vector scratch */
+    double* rhob;              /* m-vector scratch */
+    double* pair;              /* n x 2ld pair buffer [p | Wf] (single-entry operator), or NULL */
+    const int64_t* con_indptr; /* constraint CSR with resolved positions */
+    const int32_t* con_pi;
+    const int32_t* con_pj;
+    const double* con_val;
+    cl_pattern omega;          /* Omega (cv + adjoint rows, scratch) */
+    cl_pattern apat;           /* Omega_A (adjoint rows, scratch) */
+    const double* single_a;    /* Omega_A slot coefficients of single-entry constraints, or NULL */
+    double rho, scale, binf, rel_floor, primal_coeff;
+    int32_t cg_cap;
+    double* slab;              /* 8 device doubles */
+    double* host;              /* 8 pinned host doubles */
+    double* ws;
+    void* stream;
+} cl_admm_generic_args;
+
+int cl_admm_step_generic(const cl_admm_generic_args* a, cl_admm_step_stats* out);
+
 /* ALM inner solve (alm.py:268 alm_inner) for diagonal constraints: the
  * iteration of the Python host path (vector-free L-BFGS over a host Gram
  * matrix, exact quartic line search, fused step/gradient/Gram-row update)

@@ -55,7 +55,7 @@ def barrier_timeout(rc, what):
 
 EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint_eval_halo", "cl_constraint_eval_pair",
            "cl_diag_constraint_eval", "cl_sddmm",
-           "cl_gather_rows", "cl_diag_cg_apply", "cl_diag_cg_apply_rows", "cl_diag_cg_step", "cl_cg_step", "cl_cg_step_dev", "cl_admm_step_diag", "cl_admm_step_diag_fused", "cl_alm_inner_diag", "cl_alm_inner_diag_fused", "cl_alm_inner_generic",
+           "cl_gather_rows", "cl_diag_cg_apply", "cl_diag_cg_apply_rows", "cl_diag_cg_step", "cl_cg_step", "cl_cg_step_dev", "cl_admm_step_diag", "cl_admm_step_diag_fused", "cl_admm_step_generic", "cl_alm_inner_diag", "cl_alm_inner_diag_fused", "cl_alm_inner_generic",
            "cl_diag_admm_cg_init", "cl_diag_admm_step_end", "cl_diag_admm_step_end_rows", "cl_single_entry_apply", "cl_single_entry_apply_pair", "cl_pair_pack", "cl_cg_direction_pair", "cl_lanczos_loop", "cl_lanczos_loop_fused",
            "cl_pattern_assemble", "cl_lanczos_update",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
@@ -114,6 +114,15 @@ class AdmmDiagArgs(ctypes.Structure):
                 ("want_balance", I32), ("dist", ctypes.POINTER(DistHooks))]
 
 
+class AdmmGenericArgs(ctypes.Structure):
+    _fields_ = [("n", I64), ("m", I64), ("ld", I32), ("b", P), ("lam", P), ("ax", P), ("ax_new", P),
+                ("U", P), ("V", P), ("U_new", P), ("V_new", P), ("rhs", P), ("r", P), ("p", P), ("Q", P),
+                ("y", P), ("nlam", P), ("rhob", P), ("pair", P), ("con_indptr", P), ("con_pi", P), ("con_pj", P),
+                ("con_val", P), ("omega", Pattern), ("apat", Pattern), ("single_a", P), ("rho", D), ("scale", D),
+                ("binf", D), ("rel_floor", D), ("primal_coeff", D), ("cg_cap", I32), ("slab", P), ("host", P),
+                ("ws", P), ("stream", P)]
+
+
 class AdmmStepStats(ctypes.Structure):
     _fields_ = [("it_u", I32), ("it_v", I32), ("res_u", D), ("res_v", D), ("eps_u", D), ("eps_v", D),
                 ("pnorm2", D), ("hit_cap", I32), ("status", I32), ("bad_half", I32), ("bad_is_new", I32),
@@ -168,6 +177,7 @@ def _declare(lib):
     lib.cl_diag_cg_step.argtypes = [I64, I32, D, P, P, D, D, P, P, P, P, P, P, P, P]
     lib.cl_admm_step_diag.argtypes = [ctypes.POINTER(AdmmDiagArgs), ctypes.POINTER(AdmmStepStats)]
     lib.cl_admm_step_diag_fused.argtypes = [ctypes.POINTER(AdmmDiagArgs), ctypes.POINTER(AdmmStepStats)]
+    lib.cl_admm_step_generic.argtypes = [ctypes.POINTER(AdmmGenericArgs), ctypes.POINTER(AdmmStepStats)]
     lib.cl_alm_inner_diag.argtypes = [ctypes.POINTER(AlmInnerArgs), ctypes.POINTER(AlmInnerStats)]
     lib.cl_alm_inner_diag_fused.argtypes = [ctypes.POINTER(AlmInnerArgs), ctypes.POINTER(AlmInnerStats)]
     lib.cl_alm_inner_generic.argtypes = [ctypes.POINTER(AlmInnerArgs), ctypes.POINTER(AlmInnerStats)]

@@ -337,6 +337,7 @@ def _resid(ops, ax, res, at):
 # single-entry constraints: CG operator on the pair buffer [p | Wf] (cl_single_entry_apply_pair)
 PAIR = os.environ.get("CULORADS_PAIR", "1") != "0"
 NATIVE = True     # diagonal constraints: run the step's control flow in C++ (row-sharded: with hooks)
+NATIVE_GENERIC = True   # other constraint families on one GPU: cl_admm_step_generic
 # Problems with at most this many row-lanes (n times the lanes that share a factor row,
 # lanes_for(ld)) run each ADMM step as one cooperative launch (cl_admm_step_diag_fused):
 # there, latency rather than HBM bounds the step (measured crossover).
@@ -563,6 +564,64 @@ def _admm_step_diag_py(state, ops, scale, cg_cap, rel_floor, coeff, hs, pool):
     return StepStats(st_u[2], st_v[2], st_u[3], st_v[3], bool(hit_cap))
 
 
+def _admm_step_generic_native(state, ops, scale, cg_cap, rel_floor, coeff, hs, pool):
+    """admm_step's generic branch below through cl_admm_step_generic: the same launches,
+    the scalar decisions in native code (bit-identical iterates)."""
+    from . import _lib
+    dev = ops.dev
+    p = ops.problem
+    n, ld = state.U.shape
+    a = getattr(hs, "generic_args", None)
+    if a is None:
+        a = hs.generic_args = _lib.AdmmGenericArgs()
+        con = ops.cop.con
+        apat = ops.adj.apat
+        a.n, a.m, a.ld = n, p.m, ld
+        a.b = ops.b.data_ptr()
+        hs.rhs_buf = dev.empty(n, ld)
+        hs.ax_bufs = [dev.empty(p.m), dev.empty(p.m)]
+        a.rhs, a.r, a.p, a.Q = hs.rhs_buf.data_ptr(), hs.r.data_ptr(), hs.p.data_ptr(), hs.Q.data_ptr()
+        a.y, a.nlam, a.rhob = hs.y.data_ptr(), hs.nlam.data_ptr(), hs.rhob.data_ptr()
+        single = apat.single_a is not None and apat.halo is None and ld <= 64
+        a.single_a = apat.single_a.data_ptr() if single else None
+        if single and PAIR:
+            if getattr(hs, "P2", None) is None:
+                hs.P2 = dev.empty(n, 2 * ld)
+            a.pair = hs.P2.data_ptr()
+        a.con_indptr, a.con_pi, a.con_pj, a.con_val = (con.indptr.data_ptr(), con.pi.data_ptr(),
+                                                       con.pj.data_ptr(), con.val.data_ptr())
+        a.omega = ops.adj.omega.struct(c_coeff=1.0, w1=hs.nlam, w2=hs.rhob)
+        a.apat = apat.struct(c_coeff=None, w1=hs.y)
+        a.binf = float(p.b_norminf)
+        a.slab = dev.slot(480).value
+        a.host = dev.host.data_ptr() + 8 * 480
+        a.ws, a.stream = dev.ws.data_ptr(), dev.stream.cuda_stream
+    a.lam = state.dual.lam.data_ptr()
+    a.ax = state.ax.data_ptr() if state.ax is not None else None
+    ax_new = hs.ax_bufs[0] if hs.ax_bufs[0] is not state.ax else hs.ax_bufs[1]
+    a.ax_new = ax_new.data_ptr()
+    U_new = pool.get() if pool else dev.empty(n, ld)
+    V_new = pool.get() if pool else dev.empty(n, ld)
+    a.U, a.V, a.U_new, a.V_new = state.U.data_ptr(), state.V.data_ptr(), U_new.data_ptr(), V_new.data_ptr()
+    a.rho, a.scale = float(state.dual.rho), float(scale)
+    a.rel_floor, a.primal_coeff, a.cg_cap = float(rel_floor), float(coeff), int(cg_cap)
+    st = _lib.AdmmStepStats()
+    rc = dev.lib.cl_admm_step_generic(ctypes.byref(a), ctypes.byref(st))
+    dev.launches += 12 + 4 * (st.it_u + st.it_v)
+    _lib.check(rc, f"cl_admm_step_generic (admm_native.cu:{st.err_line})")
+    if st.status:
+        last = U_new if st.bad_half == 0 else V_new
+        if st.status == 2:
+            raise SpdViolationError(f"non-positive curvature {st.pq_bad:.3e} in CG (operator not SPD)")
+        raise DivergedError("CG produced non-finite curvature" if st.status == 1 else "CG iterate diverged",
+                            last_iterate=last)
+    state.set_factors(U=U_new)
+    state.set_factors(V=V_new)
+    state.ax = ax_new
+    state.last_pnorm2 = float(st.pnorm2)
+    return StepStats(st.it_u, st.it_v, st.res_u, st.res_v, bool(st.hit_cap))
+
+
 def admm_step(state: AdmmState, ops, *, scale=1.0, cg_cap=200, cg_rel_floor=1e-10,
               cg_primal_coeff=0.05, hs=None, pool=None) -> StepStats:
     """U half-solve, V half-solve, dual ascent (admm.py:136)."""
@@ -573,6 +632,12 @@ def admm_step(state: AdmmState, ops, *, scale=1.0, cg_cap=200, cg_rel_floor=1e-1
         if NATIVE:
             return _admm_step_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, hs, pool)
         return _admm_step_diag_py(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, hs, pool)
+    if (NATIVE and NATIVE_GENERIC and dev.world == 1 and getattr(ops, "row_range", None) is None
+            and getattr(ops.cop.con, "halo", None) is None and ops.adj.omega.halo is None
+            and isinstance(state.dual.lam, torch.Tensor)):
+        n, ld = state.U.shape
+        hs = hs or HalfStep(ops, n, ld)
+        return _admm_step_generic_native(state, ops, scale, cg_cap, cg_rel_floor, cg_primal_coeff, hs, pool)
     p = ops.problem
     dual = state.dual
     rho = dual.rho

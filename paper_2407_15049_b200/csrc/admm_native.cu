@@ -333,3 +333,270 @@ extern "C" int cl_admm_step_diag(const cl_admm_diag_args* a, cl_admm_step_stats*
     return c.rc;
 #undef RET_RC
 }
+
+// ---------------------------------------------------------------------------
+// general constraints (cl_admm_step_generic): admm.admm_step's generic branch
+// ---------------------------------------------------------------------------
+
+namespace {
+
+struct GCtx {
+    const cl_admm_generic_args* a;
+    cudaStream_t st;
+    int rc;
+    int64_t N;   // n * ld
+    int line;
+};
+
+// slots inside the caller's slab
+enum { G_PM = 0, G_RHSU = 1, G_RHSV = 2, G_QR = 3, G_PQ = 4, G_QN = 5, G_XX = 6, G_SCR = 7 };
+
+bool gfetch(GCtx& c, int lo, int cnt) {
+    if (c.rc) return false;
+    cudaError_t e = cudaMemcpyAsync(c.a->host + lo, c.a->slab + lo, cnt * sizeof(double), cudaMemcpyDeviceToHost,
+                                    c.st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.st);
+    if (e != cudaSuccess) {
+        c.rc = (int)e;
+        c.line = __LINE__;
+        return false;
+    }
+    return true;
+}
+
+// cl_lincomb in mode PAIRS with at most one dot (da, db); dot_slot < 0: none
+void glin(GCtx& c, double* out, int nin, const double* const* in, const double* coef, int64_t N, int dot_slot,
+          uint8_t da = CL_OUT, uint8_t db = CL_OUT) {
+    cl_lincomb_args L;
+    memset(&L, 0, sizeof(L));
+    L.nin = nin;
+    L.mode = CL_DOT_PAIRS;
+    for (int j = 0; j < nin; ++j) {
+        L.in[j] = in[j];
+        L.coef[j] = coef[j];
+    }
+    L.out = out;
+    if (dot_slot >= 0) {
+        L.ndot = 1;
+        L.da[0] = da;
+        L.db[0] = db;
+    }
+    CL_TRY(c, cl_lincomb(&L, N, dot_slot >= 0 ? c.a->slab + dot_slot : nullptr, c.a->ws, (void*)c.st));
+}
+
+void gconstraint(GCtx& c, const double* X, const double* Y, double* out) {
+    const cl_admm_generic_args* a = c.a;
+    CL_TRY(c, cl_constraint_eval(a->m, a->con_indptr, a->con_pi, a->con_pj, a->con_val, a->ld, X, Y, nullptr, nullptr,
+                                 out, nullptr, nullptr, nullptr, (void*)c.st));
+}
+
+bool single_entry(const cl_admm_generic_args* a) { return a->single_a != nullptr && a->ld <= 64; }
+
+// HalfStep.apply: out = rho (A*(A(W Wf^T)) Wf + W); <W, out> -> slab[dot_slot] (dot_slot < 0: none)
+void gapply(GCtx& c, const double* W, const double* Wf, double* out, int dot_slot) {
+    const cl_admm_generic_args* a = c.a;
+    if (single_entry(a)) {
+        CL_TRY(c, cl_single_entry_apply(a->apat.nrows, a->apat.indptr, a->apat.indices, a->single_a, a->ld, W, Wf,
+                                        a->rho, out, a->slab + (dot_slot >= 0 ? dot_slot : G_SCR), a->ws,
+                                        (void*)c.st));
+        return;
+    }
+    gconstraint(c, W, Wf, a->y);
+    cl_pattern P = a->apat;
+    P.cv = nullptr;
+    P.c_coeff = 0.0;
+    P.w1 = a->y;
+    P.w2 = nullptr;
+    cl_epilogue E;
+    memset(&E, 0, sizeof(E));
+    E.ny = 1;
+    E.Y[0] = W;
+    E.ycoef[0] = a->rho;
+    if (dot_slot >= 0) {
+        E.ndot = 1;
+        E.da[0] = 0;        // Y[0] = W
+        E.db[0] = CL_OUT;
+    }
+    CL_TRY(c, cl_pattern_spmm(&P, Wf, a->ld, a->rho, &E, out, dot_slot >= 0 ? a->slab + dot_slot : nullptr,
+                              dot_slot >= 0 ? a->ws : nullptr, (void*)c.st));
+}
+
+// HalfStep.rhs: out = S_b Wf + rho Wf, S_b = -scale C - A*(lam) + rho A*(b); ||out||^2 -> slab[slot]
+void grhs(GCtx& c, const double* Wf, double* out, int slot) {
+    const cl_admm_generic_args* a = c.a;
+    {
+        const double* in[1] = {a->lam};
+        const double cf[1] = {-1.0};
+        glin(c, a->nlam, 1, in, cf, a->m, -1);
+    }
+    {
+        const double* in[1] = {a->b};
+        const double cf[1] = {a->rho};
+        glin(c, a->rhob, 1, in, cf, a->m, -1);
+    }
+    cl_pattern P = a->omega;
+    P.c_coeff = -a->scale;
+    P.w1 = a->nlam;
+    P.w2 = a->rhob;
+    cl_epilogue E;
+    memset(&E, 0, sizeof(E));
+    E.ny = 1;
+    E.Y[0] = Wf;
+    E.ycoef[0] = a->rho;
+    E.ndot = 1;
+    E.da[0] = CL_OUT;
+    E.db[0] = CL_OUT;
+    CL_TRY(c, cl_pattern_spmm(&P, Wf, a->ld, 1.0, &E, out, a->slab + slot, a->ws, (void*)c.st));
+}
+
+// HalfStep.cg (admm.py:65): x = x0, then CG on the half-step operator. Returns 0, or the
+// failure status (1 non-finite curvature, 2 non-positive curvature, 3 non-finite iterate).
+int gcg(GCtx& c, double* x, const double* x0, const double* Wf, const double* rhs, double eps, int* its_out,
+        double* rnorm_out, double* pq_bad) {
+    const cl_admm_generic_args* a = c.a;
+    int its = 0;
+    {
+        const double* in[1] = {x0};
+        const double cf[1] = {1.0};
+        glin(c, x, 1, in, cf, c.N, -1);
+    }
+    gapply(c, x, Wf, a->Q, -1);
+    {
+        const double* in[2] = {rhs, a->Q};
+        const double cf[2] = {1.0, -1.0};
+        glin(c, a->r, 2, in, cf, c.N, G_QR);
+    }
+    if (!gfetch(c, G_QR, 1)) return 0;
+    double qr = a->host[G_QR];
+    double rnorm = sqrt(qr);
+    *its_out = 0;
+    *rnorm_out = rnorm;
+    if (rnorm <= eps) return 0;
+    {
+        const double* in[1] = {a->r};
+        const double cf[1] = {1.0};
+        glin(c, a->p, 1, in, cf, c.N, -1);
+    }
+    const bool pair = a->pair != nullptr && single_entry(a);
+    if (pair) {
+        CL_TRY(c, cl_pair_pack(a->n, a->ld, Wf, a->pair, 1, (void*)c.st));
+        CL_TRY(c, cl_pair_pack(a->n, a->ld, a->p, a->pair, 0, (void*)c.st));
+    }
+    for (int k = 0; k < a->cg_cap; ++k) {
+        if (pair)
+            CL_TRY(c, cl_single_entry_apply_pair(a->apat.nrows, a->apat.indptr, a->apat.indices, a->single_a, a->ld,
+                                                 a->pair, a->rho, a->Q, a->slab + G_PQ, a->ws, (void*)c.st));
+        else
+            gapply(c, a->p, Wf, a->Q, G_PQ);
+        CL_TRY(c, cl_cg_step_dev(c.N, qr, a->slab + G_PQ, x, x, a->p, a->r, a->Q, a->slab + G_QN, a->ws,
+                                 (void*)c.st));
+        if (!gfetch(c, G_PQ, 2)) return 0;
+        const double pq = a->host[G_PQ];
+        if (!isfinite(pq)) {
+            *pq_bad = pq;
+            *its_out = its;
+            return 1;
+        }
+        if (pq <= 0.0) {
+            *pq_bad = pq;
+            *its_out = its;
+            return 2;
+        }
+        const double qn = a->host[G_QN];
+        rnorm = sqrt(qn);
+        its = k + 1;
+        if (rnorm <= eps) break;
+        if (pair) {
+            CL_TRY(c, cl_cg_direction_pair(a->n, a->ld, qn / qr, a->r, a->p, a->pair, (void*)c.st));
+        } else {
+            const double* in[2] = {a->r, a->p};
+            const double cf[2] = {1.0, qn / qr};
+            glin(c, a->p, 2, in, cf, c.N, -1);
+        }
+        qr = qn;
+    }
+    {
+        const double* in[1] = {x};
+        const double cf[1] = {0.0};
+        glin(c, nullptr, 1, in, cf, c.N, G_XX, 0, 0);
+    }
+    *its_out = its;
+    *rnorm_out = rnorm;
+    if (!gfetch(c, G_XX, 1)) return 0;
+    if (!isfinite(a->host[G_XX])) return 3;
+    return 0;
+}
+
+}  // namespace
+
+extern "C" int cl_admm_step_generic(const cl_admm_generic_args* a, cl_admm_step_stats* out) {
+    if (a == nullptr || out == nullptr || a->n < 0 || a->m < 0 || a->ld < 2 || (a->ld & 1) || a->cg_cap < 0 ||
+        a->ax_new == nullptr || a->U_new == nullptr || a->V_new == nullptr || a->omega.indptr == nullptr ||
+        a->apat.indptr == nullptr)
+        return CL_EARG;
+    GCtx c;
+    c.a = a;
+    c.st = reinterpret_cast<cudaStream_t>(a->stream);
+    c.rc = 0;
+    c.line = 0;
+    c.N = a->n * (int64_t)a->ld;
+    memset(out, 0, sizeof(*out));
+    out->du2 = out->dv2 = -1.0;
+#define GRET()                  \
+    do {                        \
+        out->err_line = c.line; \
+        return c.rc;            \
+    } while (0)
+    const double* ax = a->ax;
+    if (ax == nullptr) {
+        gconstraint(c, a->U, a->V, a->ax_new);
+        ax = a->ax_new;
+    }
+    {
+        const double* in[2] = {ax, a->b};
+        const double cf[2] = {1.0, -1.0};
+        glin(c, a->y, 2, in, cf, a->m, G_PM);
+    }
+    if (!gfetch(c, G_PM, 1)) GRET();
+    const double pmeas = sqrt(a->host[G_PM]) / (1.0 + a->binf);
+    const double yv = a->primal_coeff * pmeas;
+    const double mn = (yv < 1e-2) ? yv : 1e-2;
+    const double rel = (mn > a->rel_floor) ? mn : a->rel_floor;
+    double pqb = 0.0;
+
+    grhs(c, a->V, a->rhs, G_RHSU);
+    if (!gfetch(c, G_RHSU, 1)) GRET();
+    out->eps_u = pymax_tiny(rel * sqrt(a->host[G_RHSU]));
+    int s = gcg(c, a->U_new, a->U, a->V, a->rhs, out->eps_u, &out->it_u, &out->res_u, &pqb);
+    if (c.rc) GRET();
+    if (s) {
+        fail(out, s, 0, 1, pqb);
+        GRET();
+    }
+    grhs(c, a->U_new, a->rhs, G_RHSV);
+    if (!gfetch(c, G_RHSV, 1)) GRET();
+    out->eps_v = pymax_tiny(rel * sqrt(a->host[G_RHSV]));
+    s = gcg(c, a->V_new, a->V, a->U_new, a->rhs, out->eps_v, &out->it_v, &out->res_v, &pqb);
+    if (c.rc) GRET();
+    if (s) {
+        fail(out, s, 1, 1, pqb);
+        GRET();
+    }
+    gconstraint(c, a->U_new, a->V_new, a->ax_new);
+    {
+        const double* in[2] = {a->ax_new, a->b};
+        const double cf[2] = {1.0, -1.0};
+        glin(c, a->y, 2, in, cf, a->m, G_PM);
+    }
+    {
+        const double* in[2] = {a->lam, a->y};
+        const double cf[2] = {1.0, a->rho};
+        glin(c, a->lam, 2, in, cf, a->m, -1);
+    }
+    if (!gfetch(c, G_PM, 1)) GRET();
+    out->pnorm2 = a->host[G_PM];
+    out->hit_cap = (out->it_u >= a->cg_cap && out->res_u > out->eps_u) ||
+                   (out->it_v >= a->cg_cap && out->res_v > out->eps_v);
+    GRET();
+#undef GRET
+}

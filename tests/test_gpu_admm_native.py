@@ -158,3 +158,26 @@ def test_fused_step_returns_balance_measures():
     st.want_balance = False
     admm.admm_step(st, ops, scale=0.7, hs=hs, pool=pool, cg_cap=50)
     assert st.step_bal is None
+
+
+@pytest.mark.parametrize("case,r", [("completion", 6), ("completion", 26), ("sdpa", 4)])
+def test_native_generic_step_bit_identical(case, r):
+    """cl_admm_step_generic (general constraints: matrix completion on the pair-buffer
+    single-entry operator, a dense-constraint SDPA instance on constraint pass + Omega_A
+    product) against the Python-driven generic step."""
+    from paper_2407_15049_b200 import admm, graphs, problem
+    if case == "completion":
+        p = problem.build_matrix_completion(graphs.random_completion(500, 420, 10000, seed=r))
+    else:
+        from tests._golden import load, problem_from
+        p = problem_from(load("solve_random_sdp.npz"))
+    a = _run_steps(True, p, 8, r=r, seed=3)
+    admm.NATIVE_GENERIC = False
+    try:
+        b = _run_steps(True, p, 8, r=r, seed=3)
+    finally:
+        admm.NATIVE_GENERIC = True
+    assert sum(s[0] + s[1] for s in a[3]) > 0
+    for x, y in zip(a[:3], b[:3]):
+        assert x.tobytes() == y.tobytes()
+    assert a[3] == b[3]
