@@ -677,7 +677,23 @@ def run_ours(args, rank, world, local_rank):
             e_ms = (time.perf_counter() - te) * 1e3 / K
         if world > 1:
             e_ms = _max_over_ranks(e_ms)
+        # the copy floor of a step: the same H2D and D2H bytes on the two copy streams alone
+        with torch.cuda.stream(st):
+            def copies_only():
+                with torch.cuda.stream(s_in):
+                    R_dev[0].copy_(R_pin, non_blocking=True)
+                    lam_dev[0].copy_(lam_pin, non_blocking=True)
+                with torch.cuda.stream(s_out):
+                    out_pin[1].copy_(R_dev[1], non_blocking=True)
+            copies_only()
+            torch.cuda.synchronize()
+            tc = time.perf_counter()
+            for _ in range(3):
+                copies_only()
+            torch.cuda.synchronize()
+            floor_ms = (time.perf_counter() - tc) * 1e3 / 3
         e2e = {"value": step_bytes_all / (e_ms * 1e-3) / 1e9, "unit": UNIT,
+               "copy_floor_ms": floor_ms, "frac_of_copy_floor": floor_ms / e_ms,
                "ms_per_step": e_ms, "h2d_bytes_per_step": int(R_host.nbytes + lam_host.nbytes),
                "d2h_bytes_per_step": int(n * r * 8),
                "path": "alm.alm_gradient (reference alm.py:239 signature) on pinned host R, lam; "
