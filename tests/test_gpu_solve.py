@@ -124,3 +124,25 @@ def test_reorder_skipped_for_random_graphs():
     a = driver.solve(p, driver.SolverConfig(deterministic=True))
     b = driver.solve(p, driver.SolverConfig(deterministic=True, reorder=True))
     assert trace_array(a.trace_rows).tobytes() == trace_array(b.trace_rows).tobytes()
+
+
+def test_memory_guard_caps_rank_escalation():
+    """SolverConfig.memory_budget: an escalation whose stage buffers would not fit is refused
+    like one at the sqrt(2m) cap -- the solve continues at its rank and reports it -- instead
+    of failing out of memory."""
+    import torch
+    from paper_2407_15049_b200 import driver, graphs, linops, problem
+    p = problem.build_maxcut(graphs.random_sparse(3000, deg=8.0, seed=2))
+    cfg = dict(alm_inner_cap=20, alm_outer_cap=8, admm_step_cap=30, max_reopts=0)
+    free = driver.SolverConfig(**cfg)
+    rep = driver.solve(p, free)
+    assert len(rep.rank_history) > 1 and not rep.memory_capped       # this run escalates
+    ops = linops.build_operators(p)
+    torch.cuda.synchronize()
+    r0 = driver.initial_rank(p.m, p.n)
+    base = torch.cuda.memory_allocated()
+    budget = base + driver.factor_bytes_needed(p.n, p.m, r0, 8) + 4 * 2 ** 20   # r0 fits, nothing more
+    capped = driver.solve(p, driver.SolverConfig(memory_budget=budget, **cfg), ops=ops)
+    assert capped.memory_capped and capped.rank_history == [r0]
+    assert capped.memory_rank_refused == rep.rank_history[1]
+    assert capped.status in ("best_effort", "optimal", "timeout") and capped.rank_final == r0
