@@ -179,6 +179,110 @@ class HaloPlan:
         return (self.world - 1) * self.maxb * ld * 8
 
 
+def _all_to_all_v(out, inp, out_splits, in_splits, group=None):
+    """all_to_all_single with split sizes; CUDA tensors on gloo are staged through the host."""
+    if inp.is_cuda and not _nccl(group):
+        h_out = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(h_out, inp.cpu(), out_splits, in_splits, group=group)
+        out.copy_(h_out)
+        return out
+    dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+    return out
+
+
+class PeerHaloPlan:
+    """Point-to-point halo of one contiguously partitioned row space: rank r receives from
+    each rank s exactly the rows of s that r's pattern rows reference (one all-to-all with
+    split sizes), instead of every rank's whole publish list (HaloPlan's all-gather).
+
+    On a uniformly random graph a rank's rows reference about half of any other block,
+    while every row of it is referenced by some rank, so the all-gather moves (N-1)/N of
+    the factor to every rank and this plan about half of that: half the NVLink bytes and
+    half the receive buffer. Same interface as HaloPlan: ``local_indices`` (owned columns
+    in [0, nown), remote column j at nown + its rank among this rank's needed ids -- the
+    receive layout is ordered by owner, and the blocks are contiguous, so that is the sorted
+    order), ``remap``, ``exchange``, ``halo_bytes``, ``halo_rows`` (receive rows), ``maxb``
+    (send rows), ``counts`` (every rank's receive rows), ``publish`` (rows sent)."""
+
+    def __init__(self, lo, hi, indptr, indices, bounds, rank, world, group=None):
+        self.lo, self.hi, self.rank, self.world, self.group = lo, hi, rank, world, group
+        self.nown = hi - lo
+        self.bounds = bounds
+        dev = indices.device
+        indices = indices.to(I64)
+        own = (indices >= lo) & (indices < hi)
+        self.need = torch.unique(indices[~own])                       # sorted global ids
+        bt = torch.tensor(bounds, dtype=I64, device=dev)
+        owner = torch.searchsorted(bt, self.need, right=True) - 1
+        recv = torch.bincount(owner, minlength=world).to(I64)
+        send = torch.empty_like(recv)
+        _all_to_all_v(send, recv, [1] * world, [1] * world, group)
+        self.recv_counts = recv.cpu().tolist()
+        self.send_counts = send.cpu().tolist()
+        ids = torch.empty(sum(self.send_counts), dtype=I64, device=dev)
+        _all_to_all_v(ids, self.need, self.send_counts, self.recv_counts, group)
+        if ids.numel() and not bool(((ids >= lo) & (ids < hi)).all()):
+            raise ValueError("peer halo: a rank requested rows outside this block")
+        self.publish = (ids - lo).to(I32).contiguous()                # rows sent, destination-major
+        self.halo_rows = int(sum(self.recv_counts))
+        self.maxb = max(1, int(sum(self.send_counts)))
+        tot = torch.tensor([self.halo_rows], dtype=I64, device=dev)
+        self.counts = _all_gather_1d(tot, world, group).view(-1).cpu().tolist()
+        if self.nown + self.halo_rows >= 2 ** 31:
+            raise ValueError("owned block plus halo exceeds int32 indices")
+        self.local_indices = self.remap(indices).to(I32).contiguous()
+        self._bufs = {}
+
+    def remap(self, ids):
+        ids = ids.to(I64)
+        own = (ids >= self.lo) & (ids < self.hi)
+        out = ids - self.lo
+        remote = ids[~own]
+        if remote.numel():
+            need = self.need.to(ids.device)
+            pos = torch.searchsorted(need, remote).clamp(max=max(need.numel() - 1, 0))
+            if need.numel() == 0 or not bool((need[pos] == remote).all()):
+                raise ValueError("a referenced remote index is missing from this rank's peer halo")
+            out[~own] = self.nown + pos
+        return out
+
+    def buffers(self, ld, like, slot=0):
+        key = (ld, like.device, slot)
+        b = self._bufs.get(key)
+        if b is None:
+            for k in [k for k in self._bufs if k[0] != ld]:
+                del self._bufs[k]
+            send = torch.zeros((max(1, self.publish.numel()), ld), dtype=like.dtype, device=like.device)
+            recv = torch.zeros((max(1, self.halo_rows), ld), dtype=like.dtype, device=like.device)
+            b = self._bufs[key] = (send, recv)
+        return b
+
+    def exchange(self, X, ld, pack, slot=0):
+        """Pack the rows each peer needs (destination-major) and exchange them all-to-all."""
+        send, recv = self.buffers(ld, X, slot)
+        if self.publish.numel():
+            pack(self.publish, X.reshape(-1, ld), send)
+        _all_to_all_v(recv.view(-1)[:self.halo_rows * ld], send.view(-1)[:self.publish.numel() * ld],
+                      [c * ld for c in self.recv_counts], [c * ld for c in self.send_counts], self.group)
+        return recv
+
+    def halo_bytes(self, ld):
+        return self.halo_rows * ld * 8
+
+
+def make_halo_plan(lo, hi, indptr, indices, bounds, rank, world, group=None, mode="auto"):
+    """The halo plan of a symmetric pattern's row block: the all-gather plan (HaloPlan) or the
+    point-to-point one (PeerHaloPlan), whichever receives fewer rows on the worst rank
+    ("auto"; every rank takes the same decision)."""
+    if mode == "allgather" or world == 1:
+        return HaloPlan(lo, hi, indptr, indices, bounds, rank, world, group)
+    peer = PeerHaloPlan(lo, hi, indptr, indices, bounds, rank, world, group)
+    if mode == "p2p":
+        return peer
+    ag = HaloPlan(lo, hi, indptr, indices, bounds, rank, world, group)
+    return peer if max(peer.counts) < world * ag.maxb else ag
+
+
 def torch_pack(idx, X, out):
     """Reference packing (tests): out[i] = X[idx[i]]."""
     out[:idx.numel()] = X[idx.long()]
@@ -253,7 +357,7 @@ def sharded_maxcut_ops(n_global, deg, seed, rank, world, dev, group=None):
     indptr, cols, vals = maxcut_rows(n_global, eu, ev, lo, hi)
     n_edges = int(eu.numel())
     del eu, ev
-    plan = HaloPlan(lo, hi, indptr, cols, b, rank, world, group)
+    plan = make_halo_plan(lo, hi, indptr, cols, b, rank, world, group)
     pad_ptr = torch.zeros(nown + 1 + 16, dtype=I64, device=dev.dev)
     pad_ptr[:nown + 1] = indptr
     cpat = DevicePattern(nown, pad_ptr[:nown + 1], padded(plan.local_indices), padded(vals),
@@ -302,7 +406,7 @@ def slice_pattern(pat, lo, hi, bounds, rank, world, group, con_map=None, halo=Tr
     s0, s1 = int(ptr[lo]), int(ptr[hi])
     indptr = ptr[lo:hi + 1] - s0
     cols = pat.indices[s0:s1].to(I64)
-    plan = HaloPlan(lo, hi, indptr, cols, bounds, rank, world, group)
+    plan = make_halo_plan(lo, hi, indptr, cols, bounds, rank, world, group)
     pad_ptr = torch.zeros(hi - lo + 1 + 16, dtype=I64, device=ptr.device)
     pad_ptr[:hi - lo + 1] = indptr
     cv = padded(pat.cv[s0:s1]) if pat.cv is not None else None
@@ -367,7 +471,7 @@ def build_sharded_diag_operators(p, rank, world, dev, group=None):
     cv[slot_c] = vals
     sup_r, sup_c = sup // n, sup % n
     o_ptr = _csr_ptr(sup_r, nown)
-    plan = HaloPlan(lo, hi, o_ptr, sup_c, b, rank, world, group)
+    plan = make_halo_plan(lo, hi, o_ptr, sup_c, b, rank, world, group)
     aval = torch.as_tensor(np.ascontiguousarray(p.a_val[lo:hi], dtype=np.float64)).to(tdev)
     omega = DevicePattern(nown, o_ptr, padded(plan.local_indices), cv, _csr_ptr(slot_d, S),
                           padded(ar.to(I32)), padded(aval.clone()))
@@ -558,8 +662,13 @@ def halo_buffer_rows(ops):
     return sum(slots * (h.halo_rows + h.maxb) for h, slots in plans.values())
 
 
+def _peer_rows(n_loc, world, deg):
+    import math
+    return int((world - 1) * n_loc * (1.0 - math.exp(-max(deg, 0.0) / world)))
+
+
 def memory_model(n_global, world, r, nnz_c_per_row, m_global=None, nnz_a_per_con=1.0, halo_frac=1.0,
-                 memory=8, halo_slots=1, pair=False):
+                 memory=8, halo_slots=1, pair=False, peer=False):
     """Per-rank device bytes of a row-sharded solve at rank r.
 
     * stage buffers: driver.stage_factor_buffers(memory, pair) factors of n_loc x ld fp64
@@ -567,7 +676,10 @@ def memory_model(n_global, world, r, nnz_c_per_row, m_global=None, nnz_a_per_con
       the pair buffer of single-entry constraints);
     * halo: ``halo_slots`` receive buffers of world * maxb rows plus the send buffer,
       maxb = halo_frac * n_loc published rows (random graphs: every row has a remote
-      neighbour, halo_frac ~ 1; locality-ordered meshes: only the block-boundary band);
+      neighbour, halo_frac ~ 1; locality-ordered meshes: only the block-boundary band).
+      ``peer``: the point-to-point plan (PeerHaloPlan) on a uniformly random pattern of
+      nnz_c_per_row - 1 neighbours per row: each rank receives, and sends, the
+      1 - exp(-deg/world) share of every other block that it references;
     * operators: C rows (int32 index + fp64 value per nonzero, int64 row pointer), Omega
       (index, value, adjoint pointer per slot; constraint id + coefficient per adjoint
       entry), Omega_A and the constraint rows;
@@ -586,7 +698,8 @@ def memory_model(n_global, world, r, nnz_c_per_row, m_global=None, nnz_a_per_con
     out = {
         "n_per_rank": n_loc, "ld": ld, "factor_bytes": factor,
         "stage_buffers": stage_factor_buffers(memory, pair) * factor,
-        "halo": (halo_slots * (world * maxb) + maxb) * ld * 8 if world > 1 else 0,
+        "halo": ((halo_slots + 1) * _peer_rows(n_loc, world, nnz_c_per_row - 1) if peer
+                 else halo_slots * (world * maxb) + maxb) * ld * 8 if world > 1 else 0,
         "operators": (nnz_c * 12 + n_loc * 8) + (nnz_c + 2 * nnz_a) * 20 + nnz_a * 12 * 2 + nnz_a * 28
                      + m_loc * 8 + 2 * n_loc * 8,
         "m_vectors": 16 * 8 * m_loc,
