@@ -25,6 +25,8 @@ VARIANTS = {
     "sp1_4": ["-DSP_MINB1=4"],
     "spu12": ["-DSP_UNROLL=12"],
     "spu4": ["-DSP_UNROLL=4"],
+    "split0": ["-DSP_SPLIT_LD=0"],
+    "nosplit": ["-DSP_SPLIT_LD=100000"],
     "sp5": ["-DSP_MINB0=5"],
     "sp6": ["-DSP_MINB0=6"],
 }
