@@ -861,14 +861,8 @@ __global__ void __launch_bounds__(NT) basis_subtract_kernel(const double* __rest
 // Plain-store variant: more gathers in flight for narrow rows (12: 4.32 -> 4.12 ms for C R at
 // n = 1e7, ld 26), fewer for wide rows where one group already covers 512 bytes per gather
 // (4: 13.3 -> 12.6 ms at ld 822); the epilogue variants lose registers to more (occupancy_sweep).
-#ifndef SP_SPLIT_LD
-#define SP_SPLIT_LD 64      // wider rows run a dots-only epilogue as a separate streaming pass
-#endif
 #ifndef SP_UNROLL0
 #define SP_UNROLL0 12
-#endif
-#ifndef SP_SPLIT_LD
-#define SP_SPLIT_LD 64      // wider rows run a dots-only epilogue as a separate streaming pass
 #endif
 #ifndef SP_UNROLL0_WIDE
 #define SP_UNROLL0_WIDE 4
@@ -1802,30 +1796,6 @@ int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alp
                        E.ny <= SP_NY && E.nz <= SP_NZ && E.ndot <= SP_ND &&
                        aligned16(S->indptr) && aligned16(S->indices) &&
                        (need_asm ? aligned16(S->scratch) : aligned16(P.cv));
-    if (tiled && ld > SP_SPLIT_LD && E.ny == 0 && E.drow == nullptr && E.nz > 0 && E.ndot > 0 && out != nullptr) {
-        // Wide rows (high rank) with an epilogue of row-local dots only (the line search's
-        // C D with <CD,R>, <CD,D>, <CR,D>): the plain product, then the dots as one streaming
-        // pass. The fused epilogue re-read its Z rows chunk by chunk after each chunk's
-        // gathers and ran at 3.3 TB/s at ld 822 against 4.35 for the plain product; the
-        // split adds one read of `out` and streams the rest (profiles/r2/ncu_summary.md).
-        cl_epilogue plain;
-        memset(&plain, 0, sizeof(plain));
-        const int rc = cl_pattern_spmm(S, X, ld, alpha, &plain, out, nullptr, nullptr, stream);
-        if (rc != CL_OK) return rc;
-        cl_lincomb_args L;
-        memset(&L, 0, sizeof(L));
-        L.nin = 1 + E.nz;
-        L.mode = CL_DOT_PAIRS;
-        L.in[0] = out;
-        for (int j = 0; j < E.nz; ++j) L.in[1 + j] = E.Z[j];
-        L.out = nullptr;
-        L.ndot = E.ndot;
-        for (int d = 0; d < E.ndot; ++d) {
-            L.da[d] = E.da[d] == CL_OUT ? 0 : (uint8_t)(1 + (E.da[d] - 16));
-            L.db[d] = E.db[d] == CL_OUT ? 0 : (uint8_t)(1 + (E.db[d] - 16));
-        }
-        return cl_lincomb(&L, P.nrows * (int64_t)ld, dots_out, ws, stream);
-    }
     if (tiled) {
         // operand codes of the compact tiled epilogue: Y j -> j, out -> SP_NY, Z j -> SP_NY + 1 + j
         for (int d = 0; d < E.ndot; ++d) {
