@@ -221,38 +221,6 @@ __global__ void __launch_bounds__(NT) lincomb_kernel(LcDev a, int64_t n2, int ta
     }
 }
 
-// MODE 2 (in0·in_j, in1·in_j, no output) without holding every input: each input is
-// used as it arrives, so registers do not scale with the capacity (the MODE 2 instance of
-// lincomb_kernel needed 254 registers at 20 inputs: one CTA per SM). Each accumulator
-// receives the same products in the same element order: bit-identical dots.
-template <int KIN>
-__global__ void __launch_bounds__(NT) lincomb_first_two_kernel(LcDev a, int64_t n2, int tail, double* ws,
-                                                               double* dots_out) {
-    constexpr int ND = 2 * KIN - 1;
-    double acc[ND];
-#pragma unroll
-    for (int d = 0; d < ND; ++d) acc[d] = 0.0;
-    const int nin = a.nin;
-    const int64_t stride = (int64_t)gridDim.x * NT;
-    for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < n2 + (tail ? 1 : 0); k += stride) {
-        const bool is_tail = (k == n2);
-        const double2 v0 = !is_tail ? ld2cs(a.in[0] + 2 * k) : make_double2(a.in[0][2 * k], 0.0);
-        const double2 v1 = !is_tail ? ld2cs(a.in[1] + 2 * k) : make_double2(a.in[1][2 * k], 0.0);
-        acc[0] += dot2(v0, v0);
-        acc[1] += dot2(v0, v1);
-        acc[KIN] += dot2(v1, v1);
-#pragma unroll
-        for (int j = 2; j < KIN; ++j) {
-            if (j < nin) {
-                const double2 vj = !is_tail ? ld2cs(a.in[j] + 2 * k) : make_double2(a.in[j][2 * k], 0.0);
-                acc[j] += dot2(v0, vj);
-                acc[KIN + j - 1] += dot2(v1, vj);
-            }
-        }
-    }
-    if (a.ndot > 0) reduce_and_finish<ND>(acc, a.ndot, ws, dots_out, KIN, CL_MAXIN - KIN);
-}
-
 // ---------------------------------------------------------------------------
 // pattern (CSR over positions) times factor, fused coefficient assembly
 // ---------------------------------------------------------------------------
@@ -1767,17 +1735,14 @@ int cl_lincomb(const cl_lincomb_args* args, int64_t N, double* dots_out, double*
             }
             break;
         default:
-#define CL_LF(K) lincomb_first_two_kernel<K><<<occ_grid((const void*)lincomb_first_two_kernel<K>, n2 + tail), NT, 0, \
-                                                    st>>>(d, n2, tail, ws, dots_out)
             switch (kin) {
                 case 2:
-                case 4: CL_LF(4); break;
-                case 8: CL_LF(8); break;
-                case 12: CL_LF(12); break;
-                case 17: CL_LF(17); break;
-                default: CL_LF(CL_MAXIN); break;
+                case 4: CL_LC(2, 4); break;
+                case 8: CL_LC(2, 8); break;
+                case 12: CL_LC(2, 12); break;
+                case 17: CL_LC(2, 17); break;
+                default: CL_LC(2, CL_MAXIN); break;
             }
-#undef CL_LF
 #undef CL_LC
             break;
     }
