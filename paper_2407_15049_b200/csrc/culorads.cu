@@ -867,6 +867,9 @@ __global__ void __launch_bounds__(NT) basis_subtract_kernel(const double* __rest
 #ifndef SP_UNROLL0_WIDE
 #define SP_UNROLL0_WIDE 4
 #endif
+#ifndef SP_MINB2
+#define SP_MINB2 3          // the diagonal ADMM epilogues (CG start, step end)
+#endif
 #ifndef SP_MINB1
 #define SP_MINB1 3          // resident CTAs per SM the epilogue variants are compiled for
 #endif
@@ -958,7 +961,7 @@ __device__ __forceinline__ void sp_issue(const SpDev& a, SpTile* T, int64_t (*me
 }
 
 template <int G, int VEC, int EPI, int GHOST>
-__global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : SP_MINB1) spmm_tiled_kernel(SpDev a, EpiDev E, double* ws,
+__global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : (EPI >= 2 ? SP_MINB2 : SP_MINB1)) spmm_tiled_kernel(SpDev a, EpiDev E, double* ws,
                                                                                      double* dots_out) {
     constexpr int NG = NT / G;
     constexpr int SPU = EPI == 0 ? (G == 32 ? SP_UNROLL0_WIDE : SP_UNROLL0) : SP_UNROLL;

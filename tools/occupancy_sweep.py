@@ -27,6 +27,7 @@ VARIANTS = {
     "spu4": ["-DSP_UNROLL=4"],
     "split0": ["-DSP_SPLIT_LD=0"],
     "nosplit": ["-DSP_SPLIT_LD=100000"],
+    "sp2_4": ["-DSP_MINB2=4"],
     "sp5": ["-DSP_MINB0=5"],
     "sp6": ["-DSP_MINB0=6"],
 }
