@@ -499,6 +499,133 @@ def build_sharded_diag_operators(p, rank, world, dev, group=None):
     return ops
 
 
+def is_single_entry_problem(p):
+    """Every constraint is one stored entry a_c at its own position (a_c (e_r e_k^T + e_k e_r^T),
+    or a_c e_r e_r^T): matrix completion's family (problem.py:410)."""
+    m = p.m
+    if not (p.a_con.size == m and np.array_equal(p.a_con, np.arange(m))):
+        return False
+    if m and not np.all(np.asarray(p.a_val) != 0.0):
+        return False
+    from .problem import n_unique
+    return n_unique(np.asarray(p.a_row) * p.n + np.asarray(p.a_col)) == m
+
+
+def build_sharded_single_entry_operators(p, rank, world, dev, group=None):
+    """Rank-local operators of a single-entry-constraint problem (matrix completion), built
+    from the rank's own rows and the constraints that touch them: no global operator build.
+
+    The same patterns, plans, multiplier halo, renumbering and constraint rows as slicing
+    the single-device operators (``build_sharded_operators(local=False)``; tested equal):
+    constraint c at (r, k) has the positions (r, k) and (k, r) (one if r = k), ordered by
+    code; it is owned by the rank of row r when c is even, of row k when odd (the general
+    path's alternation over a constraint's positions); constraints are renumbered
+    owner-major. The compressed-column ids of the constraint rows (``colidx``, used only
+    by the host-API ``cop.apply``) are left local, and ``cop`` carries no global maps."""
+    from .linops import (AdjointOperator, CompressedOperator, ConstraintCSR, DevicePattern, ObjectiveMatrix,
+                         OperatorBundle, _csr_ptr, padded)
+
+    n, m = p.n, p.m
+    tdev = dev.dev
+    F64 = torch.float64
+    b = block_bounds(n, world)
+    lo, hi = b[rank], b[rank + 1]
+    nown = hi - lo
+    bt = torch.tensor(b, dtype=I64, device=tdev)
+    T = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to(device=tdev, dtype=dt)  # noqa: E731
+    r, k, v = T(p.a_row, I64), T(p.a_col, I64), T(p.a_val, F64)
+    c = torch.arange(m, device=tdev, dtype=I64)
+    two = r != k
+    # ownership and owner-major renumbering (build_sharded_operators' general rule)
+    prow = torch.where(two & (c % 2 == 1), k, r)
+    owner = torch.searchsorted(bt, prow, right=True) - 1
+    counts = torch.bincount(owner, minlength=world)
+    bm = [0] + torch.cumsum(counts, 0).cpu().tolist()
+    order = torch.argsort(owner * m + c)
+    new_id = torch.empty(m, dtype=I64, device=tdev)
+    new_id[order] = c
+    lo_m, hi_m = bm[rank], bm[rank + 1]
+    owned = order[lo_m:hi_m]
+    inb = lambda x: (x >= lo) & (x < hi)  # noqa: E731
+    ro, ko = r[owned], k[owned]
+    if not bool((inb(ro) | inb(ko)).all()):       # cannot happen: the owner holds one of the rows
+        raise AssertionError("single-entry ownership")
+    pub = torch.unique(new_id[owned[~(inb(ro) & inb(ko))]] - lo_m)
+    # constraint positions in this rank's rows: (r, k) for r in block, (k, r) for k in block
+    s1 = inb(r)
+    s2 = two & inb(k)
+    a_rows = torch.cat([r[s1], k[s2]])
+    a_cols = torch.cat([k[s1], r[s2]])
+    a_con = torch.cat([c[s1], c[s2]])
+    a_val = torch.cat([v[s1], v[s2]])
+    acode = (a_rows - lo) * n + a_cols
+    oa = torch.argsort(acode)
+    acode, a_con, a_val = acode[oa], a_con[oa], a_val[oa]
+    # the objective's mirrored entries in this rank's rows
+    cr, cc, cvv = np.asarray(p.C.rows), np.asarray(p.C.cols), np.asarray(p.C.vals)
+    t1 = (cr >= lo) & (cr < hi)
+    t2 = (cr != cc) & (cc >= lo) & (cc < hi)
+    c_rows = T(np.concatenate([cr[t1], cc[t2]]), I64)
+    c_cols = T(np.concatenate([cc[t1], cr[t2]]), I64)
+    c_vals = T(np.concatenate([cvv[t1], cvv[t2]]), F64)
+    ccode = (c_rows - lo) * n + c_cols
+    oc = torch.argsort(ccode)
+    ccode, c_vals = ccode[oc], c_vals[oc]
+    # Omega rows: union of both supports; one adjoint entry per constraint position
+    sup = torch.unique(torch.cat([acode, ccode]), sorted=True)
+    S = int(sup.numel())
+    cv = padded(torch.zeros(S, dtype=F64, device=tdev))
+    cv[torch.searchsorted(sup, ccode)] = c_vals
+    slot_a = torch.searchsorted(sup, acode)
+    o_ptr = _csr_ptr(sup // n, nown)
+    ref = new_id[a_con]
+    mplan = HaloPlan(lo_m, hi_m, None, ref, bm, rank, world, group, publish=pub)
+    oplan = make_halo_plan(lo, hi, o_ptr, sup % n, b, rank, world, group)
+    at_con = padded(mplan.remap(ref).to(I32))
+    omega = DevicePattern(nown, o_ptr, padded(oplan.local_indices), cv, _csr_ptr(slot_a, S), at_con,
+                          padded(a_val.clone()))
+    a_ptr = _csr_ptr(acode // n, nown)
+    aplan = make_halo_plan(lo, hi, a_ptr, acode % n, b, rank, world, group)
+    apat = DevicePattern(nown, a_ptr, padded(aplan.local_indices), None,
+                         _csr_ptr(torch.arange(acode.numel(), device=tdev, dtype=I64), acode.numel()),
+                         padded(mplan.remap(ref).to(I32)), padded(a_val.clone()))
+    c_ptr = _csr_ptr(ccode // n, nown)
+    cplan = make_halo_plan(lo, hi, c_ptr, ccode % n, b, rank, world, group)
+    cpat = DevicePattern(nown, c_ptr, padded(cplan.local_indices), padded(c_vals.clone()), None, None, None)
+    for pat, plan in ((omega, oplan), (apat, aplan), (cpat, cplan)):
+        pat.halo = plan if (world > 1 and sum(plan.counts) > 0) else None
+    for pat in (omega, apat):
+        pat.mhalo = mplan if (world > 1 and sum(mplan.counts) > 0) else None
+    # owned constraint rows: positions in code order, remapped through the Omega halo
+    two_o = two[owned]
+    lens = torch.where(two_o, 2, 1).to(I64)
+    ptr = torch.zeros(hi_m - lo_m + 1, dtype=I64, device=tdev)
+    ptr[1:] = torch.cumsum(lens, 0)
+    first_r = torch.minimum(ro, ko)            # code order: the smaller row first
+    first_c = torch.maximum(ro, ko)
+    pi = torch.stack([first_r, first_c], 1)
+    pj = torch.stack([first_c, first_r], 1)
+    keep = torch.stack([torch.ones_like(two_o), two_o], 1).reshape(-1)
+    pi, pj = pi.reshape(-1)[keep], pj.reshape(-1)[keep]
+    vv = torch.stack([v[owned], v[owned]], 1).reshape(-1)[keep]
+    con = ConstraintCSR(m=hi_m - lo_m, indptr=ptr, colidx=padded(torch.zeros(pi.numel(), dtype=I32, device=tdev)),
+                        pi=oplan.remap(pi).to(I32).contiguous(), pj=oplan.remap(pj).to(I32).contiguous(),
+                        val=padded(vv), diag_aval=None)
+    con.halo = oplan if world > 1 else None
+    sp_ = ShardProblem(p, lo, hi)
+    sp_.m = hi_m - lo_m
+    K = int(m + int(two.sum()))
+    cop = CompressedOperator(hi_m - lo_m, nown, K, None, None, None, con, dev)
+    adj = AdjointOperator(hi_m - lo_m, nown, None, None, omega, apat, omega.cv, dev)
+    omega_total = int(_all_gather_1d(torch.tensor([S], dtype=I64, device=tdev), world, group).sum())
+    ops = OperatorBundle(problem=sp_, cop=cop, adj=adj, c_mat=ObjectiveMatrix(adj, cpat), dev=dev,
+                         b=T(np.asarray(p.b), F64)[owned].clone(), diag_aval=None,
+                         omega_size_ref=K if p.dense_c else omega_total)
+    ops.row_range = (lo, hi)
+    ops.con_range = (lo_m, hi_m)
+    return ops
+
+
 def build_sharded_operators(p, rank, world, dev, group=None, local=True):
     """Rank-local OperatorBundle of a row-sharded solve.
 
@@ -520,6 +647,8 @@ def build_sharded_operators(p, rank, world, dev, group=None, local=True):
 
     if local and is_diag_problem(p):
         return build_sharded_diag_operators(p, rank, world, dev, group)
+    if local and is_single_entry_problem(p):
+        return build_sharded_single_entry_operators(p, rank, world, dev, group)
     full = build_operators(p, dev=dev)
     tdev = full.b.device
     b = block_bounds(p.n, world)

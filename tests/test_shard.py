@@ -260,3 +260,36 @@ def _check_peer_halo_spmm(rank, world, d, n, seed, deg, ld):
 @pytest.mark.parametrize("world,n,deg,ld", [(2, 600, 6, 4), (3, 1000, 10, 26), (4, 257, 4, 6)])
 def test_peer_halo_reproduces_global_spmm(world, n, deg, ld):
     _run(_check_peer_halo_spmm, world, n, 11 + n, deg, ld)
+
+
+def _check_local_single_entry_build(rank, world, d, n2, n1, m):
+    """The per-rank matrix-completion build (no global operator build) equals slicing the
+    global one: patterns, halo plans, multiplier halo, renumbered constraint rows."""
+    from paper_2407_15049_b200 import graphs, problem, shard
+    p = problem.build_matrix_completion(graphs.random_completion(n2, n1, m, seed=7))
+    assert shard.is_single_entry_problem(p) and not shard.is_diag_problem(p)
+    dev = _CpuDev()
+    a = shard.build_sharded_operators(p, rank, world, dev, None, local=False)
+    b = shard.build_sharded_operators(p, rank, world, dev, None, local=True)
+    for pa, pb in ((a.adj.omega, b.adj.omega), (a.adj.apat, b.adj.apat), (a.c_mat.cpat, b.c_mat.cpat)):
+        for f in ("indptr", "indices", "cv", "at_ptr", "at_con", "at_val"):
+            assert _same(getattr(pa, f), getattr(pb, f)), f
+        assert pa.nrows == pb.nrows
+        for h in ("halo", "mhalo"):
+            ha, hb = getattr(pa, h), getattr(pb, h)
+            assert (ha is None) == (hb is None), h
+            if ha is not None:
+                assert type(ha) is type(hb) and ha.counts == hb.counts and torch.equal(ha.publish, hb.publish)
+    ca, cb = a.cop.con, b.cop.con
+    for f in ("indptr", "pi", "pj", "val"):
+        assert _same(getattr(ca, f), getattr(cb, f)), f
+    assert (ca.halo is None) == (cb.halo is None)
+    assert torch.equal(a.b, b.b) and a.diag_aval is None and b.diag_aval is None
+    assert a.omega_size_ref == b.omega_size_ref and a.cop.ncols == b.cop.ncols
+    assert a.row_range == b.row_range and a.con_range == b.con_range
+    assert a.problem.m == b.problem.m and a.problem.n == b.problem.n
+
+
+@pytest.mark.parametrize("world,n2,n1,m", [(2, 40, 30, 300), (3, 61, 47, 900)])
+def test_local_single_entry_build_matches_global_slice(world, n2, n1, m):
+    _run(_check_local_single_entry_build, world, n2, n1, m)
