@@ -2,6 +2,8 @@
 
 * ``random_sparse`` -- uniform random simple graph with about n*deg/2 unit
   edges (BASELINE configs: "synthetic random sparse graph, avg degree ~6").
+* ``path_like`` -- a long random path plus sparse chords (degree ~2.2), the shape of
+  the paper's largest instance (kmer_A2a, 1.7e8 nodes).
 * ``delaunay_like`` -- triangulated periodic lattice with randomly permuted
   vertex labels: every vertex has degree 6 like a planar Delaunay mesh
   (the paper's 10^7-scale instances are delaunay_n23/n24), no locality.
@@ -48,7 +50,19 @@ def delaunay_like(n, seed=0):
     return _finish(n, perm[u], perm[v], rng)
 
 
-GENERATORS = {"random_sparse": random_sparse, "delaunay_like": delaunay_like}
+def path_like(n, extra=0.1, seed=0):
+    """A k-mer-graph-like instance (the paper's 1.7e8-node kmer_A2a family is mostly long
+    chains): one path through all n vertices in a random order, plus ``extra * n`` random
+    chords; average degree ~ 2 + 2 extra, no locality in the labels."""
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(n).astype(np.int64)
+    me = int(round(extra * n))
+    u = np.concatenate([perm[:-1], rng.integers(0, n, size=me, dtype=np.int64)])
+    v = np.concatenate([perm[1:], rng.integers(0, n, size=me, dtype=np.int64)])
+    return _finish(n, u, v, rng)
+
+
+GENERATORS = {"random_sparse": random_sparse, "delaunay_like": delaunay_like, "path_like": path_like}
 
 
 def random_completion(n2, n1, m, rank=2, seed=0):

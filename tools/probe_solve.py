@@ -16,6 +16,12 @@ import torch  # noqa: E402
 from paper_2407_15049_b200 import driver, graphs, linops, problem  # noqa: E402
 
 args = [a for a in sys.argv[1:]]
+overrides = {}
+while "--cfg" in args:            # --cfg key=value: a SolverConfig option (the reference's names)
+    k = args.index("--cfg")
+    key, val = args[k + 1].split("=", 1)
+    overrides[key] = None if val == "None" else (int(val) if val.lstrip("-").isdigit() else float(val))
+    del args[k:k + 2]
 out = None
 if "--out" in args:
     k = args.index("--out")
@@ -27,7 +33,12 @@ tl = float(args[2]) if len(args) > 2 else 600.0
 kind = args[3] if len(args) > 3 else "random"
 reorder = len(args) > 4 and args[4] == "reorder"
 t = time.perf_counter()
-g = graphs.delaunay_like(n, seed=0) if kind == "delaunay" else graphs.random_sparse(n, deg=deg, seed=0)
+if kind == "delaunay":
+    g = graphs.delaunay_like(n, seed=0)
+elif kind == "path":
+    g = graphs.path_like(n, extra=max(deg - 2.0, 0.0) / 2.0, seed=0)
+else:
+    g = graphs.random_sparse(n, deg=deg, seed=0)
 t_g = time.perf_counter() - t
 t = time.perf_counter()
 p = problem.build_maxcut(g)
@@ -39,7 +50,8 @@ t_o = time.perf_counter() - t
 print(f"{kind} reorder={reorder} n={n} edges={g.edges_u.size} gen {t_g:.2f}s build_maxcut {t_p:.2f}s "
       f"build_operators {t_o:.2f}s", flush=True)
 t = time.perf_counter()
-rep = driver.solve(p, driver.SolverConfig(time_limit=tl, reorder=reorder), ops=ops)
+rep = driver.solve(p, driver.SolverConfig(time_limit=tl, reorder=reorder, **overrides), ops=ops)
+print("options", overrides, flush=True)
 torch.cuda.synchronize()
 dt = time.perf_counter() - t
 print(f"solve {dt:.2f}s status {rep.status} obj {rep.objective:.10g} err1 {rep.err1:.2e} err3 {rep.err3:.2e} "
