@@ -824,12 +824,17 @@ __global__ void __launch_bounds__(NT) basis_project_kernel(const double* __restr
     }
 }
 
+// h[t] = sum over chunks of the partials: a warp per t (lanes stride over the chunks, a
+// shuffle tree), so the chunk loads are in flight together -- one thread per t read them
+// one after another and cost 26 us per Gram-Schmidt pass at n = 2e5
 __global__ void basis_project_finish(const double* ws, int nchunks, int kc, double* h) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < kc; t += gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int c = 0; c < nchunks; ++c) s += ws[(int64_t)c * kc + t];
-        h[t] = s;
-    }
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (t >= kc) return;
+    double s = 0.0;
+    for (int c = lane; c < nchunks; c += 32) s += ws[(int64_t)c * kc + t];
+    s = warp_sum(s);
+    if (lane == 0) h[t] = s;
 }
 
 __global__ void __launch_bounds__(NT) basis_subtract_kernel(const double* __restrict__ Q, int64_t ldq, int kc,
@@ -2321,7 +2326,7 @@ int cl_basis_project(const double* Q, int64_t ldq, int32_t k_cnt, int64_t n, con
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     dim3 grid(BP_CHUNKS, (k_cnt + BP_TILE - 1) / BP_TILE);
     basis_project_kernel<<<grid, NT, 0, st>>>(Q, ldq, k_cnt, n, v, ws);
-    basis_project_finish<<<(k_cnt + 127) / 128, 128, 0, st>>>(ws, BP_CHUNKS, k_cnt, h);
+    basis_project_finish<<<(k_cnt + 3) / 4, 128, 0, st>>>(ws, BP_CHUNKS, k_cnt, h);
     return (int)cudaGetLastError();
 }
 
