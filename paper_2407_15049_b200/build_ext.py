@@ -14,7 +14,8 @@ ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "culorads.cu"), os.path.join(HERE, "csrc", "admm_native.cu"),
        os.path.join(HERE, "csrc", "alm_native.cu"), os.path.join(HERE, "csrc", "spectral_native.cu"),
        os.path.join(HERE, "csrc", "admm_fused.cu"), os.path.join(HERE, "csrc", "alm_fused.cu")]
-HDR = [os.path.join(ROOT, "include", "culorads.h")]
+HDR = [os.path.join(ROOT, "include", "culorads.h")] + [
+    os.path.join(HERE, "csrc", f) for f in sorted(os.listdir(os.path.join(HERE, "csrc"))) if f.endswith(".cuh")]
 OUT = os.path.join(HERE, "libculorads.so")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
@@ -36,12 +37,28 @@ def stale():
 
 
 def build(force=False, verbose=False):
+    """Compile every source to an object in parallel (one nvcc per file), then link."""
     if not force and not stale():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp", *SRC]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    with tempfile.TemporaryDirectory() as tmp:
+        objs = [os.path.join(tmp, os.path.basename(src) + ".o") for src in SRC]
+        cmds = [[nvcc(), *flags, "-I", os.path.join(ROOT, "include"), "-c", "-o", o, src]
+                for src, o in zip(SRC, objs)]
+        if verbose:
+            for c in cmds:
+                print(" ".join(c), flush=True)
+        with ThreadPoolExecutor(len(cmds)) as pool:
+            for r in pool.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds):
+                if r.returncode != 0:
+                    raise RuntimeError(f"nvcc failed:\n{r.stderr[-4000:]}")
+        link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+                "-o", OUT + ".tmp", *objs]
+        if verbose:
+            print(" ".join(link), flush=True)
+        subprocess.run(link, check=True)
     os.replace(OUT + ".tmp", OUT)
     return OUT
 
