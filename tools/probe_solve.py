@@ -33,7 +33,10 @@ tl = float(args[2]) if len(args) > 2 else 600.0
 kind = args[3] if len(args) > 3 else "random"
 reorder = len(args) > 4 and args[4] == "reorder"
 t = time.perf_counter()
-if kind == "delaunay":
+if kind == "completion":
+    # matrix completion with n rows+cols split in half and deg*n/2 observations (configs[3] family)
+    g = graphs.random_completion(n // 2, n - n // 2, int(deg * n / 2), seed=0)
+elif kind == "delaunay":
     g = graphs.delaunay_like(n, seed=0)
 elif kind == "path":
     g = graphs.path_like(n, extra=max(deg - 2.0, 0.0) / 2.0, seed=0)
@@ -41,13 +44,13 @@ else:
     g = graphs.random_sparse(n, deg=deg, seed=0)
 t_g = time.perf_counter() - t
 t = time.perf_counter()
-p = problem.build_maxcut(g)
+p = problem.build_matrix_completion(g) if kind == "completion" else problem.build_maxcut(g)
 t_p = time.perf_counter() - t
 t = time.perf_counter()
 ops = None if reorder else linops.build_operators(p)
 torch.cuda.synchronize()
 t_o = time.perf_counter() - t
-print(f"{kind} reorder={reorder} n={n} edges={g.edges_u.size} gen {t_g:.2f}s build_maxcut {t_p:.2f}s "
+print(f"{kind} reorder={reorder} n={n} m={p.m} gen {t_g:.2f}s build_problem {t_p:.2f}s "
       f"build_operators {t_o:.2f}s", flush=True)
 t = time.perf_counter()
 rep = driver.solve(p, driver.SolverConfig(time_limit=tl, reorder=reorder, **overrides), ops=ops)
