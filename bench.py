@@ -330,6 +330,8 @@ def solve_runs(dev, time_limit, instances, seed):
         entry = {
             "config": name, "n": p.n, "m": p.m, "time_limit_s": time_limit,
             "stop": "reopt_level 1: max(err1, err3) < 1e-5 (SolverConfig defaults)",
+            "deadline": "checked once per ALM outer iteration / ADMM step, as the reference does "
+                        "(alm.py:362, admm.py:232): a solve overruns the limit by up to one inner solve",
             "status": rep.status, "seconds": rep.time_total_s + build_s, "solve_s": rep.time_total_s,
             "build_operators_s": build_s, "time_alm_s": rep.time_alm_s, "time_admm_s": rep.time_admm_s,
             "objective": rep.objective, "err1": rep.err1, "err2": rep.err2, "err3": rep.err3,
