@@ -50,3 +50,23 @@ def test_cooperative_launch_refusal_is_recognised():
         assert not _lib.coop_refused(0, "x") and not _lib.coop_refused(_lib.CL_EARG + 1, "x")
         assert not _lib.coop_refused(700, "x")          # an illegal address is a fault, not a refusal
     assert len(w) == 1 and "multi-launch" in str(w[0].message)
+
+
+def test_inconsistent_arguments_return_earg_without_device():
+    """Argument checks run before any device work: inconsistent sizes or missing operands
+    return CL_EARG (the header's error contract), on a host with no GPU as on a B200."""
+    import ctypes as C
+    from paper_2407_15049_b200 import _lib, build_ext
+    build_ext.build()
+    lib = _lib.load(require_device=False)
+    E = _lib.CL_EARG
+    assert lib.cl_lincomb(None, 10, None, None, None) == E                     # no args
+    a = _lib.LincombArgs()
+    a.nin = _lib.CL_MAXIN + 1
+    assert lib.cl_lincomb(C.byref(a), 10, None, None, None) == E               # too many inputs
+    assert lib.cl_pattern_spmm(None, None, 26, 1.0, None, None, None, None, None) == E
+    s = _lib.Pattern()
+    assert lib.cl_pattern_spmm(C.byref(s), None, 26, 1.0, None, None, None, None, None) == E
+    assert lib.cl_gather_rows(None, -1, 26, None, None, None) == E             # negative count
+    assert lib.cl_gather_rows(None, 5, 26, None, None, None) == E              # missing operands
+    assert lib.cl_gather_rows(None, 0, 26, None, None, None) == 0              # empty is fine
