@@ -439,6 +439,7 @@ __global__ void __launch_bounds__(AT) alm_fused_kernel(Az z) {
 #endif
     for (int it = 0; it < a.max_iter; ++it) {
         AFZ_T(5);
+        __syncthreads();    // every thread has read the previous c.stop before thread 0 rewrites it
         if (t0) {
             c.gnorm = sqrt(c.gg);
             if (blockIdx.x == 0 && c.ngn < a.rec_cap) z.gnorms[c.ngn] = c.gnorm;
@@ -503,6 +504,7 @@ __global__ void __launch_bounds__(AT) alm_fused_kernel(Az z) {
                 if (ln == 0) c.tc[pos] = c.tc[pos] + (av - bb) * pr.sigma;
                 __syncwarp();
             }
+            __syncwarp();   // all lanes read c.nt above (no shuffle between when the history is empty)
             if (ln == 0) c.nt = nt;
         }
         __syncthreads();
