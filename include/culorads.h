@@ -51,6 +51,19 @@ extern "C" {
 #define CL_EARG 1001          /* inconsistent arguments                      */
 #define CL_ENODEV 1002        /* no usable sm_100 device                     */
 
+/* Peer-memory ghost rows of a row-sharded solve (shard.py NvlinkHaloPlan): instead of
+ * a halo buffer filled by a collective, a pattern's remote column is encoded in its
+ * int32 index as CL_PEER_COL(owner, row) (negative: bit 31 set) and the SpMM loads that
+ * factor row in place from the owner GPU's memory over NVLink. cl_pattern.nown ==
+ * CL_GHOST_PEERS marks the mode; cl_pattern.ghost then points at a HOST table of
+ * CL_MAX_PEERS device addresses (rank k's row block of X as mapped in this process,
+ * cl_ipc_import), which the launch copies into the kernel's parameters. */
+#define CL_MAX_PEERS 8
+#define CL_PEER_ROW_BITS 28
+#define CL_PEER_ROW_MASK ((1u << CL_PEER_ROW_BITS) - 1u)
+#define CL_GHOST_PEERS (-2)
+#define CL_PEER_COL(owner, row) ((int32_t)(0x80000000u | ((uint32_t)(owner) << CL_PEER_ROW_BITS) | (uint32_t)(row)))
+
 /* Operand index meaning "the freshly computed output" in dot specifications. */
 #define CL_OUT 255
 
@@ -96,7 +109,8 @@ typedef struct {
     const double* w2;
     int64_t nnz;            /* slots (indptr[nrows]); the host knows it, the launch needs it */
     double* scratch;        /* nnz+16 doubles for assembled coefficients, or NULL */
-    const double* ghost;    /* row-sharded solve: rows >= nown of X live here (halo), or NULL */
+    const double* ghost;    /* row-sharded solve: rows >= nown of X live here (halo), or NULL;
+                               nown == CL_GHOST_PEERS: host table of peer row blocks (above) */
     int64_t nown;           /* rows of X owned by this rank (column j >= nown reads ghost[j-nown]) */
     const double* w1g;      /* row-sharded solve: multipliers of constraints owned by other ranks */
     const double* w2g;      /* (adjoint entry con >= mown reads w?g[con-mown]), or NULL */
@@ -310,6 +324,11 @@ typedef struct {
     const double* (*exchange)(void* ctx, const double* X, int32_t ld);
     int32_t (*reduce)(void* ctx, double* slab, double* host, int32_t count, void* stream);
     int64_t nown;
+    /* Peer-memory mode (nown == CL_GHOST_PEERS): exchange returns the host table of the
+     * peers' row blocks of X after a stream-ordered fence (every rank's X complete), and
+     * release, called right after the product is queued, fences again so that no rank
+     * overwrites its rows while a peer may still read them. NULL in the halo modes. */
+    int32_t (*release)(void* ctx, void* stream);
 } cl_dist_hooks;
 
 /* One ADMM step (admm.py:136 admm_step: U half-solve, V half-solve, dual
@@ -551,6 +570,17 @@ int cl_lanczos_update(int32_t mode, int64_t n, const double* alpha, const double
 /* L2 fetch granularity hint of the current device (cudaLimitMaxL2FetchGranularity, 0..128 bytes). */
 int cl_set_l2_fetch_granularity(int32_t bytes);
 int cl_get_l2_fetch_granularity(void);
+
+/* CUDA IPC of a factor's device allocation, for the peer-memory ghost mode (replaces
+ * the all-gather / all-to-all halo of shard.py HaloPlan / PeerHaloPlan: reference
+ * north_star "remote factor rows come in by NCCL all-gather or halo exchange over
+ * NVLink"). cl_ipc_export: the 64-byte IPC handle of the allocation holding `ptr` and
+ * ptr's byte offset in it. cl_ipc_import: map a peer's handle (another process) and
+ * return the allocation's base here; cl_ipc_close unmaps it. */
+#define CL_IPC_HANDLE_BYTES 64
+int cl_ipc_export(const void* ptr, void* handle, int64_t* offset);
+int cl_ipc_import(const void* handle, void** base);
+int cl_ipc_close(void* base);
 
 /* Library identity, for load checks. */
 const char* cl_version(void);

@@ -59,7 +59,12 @@ EXPORTS = ("cl_lincomb", "cl_pattern_spmm", "cl_constraint_eval", "cl_constraint
            "cl_diag_admm_cg_init", "cl_diag_admm_step_end", "cl_diag_admm_step_end_rows", "cl_single_entry_apply", "cl_single_entry_apply_pair", "cl_pair_pack", "cl_cg_direction_pair", "cl_lanczos_loop", "cl_lanczos_loop_fused",
            "cl_pattern_assemble", "cl_lanczos_update",
            "cl_diag_alm_update", "cl_basis_project", "cl_basis_subtract",
-           "cl_set_l2_fetch_granularity", "cl_get_l2_fetch_granularity", "cl_version", "cl_device_ok")
+           "cl_set_l2_fetch_granularity", "cl_get_l2_fetch_granularity", "cl_ipc_export", "cl_ipc_import",
+           "cl_ipc_close", "cl_version", "cl_device_ok")
+
+CL_IPC_HANDLE_BYTES = 64
+CL_MAX_PEERS = 8
+CL_GHOST_PEERS = -2
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64
@@ -100,8 +105,12 @@ REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, c
                              ctypes.c_void_p)
 
 
+RELEASE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p)
+
+
 class DistHooks(ctypes.Structure):
-    _fields_ = [("ctx", P), ("exchange", EXCHANGE_FN), ("reduce", REDUCE_FN), ("nown", I64)]
+    _fields_ = [("ctx", P), ("exchange", EXCHANGE_FN), ("reduce", REDUCE_FN), ("nown", I64),
+                ("release", RELEASE_FN)]
 
 
 class AdmmDiagArgs(ctypes.Structure):
@@ -200,6 +209,9 @@ def _declare(lib):
     lib.cl_basis_subtract.argtypes = [P, I64, I32, I64, P, P, P]
     lib.cl_set_l2_fetch_granularity.argtypes = [I32]
     lib.cl_get_l2_fetch_granularity.argtypes = []
+    lib.cl_ipc_export.argtypes = [P, P, ctypes.POINTER(I64)]
+    lib.cl_ipc_import.argtypes = [P, ctypes.POINTER(P)]
+    lib.cl_ipc_close.argtypes = [P]
     lib.cl_version.restype = ctypes.c_char_p
     lib.cl_device_ok.restype = ctypes.c_int
     for name in EXPORTS:

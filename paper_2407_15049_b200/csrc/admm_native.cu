@@ -139,6 +139,12 @@ void cg_init(Ctx& c, const double* x0, const double* Wf, double* r, int slot, do
     }
     CL_TRY(c, cl_diag_admm_cg_init(&P, Wf, x0, a->ld, a->scale, a->rho, a->nlam, a->aval, r, cw, a->slab + slot,
                                    a->ws, (void*)c.st));
+    // peer-memory ghosts: fence after the product that read the peers' rows of Wf
+    if (a->dist != nullptr && a->dist->release != nullptr && !c.rc &&
+        a->dist->release(a->dist->ctx, (void*)c.st) != 0) {
+        c.rc = CL_EARG;
+        c.line = __LINE__;
+    }
 }
 
 // step end from the C U stored by the last V start (whose Wf is the U passed here)

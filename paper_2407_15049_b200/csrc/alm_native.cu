@@ -354,11 +354,22 @@ bool c_pattern(Ctx& c, const double* X, cl_pattern* P) {
     return !c.rc;
 }
 
+// peer-memory ghosts: fence after the product that read the peers' rows (cl_dist_hooks)
+void c_release(Ctx& c) {
+    const cl_dist_hooks* d = c.a->dist;
+    if (d == nullptr || d->release == nullptr || c.rc) return;
+    if (d->release(d->ctx, (void*)c.st) != 0) {
+        c.rc = CL_EARG;
+        c.line = __LINE__;
+    }
+}
+
 void c_times(Ctx& c, const double* X, double* out) {
     const cl_alm_inner_args* a = c.a;
     cl_pattern P;
     if (!c_pattern(c, X, &P)) return;
     TRY(c, cl_pattern_spmm(&P, X, a->ld, 1.0, nullptr, out, nullptr, nullptr, (void*)c.st));
+    c_release(c);
 }
 
 int alm_inner(const cl_alm_inner_args* a, cl_alm_inner_stats* out, bool generic);
@@ -513,6 +524,7 @@ int alm_inner(const cl_alm_inner_args* a, cl_alm_inner_stats* out, bool generic)
             E.da[2] = 18;
             E.db[2] = 17;
             TRY(c, cl_pattern_spmm(&P, D, a->ld, 1.0, &E, a->CD, a->slab + S_LS, a->ws, (void*)c.st));
+            c_release(c);
         }
         if (!c.generic) {
             TRY(c, cl_diag_constraint_eval(a->n, a->aval, a->ld, R, D, D, R, a->q1, D, D, a->q2, (void*)c.st));

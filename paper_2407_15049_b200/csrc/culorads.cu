@@ -928,6 +928,9 @@ struct SpDev {
     const double* X;
     const double* Xg;     // ghost rows (row-sharded solve): column j >= nown reads Xg[j - nown]
     int32_t nown;         // INT32_MAX when there is no ghost block
+    // peer-memory ghosts (GHOST 2): a remote column is encoded as CL_PEER_COL(owner, row)
+    // and read in place from the owner's factor, Xp[owner] + row * ld (NVLink loads)
+    const double* Xp[CL_MAX_PEERS];
     int ld;
     double alpha;
     double* out;
@@ -963,6 +966,18 @@ __device__ __forceinline__ void sp_issue(const SpDev& a, SpTile* T, int64_t (*me
     bulk_g2s(T[buf].ptr, a.indptr + pb, pbytes, &bar[buf]);
     if (ibytes) bulk_g2s(T[buf].idx, a.indices + ib, ibytes, &bar[buf]);
     if (vbytes) bulk_g2s(T[buf].val, a.vals + vb, vbytes, &bar[buf]);
+}
+
+// Source row of pattern column j: own rows from X; GHOST 1: rows >= nown from the halo
+// buffer; GHOST 2: negative (encoded) columns straight from the owner rank's memory.
+template <int GHOST>
+__device__ __forceinline__ const double* sp_src(const SpDev& a, const double* X, int j, int ld) {
+    if (GHOST == 1 && j >= a.nown) return a.Xg + (int64_t)(j - a.nown) * ld;
+    if (GHOST == 2 && j < 0) {
+        const uint32_t u = (uint32_t)j;
+        return a.Xp[(u >> CL_PEER_ROW_BITS) & (CL_MAX_PEERS - 1)] + (int64_t)(u & CL_PEER_ROW_MASK) * ld;
+    }
+    return X + (int64_t)j * ld;
 }
 
 template <int G, int VEC, int EPI, int GHOST>
@@ -1059,8 +1074,7 @@ __global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : (EPI >
 #pragma unroll
                         for (int u = 0; u < SPU; ++u) {
                             if (active && s + u < s1) {
-                                const double* src = (!GHOST || jv[u] < a.nown) ? X + (int64_t)jv[u] * ld
-                                                                               : a.Xg + (int64_t)(jv[u] - a.nown) * ld;
+                                const double* src = sp_src<GHOST>(a, X, jv[u], ld);
                                 if (VEC == 2) xv[u] = ld2(src + col);
                                 else xv[u] = make_double2(__ldg(src + col), 0.0);
                             } else {
@@ -1092,14 +1106,12 @@ __global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : (EPI >
                             const double c = __shfl_sync(gmask, cc, (lane - gl) + u);
                             if (active) {
                                 if (VEC == 2) {
-                                    const double* src = (!GHOST || j < a.nown) ? X + (int64_t)j * ld
-                                                                               : a.Xg + (int64_t)(j - a.nown) * ld;
+                                    const double* src = sp_src<GHOST>(a, X, j, ld);
                                     const double2 x = ld2(src + col);
                                     acc.x = fma(c, x.x, acc.x);
                                     acc.y = fma(c, x.y, acc.y);
                                 } else {
-                                    const double* src = (!GHOST || j < a.nown) ? X + (int64_t)j * ld
-                                                                               : a.Xg + (int64_t)(j - a.nown) * ld;
+                                    const double* src = sp_src<GHOST>(a, X, j, ld);
                                     acc.x = fma(c, __ldg(src + col), acc.x);
                                 }
                             }
@@ -1231,14 +1243,38 @@ void sp_launch(const SpDev& a0, const EpiDev& E, double* ws, double* dots, cudaS
     spmm_tiled_kernel<G, VEC, EPI, GHOST><<<grid, NT, 0, st>>>(a, E, ws, dots);
 }
 
+// 0: no ghost rows; 1: halo buffer (Xg); 2: peer memory (Xp, nown = CL_GHOST_PEERS)
+static inline int sp_ghost_mode(const SpDev& a) {
+    if (a.nown == CL_GHOST_PEERS) return 2;
+    return a.Xg != nullptr ? 1 : 0;
+}
+
+// Ghost fields of a launch from the pattern: a halo buffer, or (nown == CL_GHOST_PEERS) a
+// host table of CL_MAX_PEERS device addresses -- each rank's row block of X as mapped here,
+// read now, at launch, into the kernel's parameters (so the caller may reuse the table).
+static inline void sp_set_ghost(SpDev& a, const cl_pattern* S) {
+    for (int k = 0; k < CL_MAX_PEERS; ++k) a.Xp[k] = nullptr;
+    if (S->ghost != nullptr && S->nown == CL_GHOST_PEERS) {
+        const double* const* tab = reinterpret_cast<const double* const*>(S->ghost);
+        for (int k = 0; k < CL_MAX_PEERS; ++k) a.Xp[k] = tab[k];
+        a.Xg = nullptr;
+        a.nown = CL_GHOST_PEERS;
+    } else {
+        a.Xg = S->ghost;
+        a.nown = S->ghost != nullptr ? (int32_t)S->nown : INT32_MAX;
+    }
+}
+
 template <int G, int VEC>
 void sp_dispatch_mode(int mode, const SpDev& a, const EpiDev& E, double* ws, double* dots, cudaStream_t st) {
-    const bool ghost = a.Xg != nullptr;
+    const int gm = sp_ghost_mode(a);
     if (mode == 2) {
-        if (ghost) sp_launch<G, VEC, 2, 1>(a, E, ws, dots, st);
+        if (gm == 2) sp_launch<G, VEC, 2, 2>(a, E, ws, dots, st);
+        else if (gm == 1) sp_launch<G, VEC, 2, 1>(a, E, ws, dots, st);
         else sp_launch<G, VEC, 2, 0>(a, E, ws, dots, st);
     } else {
-        if (ghost) sp_launch<G, VEC, 3, 1>(a, E, ws, dots, st);
+        if (gm == 2) sp_launch<G, VEC, 3, 2>(a, E, ws, dots, st);
+        else if (gm == 1) sp_launch<G, VEC, 3, 1>(a, E, ws, dots, st);
         else sp_launch<G, VEC, 3, 0>(a, E, ws, dots, st);
     }
 }
@@ -1246,12 +1282,14 @@ void sp_dispatch_mode(int mode, const SpDev& a, const EpiDev& E, double* ws, dou
 template <int G, int VEC>
 void sp_dispatch_epi(const SpDev& a, const EpiDev& E, double* ws, double* dots, cudaStream_t st) {
     const bool plain = E.ny == 0 && E.nz == 0 && E.ndot == 0 && E.drow == nullptr && a.out != nullptr;
-    const bool ghost = a.Xg != nullptr;
+    const int gm = sp_ghost_mode(a);
     if (plain) {
-        if (ghost) sp_launch<G, VEC, 0, 1>(a, E, ws, dots, st);
+        if (gm == 2) sp_launch<G, VEC, 0, 2>(a, E, ws, dots, st);
+        else if (gm == 1) sp_launch<G, VEC, 0, 1>(a, E, ws, dots, st);
         else sp_launch<G, VEC, 0, 0>(a, E, ws, dots, st);
     } else {
-        if (ghost) sp_launch<G, VEC, 1, 1>(a, E, ws, dots, st);
+        if (gm == 2) sp_launch<G, VEC, 1, 2>(a, E, ws, dots, st);
+        else if (gm == 1) sp_launch<G, VEC, 1, 1>(a, E, ws, dots, st);
         else sp_launch<G, VEC, 1, 0>(a, E, ws, dots, st);
     }
 }
@@ -1672,6 +1710,52 @@ int cl_get_l2_fetch_granularity(void) {
     return (int)v;
 }
 
+// Allocation base of a device address: the driver's cuMemGetAddressRange, reached
+// through the runtime's entry-point table (no link-time libcuda dependency).
+typedef int (*cu_range_fn)(unsigned long long* base, size_t* size, unsigned long long dptr);
+
+static cu_range_fn cu_mem_range() {
+    static cu_range_fn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<cu_range_fn>(f);
+    }
+    return fn;
+}
+
+int cl_ipc_export(const void* ptr, void* handle, int64_t* offset) {
+    if (ptr == nullptr || handle == nullptr || offset == nullptr) return CL_EARG;
+    cu_range_fn range = cu_mem_range();
+    if (range == nullptr) return CL_EARG;
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (unsigned long long)(uintptr_t)ptr) != 0) return CL_EARG;
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) return (int)e;
+    static_assert(sizeof(h) == CL_IPC_HANDLE_BYTES, "IPC handle size");
+    memcpy(handle, &h, sizeof(h));
+    *offset = (int64_t)((uintptr_t)ptr - (uintptr_t)base);
+    return CL_OK;
+}
+
+int cl_ipc_import(const void* handle, void** base) {
+    if (handle == nullptr || base == nullptr) return CL_EARG;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    return (int)cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess);
+}
+
+int cl_ipc_close(void* base) {
+    if (base == nullptr) return CL_EARG;
+    return (int)cudaIpcCloseMemHandle(base);
+}
+
 int cl_device_ok(void) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
@@ -1815,8 +1899,7 @@ int cl_pattern_spmm(const cl_pattern* S, const double* X, int32_t ld, double alp
         }
         SpDev a;
         a.nrows = P.nrows; a.indptr = P.indptr; a.indices = P.indices; a.X = X; a.ld = ld; a.out = out;
-        a.Xg = S->ghost;
-        a.nown = S->ghost != nullptr ? (int32_t)S->nown : INT32_MAX;
+        sp_set_ghost(a, S);
         if (need_asm) {
             if (S->nnz > 0) {
                 int64_t g = (S->nnz + NT - 1) / NT;
@@ -1916,6 +1999,7 @@ int constraint_eval_impl(int64_t m, const int64_t* indptr, const int32_t* pi, co
                          int32_t ld, const double* X1, const double* Y1, const double* X2, const double* Y2,
                          double* out1, const double* X3, const double* Y3, double* out2, const double* const* ghosts,
                          int64_t nown, int64_t sx, void* stream) {
+    if (ghosts != nullptr && nown == CL_GHOST_PEERS) return CL_EARG;   // peer-memory ghosts: SpMM only
     ConGhost gh;
     for (int k = 0; k < 6; ++k) gh.g[k] = ghosts != nullptr ? ghosts[k] : nullptr;
     gh.nown = ghosts != nullptr ? nown : -1;
@@ -2141,8 +2225,7 @@ static int diag_admm_launch(int mode, const cl_pattern* S, const double* X, int3
     SpDev a;
     a.nrows = S->nrows; a.indptr = S->indptr; a.indices = S->indices; a.vals = S->cv; a.X = X; a.ld = ld;
     a.out = nullptr; a.alpha = alpha * S->c_coeff;
-    a.Xg = S->ghost;
-    a.nown = S->ghost != nullptr ? (int32_t)S->nown : INT32_MAX;
+    sp_set_ghost(a, S);
     const int NG = NT / G;
     const double avg = S->nrows > 0 ? (double)S->nnz / (double)S->nrows : 1.0;
     int rpg = (int)((0.5 * SP_SMAX) / ((avg > 1.0 ? avg : 1.0) * NG));

@@ -144,7 +144,7 @@ class Device:
         if halo is not None:
             ghost = halo.exchange(X, ld, self.gather_rows)
             P.ghost = ghost.data_ptr()
-            P.nown = halo.nown
+            P.nown = getattr(halo, "ghost_nown", halo.nown)
         mhalo = getattr(pat, "mhalo", None)
         if mhalo is not None and (w1 is not None or w2 is not None) and P.at_ptr:
             # multipliers of constraints owned by other ranks (row-sharded solve)
@@ -158,6 +158,7 @@ class Device:
                                       ptr(self.ws) if nd else None, self.sp)
         self.launches += 1
         check(rc, "cl_pattern_spmm")
+        self._release(halo, X)
 
     def constraint_eval(self, con, ld, X1, Y1, out1, X2=None, Y2=None, X3=None, Y3=None, out2=None):
         if con.diag_aval is not None:
@@ -222,8 +223,14 @@ class Device:
         halo = getattr(pat, "halo", None)
         if halo is not None:
             P.ghost = halo.exchange(X, ld, self.gather_rows).data_ptr()
-            P.nown = halo.nown
+            P.nown = getattr(halo, "ghost_nown", halo.nown)
         return P
+
+    @staticmethod
+    def _release(halo, X):
+        """Peer-memory ghosts (shard.NvlinkHaloPlan): fence after the product that read them."""
+        if halo is not None and hasattr(halo, "release"):
+            halo.release(X)
 
     def diag_admm_cg_init(self, cpat, Wf, x0, ld, scale, rho, nlam, aval, r, at, cw=None):
         """Fused rhs + initial CG residual (cl_diag_admm_cg_init); ||rhs||^2, ||r||^2 -> slab[at:at+2];
@@ -234,6 +241,7 @@ class Device:
                                            self.sp)
         self.launches += 1
         check(rc, "cl_diag_admm_cg_init")
+        self._release(getattr(cpat, "halo", None), Wf)
 
     def diag_admm_step_end(self, cpat, U, V, ld, aval, b, lam, rho, ax, lam_new, at):
         """Fused objective / A(UV^T) / residual / dual ascent (cl_diag_admm_step_end) -> slab[at:at+3]."""
@@ -242,6 +250,7 @@ class Device:
                                             float(rho), ptr(ax), ptr(lam_new), self.slot(at), ptr(self.ws), self.sp)
         self.launches += 1
         check(rc, "cl_diag_admm_step_end")
+        self._release(getattr(cpat, "halo", None), V)
 
     def diag_admm_step_end_rows(self, CU, U, V, ld, aval, b, lam, rho, ax, lam_new, at):
         """Step end from a stored C U (cl_diag_admm_step_end_rows): <CU, V>, ||ax - b||^2,

@@ -32,6 +32,9 @@ gather kernel.
 
 from __future__ import annotations
 
+import ctypes
+import os
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -270,10 +273,197 @@ class PeerHaloPlan:
         return self.halo_rows * ld * 8
 
 
-def make_halo_plan(lo, hi, indptr, indices, bounds, rank, world, group=None, mode="auto"):
+# CL_MAX_PEERS / CL_PEER_ROW_BITS / CL_GHOST_PEERS of include/culorads.h
+MAX_PEERS = 8
+PEER_ROW_BITS = 28
+GHOST_PEERS = -2
+
+# halo mode of the diagonal-constraint (MaxCut-family) builders: "auto", "nvlink",
+# "p2p" or "allgather" (make_halo_plan)
+HALO_MODE = os.environ.get("CULORADS_HALO", "auto")
+
+
+def peer_cols(owner, row):
+    """CL_PEER_COL(owner, row) as int64 values of the int32 encoding (negative)."""
+    return ((owner.to(I64) << PEER_ROW_BITS) | row.to(I64)) - (1 << 31)
+
+
+def encode_peer_columns(ids, lo, hi, bounds):
+    """Global column ids of rows [lo, hi) -> the peer-memory encoding: owned ids become
+    local rows, remote ids CL_PEER_COL(owner, offset in the owner's block)."""
+    ids = ids.to(I64)
+    own = (ids >= lo) & (ids < hi)
+    out = ids - lo
+    remote = ids[~own]
+    if remote.numel():
+        bt = torch.tensor(bounds, dtype=I64, device=ids.device)
+        owner = torch.searchsorted(bt, remote, right=True) - 1
+        out[~own] = peer_cols(owner, remote - bt[owner])
+    return out
+
+
+def decode_peer_columns(enc, lo, bounds):
+    """Inverse of encode_peer_columns (tests): encoded local indices -> global ids."""
+    enc = enc.to(I64)
+    out = enc + lo
+    rem = enc < 0
+    if bool(rem.any()):
+        u = enc[rem] + (1 << 31)
+        owner = (u >> PEER_ROW_BITS) & (MAX_PEERS - 1)
+        row = u & ((1 << PEER_ROW_BITS) - 1)
+        bt = torch.tensor(bounds, dtype=I64, device=enc.device)
+        out[rem] = bt[owner] + row
+    return out
+
+
+class NvlinkHaloPlan:
+    """Peer-memory ghost rows: no halo buffer and no collective moving factor rows.
+
+    A remote column of this rank's pattern rows is encoded in its int32 index as
+    ``CL_PEER_COL(owner, row)`` (row = the id's offset in the owner's block), and the SpMM
+    loads that factor row in place from the owner GPU's memory (NVLink loads, issued by the
+    same warps and in the same slot order as the local gathers, so remote and local traffic
+    overlap tile by tile and the product is bit-identical to the halo paths). Each rank maps
+    the peers' device allocations once (CUDA IPC, ``cl_ipc_export``/``cl_ipc_import``); per
+    product only the (handle, offset) of every rank's operand is exchanged on the host (a
+    gloo side group, no device sync), between two stream-ordered fences: ``exchange`` waits
+    until every rank's operand is complete, ``release`` until every rank's product has
+    read it (an 8-byte NCCL all-reduce on the compute stream; a host barrier on gloo).
+
+    Replaces the all-gather / all-to-all of HaloPlan / PeerHaloPlan for patterns read only by
+    the SpMM (C and Omega of a diagonal-constraint problem). ``ghost_nown`` (= CL_GHOST_PEERS)
+    is what goes into cl_pattern.nown; ``exchange`` returns the host table of peer addresses
+    (cl_pattern.ghost)."""
+
+    ghost_nown = GHOST_PEERS
+
+    def __init__(self, lo, hi, indptr, indices, bounds, rank, world, group=None):
+        if world > MAX_PEERS:
+            raise ValueError(f"peer-memory halo supports at most {MAX_PEERS} ranks")
+        if max(bounds[k + 1] - bounds[k] for k in range(world)) >= 2 ** PEER_ROW_BITS:
+            raise ValueError("a row block exceeds the peer column encoding (2^28 rows)")
+        self.lo, self.hi, self.rank, self.world, self.group = lo, hi, rank, world, group
+        self.nown = hi - lo
+        self.bounds = bounds
+        indices = indices.to(I64)
+        self.local_indices = self.remap(indices).to(I32).contiguous()
+        nrem = torch.tensor([int(((indices < lo) | (indices >= hi)).sum())], dtype=I64, device=indices.device)
+        self.counts = _all_gather_1d(nrem, world, group).view(-1).cpu().tolist()   # remote slots per rank
+        self.remote_slots = self.counts[rank]
+        self.halo_rows = 0
+        self.maxb = 0
+        self.publish = torch.zeros(0, dtype=I32, device=indices.device)
+        self._obj_group = None
+        self._fence_t = None
+        self._imported = {}          # handle bytes -> mapped base address of a peer allocation
+        self._tables = [(ctypes.c_uint64 * MAX_PEERS)() for _ in range(4)]
+        self._tslot = 0
+
+    def remap(self, ids):
+        """Global ids -> local indices (int64 values of the int32 encoding)."""
+        return encode_peer_columns(ids, self.lo, self.hi, self.bounds)
+
+    # -- per product ---------------------------------------------------------
+    def _objects(self):
+        if self._obj_group is None:
+            self._obj_group = (dist.new_group(list(range(self.world)), backend="gloo")
+                               if _nccl(self.group) else self.group)
+        return self._obj_group
+
+    def fence(self, like):
+        """Stream-ordered barrier over the ranks: work queued before it on every rank's
+        compute stream is complete when work queued after it starts."""
+        if self.world == 1:
+            return
+        if like.is_cuda and _nccl(self.group):
+            if self._fence_t is None:
+                self._fence_t = torch.zeros(1, dtype=torch.float64, device=like.device)
+            dist.all_reduce(self._fence_t, group=self.group)
+        else:
+            torch.cuda.current_stream(like.device).synchronize()
+            dist.barrier(group=self.group)
+
+    def exchange(self, X, ld, pack=None, slot=0):
+        """Fence, then the host table of every rank's row block of X as mapped here."""
+        from . import _lib
+        lib = _lib.load(require_device=True)
+        self.fence(X)
+        h = (ctypes.c_uint8 * _lib.CL_IPC_HANDLE_BYTES)()
+        off = ctypes.c_int64(0)
+        _lib.check(lib.cl_ipc_export(ctypes.c_void_p(X.data_ptr()), h, ctypes.byref(off)), "cl_ipc_export")
+        allinfo = [None] * self.world
+        dist.all_gather_object(allinfo, (bytes(h), int(off.value)), group=self._objects())
+        tab = self._tables[self._tslot]
+        self._tslot = (self._tslot + 1) % len(self._tables)
+        for k in range(MAX_PEERS):
+            tab[k] = 0
+        for k, (hb, o) in enumerate(allinfo):
+            if k == self.rank:
+                tab[k] = X.data_ptr()
+                continue
+            base = self._imported.get(hb)
+            if base is None:
+                bp = ctypes.c_void_p()
+                buf = (ctypes.c_uint8 * len(hb)).from_buffer_copy(hb)
+                _lib.check(lib.cl_ipc_import(buf, ctypes.byref(bp)), "cl_ipc_import")
+                base = self._imported[hb] = int(bp.value)
+            tab[k] = base + o
+        return _HostTable(tab)
+
+    def release(self, X):
+        """Fence after a product that read the peers' rows (no rank may overwrite its rows
+        while another rank's product can still read them)."""
+        self.fence(X)
+
+    def close(self):
+        from . import _lib
+        lib = _lib.load(require_device=True)
+        for base in self._imported.values():
+            lib.cl_ipc_close(ctypes.c_void_p(base))
+        self._imported.clear()
+
+    def halo_bytes(self, ld):
+        """Bytes this rank reads from peers per product (remote slots x one row each)."""
+        return self.remote_slots * ld * 8
+
+
+class _HostTable:
+    """cl_pattern.ghost of the peer-memory mode: a host array of CL_MAX_PEERS addresses."""
+
+    def __init__(self, tab):
+        self.tab = tab
+
+    def data_ptr(self):
+        return ctypes.addressof(self.tab)
+
+
+def nvlink_available(rank, world, group=None, device=None):
+    """Every rank on its own CUDA device with peer access to every other (NCCL group):
+    the peer-memory halo can be used. The same answer on every rank."""
+    if world == 1 or world > MAX_PEERS or not _nccl(group):
+        return False
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    idx = torch.tensor([dev.index], dtype=I64, device=dev)
+    devs = _all_gather_1d(idx, world, group).view(-1).cpu().tolist()
+    ok = len(set(devs)) == world and all(
+        torch.cuda.can_device_access_peer(dev.index, d) for d in devs if d != dev.index)
+    flag = torch.tensor([1 if ok else 0], dtype=I64, device=dev)
+    return min(_all_gather_1d(flag, world, group).view(-1).cpu().tolist()) == 1
+
+
+def make_halo_plan(lo, hi, indptr, indices, bounds, rank, world, group=None, mode="auto", peer_ok=False):
     """The halo plan of a symmetric pattern's row block: the all-gather plan (HaloPlan) or the
     point-to-point one (PeerHaloPlan), whichever receives fewer rows on the worst rank
-    ("auto"; every rank takes the same decision)."""
+    ("auto"; every rank takes the same decision). With ``peer_ok`` (a pattern only the SpMM
+    reads), "nvlink" -- and "auto" when every rank has its own peer-accessible GPU -- gives
+    the peer-memory plan (NvlinkHaloPlan) instead."""
+    if mode is None:
+        mode = HALO_MODE
+    if world > 1 and peer_ok and (mode == "nvlink" or (
+            mode == "auto" and indices.is_cuda and nvlink_available(rank, world, group, indices.device))):
+        return NvlinkHaloPlan(lo, hi, indptr, indices, bounds, rank, world, group)
+    if mode == "nvlink":
+        mode = "auto"
     if mode == "allgather" or world == 1:
         return HaloPlan(lo, hi, indptr, indices, bounds, rank, world, group)
     peer = PeerHaloPlan(lo, hi, indptr, indices, bounds, rank, world, group)
@@ -357,7 +547,7 @@ def sharded_maxcut_ops(n_global, deg, seed, rank, world, dev, group=None):
     indptr, cols, vals = maxcut_rows(n_global, eu, ev, lo, hi)
     n_edges = int(eu.numel())
     del eu, ev
-    plan = make_halo_plan(lo, hi, indptr, cols, b, rank, world, group)
+    plan = make_halo_plan(lo, hi, indptr, cols, b, rank, world, group, mode=None, peer_ok=True)
     pad_ptr = torch.zeros(nown + 1 + 16, dtype=I64, device=dev.dev)
     pad_ptr[:nown + 1] = indptr
     cpat = DevicePattern(nown, pad_ptr[:nown + 1], padded(plan.local_indices), padded(vals),
@@ -471,7 +661,7 @@ def build_sharded_diag_operators(p, rank, world, dev, group=None):
     cv[slot_c] = vals
     sup_r, sup_c = sup // n, sup % n
     o_ptr = _csr_ptr(sup_r, nown)
-    plan = make_halo_plan(lo, hi, o_ptr, sup_c, b, rank, world, group)
+    plan = make_halo_plan(lo, hi, o_ptr, sup_c, b, rank, world, group, mode=None, peer_ok=True)
     aval = torch.as_tensor(np.ascontiguousarray(p.a_val[lo:hi], dtype=np.float64)).to(tdev)
     omega = DevicePattern(nown, o_ptr, padded(plan.local_indices), cv, _csr_ptr(slot_d, S),
                           padded(ar.to(I32)), padded(aval.clone()))
@@ -846,7 +1036,7 @@ class _RawRows:
 
     def __init__(self, addr, ld, like):
         self.addr, self.ld = addr, ld
-        self.dtype, self.device = like.dtype, like.device
+        self.dtype, self.device, self.is_cuda = like.dtype, like.device, like.is_cuda
 
     def reshape(self, *shape):
         return self
@@ -890,10 +1080,20 @@ def native_hooks(dev, ops):
             traceback.print_exc(file=sys.stderr)
             return 1
 
+    def release(ctx, stream):
+        try:
+            plan.release(dev.slab)
+            return 0
+        except Exception:             # noqa: BLE001
+            traceback.print_exc(file=sys.stderr)
+            return 1
+
     h = _lib.DistHooks()
     h.ctx = None
     h.exchange = _lib.EXCHANGE_FN(exchange)
     h.reduce = _lib.REDUCE_FN(reduce)
-    h.nown = plan.nown if plan is not None else int(ops.problem.n)
-    h._keep = (h.exchange, h.reduce)          # the callbacks live as long as the struct
+    h.nown = getattr(plan, "ghost_nown", plan.nown) if plan is not None else int(ops.problem.n)
+    peer = plan is not None and hasattr(plan, "release")
+    h.release = _lib.RELEASE_FN(release) if peer else _lib.RELEASE_FN()
+    h._keep = (h.exchange, h.reduce, h.release)   # the callbacks live as long as the struct
     return ctypes.pointer(h)

@@ -293,3 +293,62 @@ def _check_local_single_entry_build(rank, world, d, n2, n1, m):
 @pytest.mark.parametrize("world,n2,n1,m", [(2, 40, 30, 300), (3, 61, 47, 900)])
 def test_local_single_entry_build_matches_global_slice(world, n2, n1, m):
     _run(_check_local_single_entry_build, world, n2, n1, m)
+
+
+def _check_nvlink_plan(rank, world, d, n, seed, deg, ld):
+    """Peer-memory plan (shard.NvlinkHaloPlan): remote columns are encoded as
+    CL_PEER_COL(owner, row), decode to the global ids, and a product that reads each
+    encoded row from its owner's block (what the GHOST 2 SpMM does over NVLink) equals the
+    global product. No halo buffer, no collective on the data path."""
+    from paper_2407_15049_b200 import shard
+    M = _sym_pattern(n, seed, deg)
+    X = np.random.default_rng(seed + 1).standard_normal((n, ld))
+    b = shard.block_bounds(n, world)
+    lo, hi = b[rank], b[rank + 1]
+    rows = M[lo:hi]
+    indptr = torch.as_tensor(rows.indptr.astype(np.int64))
+    cols = torch.as_tensor(rows.indices.astype(np.int64))
+    plan = shard.make_halo_plan(lo, hi, indptr, cols, b, rank, world, mode="nvlink", peer_ok=True)
+    assert isinstance(plan, shard.NvlinkHaloPlan) and plan.ghost_nown == shard.GHOST_PEERS
+    # without peer_ok (patterns other kernels read too) the copy-based plans are used
+    assert not isinstance(shard.make_halo_plan(lo, hi, indptr, cols, b, rank, world, mode="nvlink"),
+                          shard.NvlinkHaloPlan)
+    li = plan.local_indices.to(torch.int64)
+    own = (cols >= lo) & (cols < hi)
+    assert plan.local_indices.dtype == torch.int32
+    assert bool((li[own] >= 0).all()) and bool((li[~own] < 0).all())
+    assert torch.equal(shard.decode_peer_columns(li, lo, b), cols)
+    assert plan.counts[rank] == int((~own).sum()) and sum(plan.counts) > 0
+    assert plan.halo_rows == 0 and plan.maxb == 0 and plan.halo_bytes(ld) == int((~own).sum()) * ld * 8
+    # emulate the kernel: owner = bits 28..30, row = bits 0..27 of the unsigned index
+    blocks = [torch.as_tensor(X[b[k]:b[k + 1]]) for k in range(world)]
+    u = li + (1 << 31)
+    got = torch.zeros((hi - lo, ld), dtype=torch.float64)
+    vals = torch.as_tensor(rows.data)
+    for i in range(hi - lo):
+        for s in range(int(indptr[i]), int(indptr[i + 1])):
+            j = int(li[s])
+            src = blocks[rank][j] if j >= 0 else blocks[int(u[s]) >> 28 & 7][int(u[s]) & ((1 << 28) - 1)]
+            got[i] += vals[s] * src
+    want = rows @ X
+    assert np.abs(got.numpy() - want).max() <= 1e-12 * (1 + np.abs(want).max())
+
+
+@pytest.mark.parametrize("world,n,deg,ld", [(2, 300, 6, 4), (3, 401, 8, 6)])
+def test_nvlink_plan_encodes_remote_rows(world, n, deg, ld):
+    _run(_check_nvlink_plan, world, n, 5 + n, deg, ld)
+
+
+def test_peer_column_encoding_limits():
+    from paper_2407_15049_b200 import shard
+    owner = torch.tensor([0, 1, 7, 7])
+    row = torch.tensor([0, 5, (1 << 28) - 1, 3])
+    enc = shard.peer_cols(owner, row)
+    assert bool((enc < 0).all()) and bool((enc >= -(1 << 31)).all())
+    assert torch.equal(enc.to(torch.int32).to(torch.int64), enc)        # fits the int32 index
+    bounds = [0, 10, 20, 30, 40, 50, 60, 70, 1 << 29]
+    dec = shard.decode_peer_columns(enc, 5, bounds)
+    assert dec.tolist() == [0 + 0, 10 + 5, 70 + (1 << 28) - 1, 70 + 3]
+    with pytest.raises(ValueError):
+        shard.NvlinkHaloPlan(0, 1, torch.zeros(2, dtype=torch.int64), torch.zeros(1, dtype=torch.int64),
+                             [0, 1, 2 ** 28 + 2], 0, 2)
