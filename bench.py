@@ -545,8 +545,10 @@ def run_ours(args, rank, world, local_rank):
         r = driver.initial_rank(p.m, p.n)
     else:
         # weak scaling: every rank owns n rows of one random graph on world*n vertices; strong
-        # scaling: the ranks split one graph on n vertices. Remote factor rows arrive by the
-        # halo all-gather inside the SpMM (shard.py); the graph is generated on the device.
+        # scaling: the ranks split one graph on n vertices. With one GPU per rank and NCCL the
+        # SpMM reads remote factor rows in place from the peers' memory over NVLink
+        # (shard.NvlinkHaloPlan); otherwise a halo all-gather / all-to-all fills a ghost
+        # buffer first. The graph is generated on the device.
         if args.graph != "random" or args.reorder:
             if rank == 0:
                 print("bench: --graph/--reorder apply at N=1 weak scaling only (the sharded instance is "
@@ -784,6 +786,11 @@ def run_ours(args, rank, world, local_rank):
         "completion": completion,
         "solve": solve,
     }
+    if world > 1:
+        # how remote factor rows reach the SpMM: NvlinkHaloPlan reads them in place from the
+        # owners' memory (no halo buffer, no data collective); HaloPlan / PeerHaloPlan copy
+        # them into a halo buffer by all-gather / all-to-all first
+        line["halo"] = {"plan": type(ops.plan).__name__, "bytes_per_spmm_per_rank": halo_bytes}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -861,7 +861,7 @@ __global__ void __launch_bounds__(NT) basis_subtract_kernel(const double* __rest
 #endif
 #define SP_PTRMAX 264       // row pointers per tile: TR + 1 + alignment slack, TR <= 256
 #ifndef SP_UNROLL
-#define SP_UNROLL 8         // gathers in flight per lane (epilogue variants)
+#define SP_UNROLL 4         // gathers in flight per lane (epilogue variants; 8 measured 8-14 % slower, profiles/r2_peer)
 #endif
 // Plain-store variant: more gathers in flight for narrow rows (12: 4.32 -> 4.12 ms for C R at
 // n = 1e7, ld 26), fewer for wide rows where one group already covers 512 bytes per gather
@@ -874,6 +874,21 @@ __global__ void __launch_bounds__(NT) basis_subtract_kernel(const double* __rest
 #endif
 #ifndef SP_MINB2
 #define SP_MINB2 3          // the diagonal ADMM epilogues (CG start, step end)
+#endif
+#ifndef SP_UNROLLG
+#define SP_UNROLLG 6        // gathers in flight per lane, plain store with ghost rows (12 spills at 64 registers)
+#endif
+#ifndef SP_UNROLLGE
+#define SP_UNROLLGE 4       // the same for the epilogue variants with ghost rows
+#endif
+#ifndef SP_MINBGE
+#define SP_MINBGE 4         // resident CTAs per SM of the epilogue variants with ghost rows
+#endif
+#ifndef SP_UNROLL2
+#define SP_UNROLL2 SP_UNROLL  // gathers in flight per lane, diagonal-ADMM epilogues
+#endif
+#ifndef SP_MINBG
+#define SP_MINBG 4          // plain-store variants with ghost rows (halo buffer / peer memory)
 #endif
 #ifndef SP_MINB1
 #define SP_MINB1 3          // resident CTAs per SM the epilogue variants are compiled for
@@ -981,10 +996,11 @@ __device__ __forceinline__ const double* sp_src(const SpDev& a, const double* X,
 }
 
 template <int G, int VEC, int EPI, int GHOST>
-__global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? 4 : SP_MINB0) : (EPI >= 2 ? SP_MINB2 : SP_MINB1)) spmm_tiled_kernel(SpDev a, EpiDev E, double* ws,
+__global__ void __launch_bounds__(NT, EPI == 0 ? (GHOST ? SP_MINBG : SP_MINB0) : (GHOST ? SP_MINBGE : (EPI >= 2 ? SP_MINB2 : SP_MINB1))) spmm_tiled_kernel(SpDev a, EpiDev E, double* ws,
                                                                                      double* dots_out) {
     constexpr int NG = NT / G;
-    constexpr int SPU = EPI == 0 ? (G == 32 ? SP_UNROLL0_WIDE : SP_UNROLL0) : SP_UNROLL;
+    constexpr int SPU = EPI == 0 ? (G == 32 ? SP_UNROLL0_WIDE : (GHOST ? SP_UNROLLG : SP_UNROLL0))
+                                 : (GHOST ? SP_UNROLLGE : (EPI >= 2 ? SP_UNROLL2 : SP_UNROLL));
     // epilogue operand set of the tiled path: Y0, Y1, out, Z0, Z1, Z2
     constexpr int NOPS = SP_NY + 1 + SP_NZ;
     __shared__ __align__(128) SpTile T[2];
