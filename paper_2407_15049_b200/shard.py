@@ -987,7 +987,7 @@ def _peer_rows(n_loc, world, deg):
 
 
 def memory_model(n_global, world, r, nnz_c_per_row, m_global=None, nnz_a_per_con=1.0, halo_frac=1.0,
-                 memory=8, halo_slots=1, pair=False, peer=False):
+                 memory=8, halo_slots=1, pair=False, peer=False, nvlink=False):
     """Per-rank device bytes of a row-sharded solve at rank r.
 
     * stage buffers: driver.stage_factor_buffers(memory, pair) factors of n_loc x ld fp64
@@ -999,6 +999,8 @@ def memory_model(n_global, world, r, nnz_c_per_row, m_global=None, nnz_a_per_con
       ``peer``: the point-to-point plan (PeerHaloPlan) on a uniformly random pattern of
       nnz_c_per_row - 1 neighbours per row: each rank receives, and sends, the
       1 - exp(-deg/world) share of every other block that it references;
+      ``nvlink``: the peer-memory plan (NvlinkHaloPlan) -- remote rows are read in place,
+      no halo buffer;
     * operators: C rows (int32 index + fp64 value per nonzero, int64 row pointer), Omega
       (index, value, adjoint pointer per slot; constraint id + coefficient per adjoint
       entry), Omega_A and the constraint rows;
@@ -1018,7 +1020,7 @@ def memory_model(n_global, world, r, nnz_c_per_row, m_global=None, nnz_a_per_con
         "n_per_rank": n_loc, "ld": ld, "factor_bytes": factor,
         "stage_buffers": stage_factor_buffers(memory, pair) * factor,
         "halo": ((halo_slots + 1) * _peer_rows(n_loc, world, nnz_c_per_row - 1) if peer
-                 else halo_slots * (world * maxb) + maxb) * ld * 8 if world > 1 else 0,
+                 else halo_slots * (world * maxb) + maxb) * ld * 8 if world > 1 and not nvlink else 0,
         "operators": (nnz_c * 12 + n_loc * 8) + (nnz_c + 2 * nnz_a) * 20 + nnz_a * 12 * 2 + nnz_a * 28
                      + m_loc * 8 + 2 * n_loc * 8,
         "m_vectors": 16 * 8 * m_loc,

@@ -221,6 +221,8 @@ def test_memory_model_configs():
     mesh = shard.memory_model(int(1.7e8), 8, 29, 7, halo_frac=0.002)
     rand = shard.memory_model(int(1.7e8), 8, 29, 7)
     peer = shard.memory_model(int(1.7e8), 8, 29, 7, peer=True)
+    nv = shard.memory_model(int(1.7e8), 8, 29, 7, nvlink=True)
+    assert nv["halo"] == 0 and nv["total"] == rand["total"] - rand["halo"]
     assert mesh["total"] < peer["total"] < rand["total"] < budget
     # the next rank (r0 = 29 -> 44) does not fit on any of them
     assert shard.memory_model(int(1.7e8), 8, 44, 7, halo_frac=0.002)["total"] > budget
