@@ -355,6 +355,7 @@ class NvlinkHaloPlan:
         self.publish = torch.zeros(0, dtype=I32, device=indices.device)
         self._obj_group = None
         self._fence_t = None
+        self.stream = None           # the compute stream the products run on (Device.stream)
         self._imported = {}          # handle bytes -> mapped base address of a peer allocation
         self._tables = [(ctypes.c_uint64 * MAX_PEERS)() for _ in range(4)]
         self._tslot = 0
@@ -375,12 +376,14 @@ class NvlinkHaloPlan:
         compute stream is complete when work queued after it starts."""
         if self.world == 1:
             return
+        st = self.stream if self.stream is not None else torch.cuda.current_stream(like.device)
         if like.is_cuda and _nccl(self.group):
             if self._fence_t is None:
                 self._fence_t = torch.zeros(1, dtype=torch.float64, device=like.device)
-            dist.all_reduce(self._fence_t, group=self.group)
+            with torch.cuda.stream(st):
+                dist.all_reduce(self._fence_t, group=self.group)
         else:
-            torch.cuda.current_stream(like.device).synchronize()
+            st.synchronize()
             dist.barrier(group=self.group)
 
     def exchange(self, X, ld, pack=None, slot=0):
@@ -548,6 +551,7 @@ def sharded_maxcut_ops(n_global, deg, seed, rank, world, dev, group=None):
     n_edges = int(eu.numel())
     del eu, ev
     plan = make_halo_plan(lo, hi, indptr, cols, b, rank, world, group, mode=None, peer_ok=True)
+    plan.stream = getattr(dev, "stream", None)
     pad_ptr = torch.zeros(nown + 1 + 16, dtype=I64, device=dev.dev)
     pad_ptr[:nown + 1] = indptr
     cpat = DevicePattern(nown, pad_ptr[:nown + 1], padded(plan.local_indices), padded(vals),
@@ -662,6 +666,7 @@ def build_sharded_diag_operators(p, rank, world, dev, group=None):
     sup_r, sup_c = sup // n, sup % n
     o_ptr = _csr_ptr(sup_r, nown)
     plan = make_halo_plan(lo, hi, o_ptr, sup_c, b, rank, world, group, mode=None, peer_ok=True)
+    plan.stream = getattr(dev, "stream", None)
     aval = torch.as_tensor(np.ascontiguousarray(p.a_val[lo:hi], dtype=np.float64)).to(tdev)
     omega = DevicePattern(nown, o_ptr, padded(plan.local_indices), cv, _csr_ptr(slot_d, S),
                           padded(ar.to(I32)), padded(aval.clone()))

@@ -91,3 +91,26 @@ def test_device_arm_two_ranks_strong_scaling_gloo():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
     assert d["config"]["n"] == 300000 and d["config"]["n_per_gpu"] == 150000
+
+
+@pytest.mark.gpu
+def test_device_arm_two_ranks_peer_memory_gloo():
+    """The N>1 bench with the peer-memory ghost rows forced (CULORADS_HALO=nvlink): the two
+    ranks map each other's factor allocations by CUDA IPC and the SpMM reads remote rows in
+    place (on an NVLink box with NCCL this plan is the default)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--nrows", "300000", "--scaling", "strong",
+           "--no-cpu-baseline", "--no-e2e", "--dist-backend", "gloo"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900,
+                         env=dict(os.environ, CULORADS_HALO="nvlink"))
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["halo"]["plan"] == "NvlinkHaloPlan" and d["halo"]["bytes_per_spmm_per_rank"] > 0
