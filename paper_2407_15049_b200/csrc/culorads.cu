@@ -867,7 +867,7 @@ __global__ void __launch_bounds__(NT) basis_subtract_kernel(const double* __rest
 // n = 1e7, ld 26), fewer for wide rows where one group already covers 512 bytes per gather
 // (4: 13.3 -> 12.6 ms at ld 822); the epilogue variants lose registers to more (occupancy_sweep).
 #ifndef SP_UNROLL0
-#define SP_UNROLL0 12
+#define SP_UNROLL0 10        // plain store, narrow rows: 4.15 ms against 4.38 ms at 12 (n = 1e7, ld 26; profiles/r2_peer)
 #endif
 #ifndef SP_UNROLL0_WIDE
 #define SP_UNROLL0_WIDE 4
