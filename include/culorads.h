@@ -57,7 +57,9 @@ extern "C" {
  * factor row in place from the owner GPU's memory over NVLink. cl_pattern.nown ==
  * CL_GHOST_PEERS marks the mode; cl_pattern.ghost then points at a HOST table of
  * CL_MAX_PEERS device addresses (rank k's row block of X as mapped in this process,
- * cl_ipc_import), which the launch copies into the kernel's parameters. */
+ * cl_ipc_import), which the launch copies into the kernel's parameters. The constraint
+ * kernel (cl_constraint_eval_halo) takes the same mode with nown == CL_GHOST_PEERS: its
+ * position indices pi/pj use the encoding and ghosts[k] is operand k's host table. */
 #define CL_MAX_PEERS 8
 #define CL_PEER_ROW_BITS 28
 #define CL_PEER_ROW_MASK ((1u << CL_PEER_ROW_BITS) - 1u)

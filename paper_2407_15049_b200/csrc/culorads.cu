@@ -395,10 +395,22 @@ struct ConGhost {
     int64_t sx;           // row stride of the local operands (ld; 2 ld for a pair buffer)
 };
 
+// nown == CL_GHOST_PEERS: position index i < 0 is CL_PEER_COL(owner, row), read in place
+// from operand k's row block on the owner rank, p[k][owner] (include/culorads.h)
+struct ConPeers {
+    const double* p[6][CL_MAX_PEERS];
+};
+
 __device__ __forceinline__ const double* grow(const double* X, const double* Xg, int64_t i, int64_t nown, int ld,
                                               int64_t sx) {
     return (nown < 0 || i < nown) ? X + i * sx : Xg + (i - nown) * ld;
 }
+
+// Row i of constraint operand k: local, halo buffer (i >= nown), or (PEER) a peer's memory.
+#define growk(PEER, X, gh, k, i, nown, ld)                                                                  \
+    ((PEER) && (i) < 0 ? pp.p[k][((uint32_t)(i) >> CL_PEER_ROW_BITS) & (CL_MAX_PEERS - 1)] +                  \
+                             (int64_t)((uint32_t)(i) & CL_PEER_ROW_MASK) * (gh).sx                             \
+                       : grow(X, (gh).g[k], i, nown, ld, (gh).sx))
 
 template <int G, int VEC>
 __device__ __forceinline__ double group_dot_rows(const double* __restrict__ x, const double* __restrict__ y, int ld,
@@ -429,7 +441,7 @@ __device__ __forceinline__ double group_dot_rows(const double* __restrict__ x, c
 #define SE_BOUNDS __launch_bounds__(NT)
 #endif
 
-template <int G, int VEC, int NP>    // NP = 1: X1 Y1 only (A(UV^T)); 3: up to three products
+template <int G, int VEC, int NP, int PEER = 0>    // NP = 1: X1 Y1 only (A(UV^T)); 3: up to three products
 __global__ void CK_BOUNDS(NP) constraint_kernel(int64_t m, const int64_t* __restrict__ indptr,
                                                         const int32_t* __restrict__ pi,
                                                         const int32_t* __restrict__ pj,
@@ -437,7 +449,7 @@ __global__ void CK_BOUNDS(NP) constraint_kernel(int64_t m, const int64_t* __rest
                                                         const double* X1, const double* Y1,
                                                         const double* X2, const double* Y2, double* out1,
                                                         const double* X3, const double* Y3, double* out2,
-                                                        ConGhost gh) {
+                                                        ConGhost gh, ConPeers pp) {
     const int lane = threadIdx.x & 31;
     const int gl = lane % G;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - gl));
@@ -461,26 +473,26 @@ __global__ void CK_BOUNDS(NP) constraint_kernel(int64_t m, const int64_t* __rest
                 double2 x1a = z2, y1a = z2, x1b = z2, y1b = z2, x2a = z2, y2a = z2, x2b = z2, y2b = z2;
                 double2 x3a = z2, y3a = z2, x3b = z2, y3b = z2;
                 if (act) {
-                    x1a = ld2(grow(X1, gh.g[0], i0, nw, ld, gh.sx) + col);
-                    y1a = ld2(grow(Y1, gh.g[1], j0, nw, ld, gh.sx) + col);
+                    x1a = ld2(growk(PEER, X1, gh, 0, i0, nw, ld) + col);
+                    y1a = ld2(growk(PEER, Y1, gh, 1, j0, nw, ld) + col);
                     if (two) {
-                        x1b = ld2(grow(X1, gh.g[0], i1, nw, ld, gh.sx) + col);
-                        y1b = ld2(grow(Y1, gh.g[1], j1, nw, ld, gh.sx) + col);
+                        x1b = ld2(growk(PEER, X1, gh, 0, i1, nw, ld) + col);
+                        y1b = ld2(growk(PEER, Y1, gh, 1, j1, nw, ld) + col);
                     }
                     if (NP > 1 && X2 != nullptr) {
-                        x2a = ld2(grow(X2, gh.g[2], i0, nw, ld, gh.sx) + col);
-                        y2a = ld2(grow(Y2, gh.g[3], j0, nw, ld, gh.sx) + col);
+                        x2a = ld2(growk(PEER, X2, gh, 2, i0, nw, ld) + col);
+                        y2a = ld2(growk(PEER, Y2, gh, 3, j0, nw, ld) + col);
                         if (two) {
-                            x2b = ld2(grow(X2, gh.g[2], i1, nw, ld, gh.sx) + col);
-                            y2b = ld2(grow(Y2, gh.g[3], j1, nw, ld, gh.sx) + col);
+                            x2b = ld2(growk(PEER, X2, gh, 2, i1, nw, ld) + col);
+                            y2b = ld2(growk(PEER, Y2, gh, 3, j1, nw, ld) + col);
                         }
                     }
                     if (NP > 1 && X3 != nullptr) {
-                        x3a = ld2(grow(X3, gh.g[4], i0, nw, ld, gh.sx) + col);
-                        y3a = ld2(grow(Y3, gh.g[5], j0, nw, ld, gh.sx) + col);
+                        x3a = ld2(growk(PEER, X3, gh, 4, i0, nw, ld) + col);
+                        y3a = ld2(growk(PEER, Y3, gh, 5, j0, nw, ld) + col);
                         if (two) {
-                            x3b = ld2(grow(X3, gh.g[4], i1, nw, ld, gh.sx) + col);
-                            y3b = ld2(grow(Y3, gh.g[5], j1, nw, ld, gh.sx) + col);
+                            x3b = ld2(growk(PEER, X3, gh, 4, i1, nw, ld) + col);
+                            y3b = ld2(growk(PEER, Y3, gh, 5, j1, nw, ld) + col);
                         }
                     }
                 }
@@ -531,14 +543,14 @@ __global__ void CK_BOUNDS(NP) constraint_kernel(int64_t m, const int64_t* __rest
         for (int64_t t = t0; t < t1; ++t) {
             const int64_t i = __ldg(pi + t), j = __ldg(pj + t);
             const double v = __ldg(val + t);
-            double x = group_dot_rows<G, VEC>(grow(X1, gh.g[0], i, nw, ld, gh.sx), grow(Y1, gh.g[1], j, nw, ld, gh.sx), ld, gl,
+            double x = group_dot_rows<G, VEC>(growk(PEER, X1, gh, 0, i, nw, ld), growk(PEER, Y1, gh, 1, j, nw, ld), ld, gl,
                                               gmask);
             if (X2 != nullptr)
-                x += group_dot_rows<G, VEC>(grow(X2, gh.g[2], i, nw, ld, gh.sx), grow(Y2, gh.g[3], j, nw, ld, gh.sx), ld, gl,
+                x += group_dot_rows<G, VEC>(growk(PEER, X2, gh, 2, i, nw, ld), growk(PEER, Y2, gh, 3, j, nw, ld), ld, gl,
                                             gmask);
             a1 += v * x;
             if (X3 != nullptr)
-                a2 += v * group_dot_rows<G, VEC>(grow(X3, gh.g[4], i, nw, ld, gh.sx), grow(Y3, gh.g[5], j, nw, ld, gh.sx), ld, gl,
+                a2 += v * group_dot_rows<G, VEC>(growk(PEER, X3, gh, 4, i, nw, ld), growk(PEER, Y3, gh, 5, j, nw, ld), ld, gl,
                                                  gmask);
         }
         if (gl == 0) {
@@ -2015,9 +2027,15 @@ int constraint_eval_impl(int64_t m, const int64_t* indptr, const int32_t* pi, co
                          int32_t ld, const double* X1, const double* Y1, const double* X2, const double* Y2,
                          double* out1, const double* X3, const double* Y3, double* out2, const double* const* ghosts,
                          int64_t nown, int64_t sx, void* stream) {
-    if (ghosts != nullptr && nown == CL_GHOST_PEERS) return CL_EARG;   // peer-memory ghosts: SpMM only
     ConGhost gh;
-    for (int k = 0; k < 6; ++k) gh.g[k] = ghosts != nullptr ? ghosts[k] : nullptr;
+    ConPeers pp;
+    const bool peer = ghosts != nullptr && nown == CL_GHOST_PEERS;
+    for (int k = 0; k < 6; ++k) {
+        // peer mode: ghosts[k] is a HOST table of CL_MAX_PEERS row-block addresses (or NULL)
+        const double* const* tab = peer ? reinterpret_cast<const double* const*>(ghosts[k]) : nullptr;
+        for (int q = 0; q < CL_MAX_PEERS; ++q) pp.p[k][q] = tab != nullptr ? tab[q] : nullptr;
+        gh.g[k] = ghosts != nullptr && !peer ? ghosts[k] : nullptr;
+    }
     gh.nown = ghosts != nullptr ? nown : -1;
     gh.sx = sx > 0 ? sx : ld;
     if (m == 0) return CL_OK;
@@ -2032,14 +2050,23 @@ int constraint_eval_impl(int64_t m, const int64_t* indptr, const int32_t* pi, co
     const int grid = (int)(g > 65535 * 8 ? 65535 * 8 : g);
     const bool one = X2 == nullptr && X3 == nullptr;
 #define CL_CK(GG)                                                                                             \
-    if (one)                                                                                                  \
+    if (peer && one)                                                                                          \
+        constraint_kernel<GG, 2, 1, 1><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, \
+                                                            Y3, out2, gh, pp);                                    \
+    else if (peer)                                                                                            \
+        constraint_kernel<GG, 2, 3, 1><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, \
+                                                            Y3, out2, gh, pp);                                    \
+    else if (one)                                                                                             \
         constraint_kernel<GG, 2, 1><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, \
-                                                         out2, gh);                                           \
+                                                         out2, gh, pp);                                           \
     else                                                                                                      \
         constraint_kernel<GG, 2, 3><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, \
-                                                         out2, gh)
-    if (ld == 1) {
-        constraint_kernel<1, 1, 3><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2, gh);
+                                                         out2, gh, pp)
+    if (ld == 1 && peer) {
+        constraint_kernel<1, 1, 3, 1><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2,
+                                                           gh, pp);
+    } else if (ld == 1) {
+        constraint_kernel<1, 1, 3><<<grid, NT, 0, st>>>(m, indptr, pi, pj, val, ld, X1, Y1, X2, Y2, out1, X3, Y3, out2, gh, pp);
     } else {
         switch (G) {
             case 1: CL_CK(1); break;

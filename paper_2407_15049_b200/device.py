@@ -184,10 +184,11 @@ class Device:
             garr = (ctypes.c_void_p * 6)(*[g.data_ptr() if g is not None else None for g in ghosts])
             rc = self.lib.cl_constraint_eval_halo(int(con.m), ptr(con.indptr), ptr(con.pi), ptr(con.pj),
                                                   ptr(con.val), int(ld), ptr(X1), ptr(Y1), ptr(X2), ptr(Y2),
-                                                  ptr(out1), ptr(X3), ptr(Y3), ptr(out2), garr, int(halo.nown),
-                                                  self.sp)
+                                                  ptr(out1), ptr(X3), ptr(Y3), ptr(out2), garr,
+                                                  int(getattr(halo, "ghost_nown", halo.nown)), self.sp)
             self.launches += 1
             check(rc, "cl_constraint_eval_halo")
+            self._release(halo, X1)
             return
         rc = self.lib.cl_constraint_eval(int(con.m), ptr(con.indptr), ptr(con.pi), ptr(con.pj),
                                          ptr(con.val), int(ld), ptr(X1), ptr(Y1), ptr(X2), ptr(Y2),

@@ -330,8 +330,9 @@ class NvlinkHaloPlan:
     until every rank's operand is complete, ``release`` until every rank's product has
     read it (an 8-byte NCCL all-reduce on the compute stream; a host barrier on gloo).
 
-    Replaces the all-gather / all-to-all of HaloPlan / PeerHaloPlan for patterns read only by
-    the SpMM (C and Omega of a diagonal-constraint problem). ``ghost_nown`` (= CL_GHOST_PEERS)
+    Replaces the all-gather / all-to-all of HaloPlan / PeerHaloPlan for the factor rows of C,
+    Omega and Omega_A of diagonal-constraint (MaxCut) and single-entry (matrix completion)
+    problems: the SpMM and the constraint kernel decode the same encoding. ``ghost_nown`` (= CL_GHOST_PEERS)
     is what goes into cl_pattern.nown; ``exchange`` returns the host table of peer addresses
     (cl_pattern.ghost)."""
 
@@ -357,7 +358,7 @@ class NvlinkHaloPlan:
         self._fence_t = None
         self.stream = None           # the compute stream the products run on (Device.stream)
         self._imported = {}          # handle bytes -> mapped base address of a peer allocation
-        self._tables = [(ctypes.c_uint64 * MAX_PEERS)() for _ in range(4)]
+        self._tables = [(ctypes.c_uint64 * MAX_PEERS)() for _ in range(8)]   # >= 6 operands per launch
         self._tslot = 0
 
     def remap(self, ids):
@@ -775,19 +776,20 @@ def build_sharded_single_entry_operators(p, rank, world, dev, group=None):
     o_ptr = _csr_ptr(sup // n, nown)
     ref = new_id[a_con]
     mplan = HaloPlan(lo_m, hi_m, None, ref, bm, rank, world, group, publish=pub)
-    oplan = make_halo_plan(lo, hi, o_ptr, sup % n, b, rank, world, group)
+    oplan = make_halo_plan(lo, hi, o_ptr, sup % n, b, rank, world, group, mode=None, peer_ok=True)
     at_con = padded(mplan.remap(ref).to(I32))
     omega = DevicePattern(nown, o_ptr, padded(oplan.local_indices), cv, _csr_ptr(slot_a, S), at_con,
                           padded(a_val.clone()))
     a_ptr = _csr_ptr(acode // n, nown)
-    aplan = make_halo_plan(lo, hi, a_ptr, acode % n, b, rank, world, group)
+    aplan = make_halo_plan(lo, hi, a_ptr, acode % n, b, rank, world, group, mode=None, peer_ok=True)
     apat = DevicePattern(nown, a_ptr, padded(aplan.local_indices), None,
                          _csr_ptr(torch.arange(acode.numel(), device=tdev, dtype=I64), acode.numel()),
                          padded(mplan.remap(ref).to(I32)), padded(a_val.clone()))
     c_ptr = _csr_ptr(ccode // n, nown)
-    cplan = make_halo_plan(lo, hi, c_ptr, ccode % n, b, rank, world, group)
+    cplan = make_halo_plan(lo, hi, c_ptr, ccode % n, b, rank, world, group, mode=None, peer_ok=True)
     cpat = DevicePattern(nown, c_ptr, padded(cplan.local_indices), padded(c_vals.clone()), None, None, None)
     for pat, plan in ((omega, oplan), (apat, aplan), (cpat, cplan)):
+        plan.stream = getattr(dev, "stream", None)
         pat.halo = plan if (world > 1 and sum(plan.counts) > 0) else None
     for pat in (omega, apat):
         pat.mhalo = mplan if (world > 1 and sum(mplan.counts) > 0) else None

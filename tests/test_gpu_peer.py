@@ -7,8 +7,10 @@ tell a local address from an NVLink-mapped one), so every kernel variant that re
 rows -- plain store, fused epilogue with dots, heavy rows, the diagonal-ADMM start and
 step end -- is checked here against the same rows with global column indices on the
 whole factor: the slot order and the loaded values are the same, so the results are
-bit-identical. The IPC mapping itself and the fences are exercised by the two-process
-solve at the bottom (two ranks sharing cuda:0 over gloo).
+bit-identical. The constraint kernel (matrix completion's A(UV^T) and the line search's three
+products) reads its positions' remote rows the same way. The IPC mapping itself and the
+fences are exercised by the two-process solves at the bottom (ranks sharing cuda:0 over
+gloo).
 """
 
 import os
@@ -180,22 +182,73 @@ def test_peer_ghost_diag_admm_bit_identical(ld, world):
         assert peer.halo.released == 2
 
 
-def test_peer_ghosts_rejected_by_constraint_kernels():
-    """Only the SpMM reads peer-encoded columns: the constraint kernels refuse the mode."""
-    import ctypes
+class _OperandPeers(_LocalPeers):
+    """Peer tables per operand: each local operand maps to its global blocks."""
 
-    from paper_2407_15049_b200 import _lib
-    lib = _lib.load()
-    t = torch.zeros(64, dtype=torch.float64, device="cuda")
-    ip = torch.zeros(18, dtype=torch.int64, device="cuda")
-    ip[1] = 1
-    ix = torch.zeros(16, dtype=torch.int32, device="cuda")
-    p = ctypes.c_void_p
-    garr = (ctypes.c_void_p * 6)(*[t.data_ptr()] * 6)
-    rc = lib.cl_constraint_eval_halo(1, p(ip.data_ptr()), p(ix.data_ptr()), p(ix.data_ptr()), p(t.data_ptr()), 2,
-                                     p(t.data_ptr()), p(t.data_ptr()), None, None, p(t.data_ptr()), None, None,
-                                     None, garr, _lib.CL_GHOST_PEERS, None)
-    assert rc == _lib.CL_EARG
+    def __init__(self, table):
+        self.table = table             # id(local operand) -> list of per-rank blocks
+        self.released = 0
+        self._tabs = []
+
+    def exchange(self, X, ld, pack=None, slot=0):
+        from paper_2407_15049_b200 import shard
+        tab = (shard.ctypes.c_uint64 * shard.MAX_PEERS)()
+        for k, blk in enumerate(self.table[id(X)]):
+            tab[k] = blk.data_ptr()
+        self._tabs.append(tab)
+        return shard._HostTable(tab)
+
+
+@pytest.mark.parametrize("world,ld", [(3, 26), (2, 8), (4, 2)])
+def test_peer_ghost_constraint_kernel_bit_identical(world, ld):
+    """cl_constraint_eval_halo in the peer mode (single-entry style constraints whose
+    positions reference any rank's rows): one and three products, against the same
+    constraint rows with global positions on whole factors."""
+    from paper_2407_15049_b200 import shard
+    from paper_2407_15049_b200.device import Device
+    from paper_2407_15049_b200.linops import ConstraintCSR, padded
+    torch.cuda.set_device(0)
+    dev = Device()
+    n, m = 3000, 5000
+    rng = np.random.default_rng(21 + world)
+    b = shard.block_bounds(n, world)
+    lens = rng.integers(1, 3, m)
+    ptr = np.concatenate([[0], np.cumsum(lens)])
+    pi = rng.integers(0, n, ptr[-1])
+    pj = rng.integers(0, n, ptr[-1])
+    val = rng.standard_normal(ptr[-1])
+    G = {k: torch.as_tensor(rng.standard_normal((n, ld))).cuda() for k in "UVD"}
+    blocks = {k: [G[k][b[q]:b[q + 1]].clone() for q in range(world)] for k in "UVD"}
+    bm = shard.block_bounds(m, world)
+    for rank in range(world):
+        lo, hi = b[rank], b[rank + 1]
+        c0, c1 = bm[rank], bm[rank + 1]
+        s0, s1 = ptr[c0], ptr[c1]
+        T = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to("cuda", dt)   # noqa: E731
+        cptr = torch.zeros(c1 - c0 + 1 + 16, dtype=torch.int64, device="cuda")
+        cptr[:c1 - c0 + 1] = T(ptr[c0:c1 + 1] - s0, torch.int64)
+
+        def con_of(pi_, pj_):
+            return ConstraintCSR(m=c1 - c0, indptr=cptr[:c1 - c0 + 1], colidx=padded(T(np.zeros(s1 - s0), torch.int32)),
+                                 pi=padded(pi_.to(torch.int32)), pj=padded(pj_.to(torch.int32)),
+                                 val=padded(T(val[s0:s1], torch.float64)), diag_aval=None)
+        gpi, gpj = T(pi[s0:s1], torch.int64), T(pj[s0:s1], torch.int64)
+        peer = con_of(shard.encode_peer_columns(gpi, lo, hi, b), shard.encode_peer_columns(gpj, lo, hi, b))
+        U, V, D = (blocks[k][rank] for k in "UVD")
+        peer.halo = _OperandPeers({id(U): blocks["U"], id(V): blocks["V"], id(D): blocks["D"]})
+        ref = con_of(gpi, gpj)
+        o = [torch.empty(c1 - c0, dtype=torch.float64, device="cuda") for _ in range(6)]
+        dev.constraint_eval(peer, ld, U, V, o[0])
+        dev.constraint_eval(ref, ld, G["U"], G["V"], o[1])
+        dev.constraint_eval(peer, ld, U, V, o[2], X2=V, Y2=U, X3=D, Y3=D, out2=o[3])
+        dev.constraint_eval(ref, ld, G["U"], G["V"], o[4], X2=G["V"], Y2=G["U"], X3=G["D"], Y3=G["D"], out2=o[5])
+        torch.cuda.synchronize()
+        assert torch.equal(o[0], o[1]) and torch.equal(o[2], o[4]) and torch.equal(o[3], o[5]), rank
+        Ug, Vg, Dg = (G[k].cpu().numpy() for k in "UVD")
+        want = np.array([sum(val[t] * Ug[pi[t]] @ Vg[pj[t]] for t in range(ptr[c], ptr[c + 1]))
+                         for c in range(c0, c1)])
+        assert np.abs(o[0].cpu().numpy() - want).max() <= 1e-12 * (1 + np.abs(want).max())
+        assert peer.halo.released == 2
 
 
 def test_ipc_export_reports_allocation_offset():
@@ -224,7 +277,7 @@ def _free_port():
     return p
 
 
-def _peer_solve_worker(rank, world, port, case, q):
+def _peer_solve_worker(rank, world, port, case, q, over=None):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -239,7 +292,9 @@ def _peer_solve_worker(rank, world, port, case, q):
         out = []
         for mode in ("nvlink", "allgather"):
             shard.HALO_MODE = mode
-            rep = shard.solve_sharded(p, driver.SolverConfig(**dict(cfg_of(z))), dev=Device())
+            cfg = dict(cfg_of(z))
+            cfg.update(over or {})
+            rep = shard.solve_sharded(p, driver.SolverConfig(**cfg), dev=Device())
             out.append((mode, np.array([r[2:7] for r in rep.trace_rows], dtype=float), rep.objective,
                         rep.status, rep.gpu_launches))
         q.put((rank, out))
@@ -251,15 +306,20 @@ def _peer_solve_worker(rank, world, port, case, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case,world", [("g1_like", 2), ("maxcut_2k_deg6", 3)])
+@pytest.mark.parametrize("case,world", [("g1_like", 2), ("maxcut_2k_deg6", 3), ("completion_30", 2),
+                                        ("completion_30", 3)])
 def test_peer_memory_sharded_solve_matches_halo_solve(case, world):
-    """A row-sharded solve whose C products read remote rows in place from the other ranks'
-    memory (CUDA IPC, stream fences; native ALM/ADMM loops with the release hook) gives the
-    bit-identical trace and objective of the all-gather halo solve."""
+    """A row-sharded solve whose C products (and, for matrix completion, constraint
+    evaluations and Omega products) read remote rows in place from the other ranks' memory
+    (CUDA IPC, stream fences; MaxCut's native ALM/ADMM loops with the release hook) gives
+    the bit-identical trace and objective of the all-gather halo solve."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    pc = mp.spawn(_peer_solve_worker, args=(world, _free_port(), case, q), nprocs=world, join=False)
+    # matrix completion (constraint rows and Omega through the peer plan): a capped solve,
+    # the gloo-staged multiplier halo is slow
+    over = dict(admm_step_cap=40, max_reopts=0) if case.startswith("completion") else None
+    pc = mp.spawn(_peer_solve_worker, args=(world, _free_port(), case, q, over), nprocs=world, join=False)
     res = [q.get(timeout=900) for _ in range(world)]
     while not pc.join():
         pass
