@@ -873,7 +873,7 @@ __global__ void __launch_bounds__(NT) basis_subtract_kernel(const double* __rest
 #endif
 #define SP_PTRMAX 264       // row pointers per tile: TR + 1 + alignment slack, TR <= 256
 #ifndef SP_UNROLL
-#define SP_UNROLL 4         // gathers in flight per lane (epilogue variants; 8 measured 8-14 % slower, profiles/r2_peer)
+#define SP_UNROLL 5         // gathers in flight per lane (epilogue variants): 4 % faster than 4, 12-17 % than 8 (profiles/r2_peer)
 #endif
 // Plain-store variant: more gathers in flight for narrow rows (12: 4.32 -> 4.12 ms for C R at
 // n = 1e7, ld 26), fewer for wide rows where one group already covers 512 bytes per gather
