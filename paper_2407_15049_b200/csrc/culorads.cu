@@ -742,8 +742,17 @@ struct DiagDev {
 // One thread per double2 of the flat n*ld factor; every thread of a row
 // recomputes the row's constraint scalars from the (read-only) m-vectors and
 // the row owner (first double2 of the row) writes ax_out and adds the m-dots.
+#ifndef DU_DIV32
+#define DU_DIV32 1
+#endif
+#ifndef DU_B17
+#define DU_B17 0
+#endif
+#ifndef DU_MINB
+#define DU_MINB 0           // resident CTAs per SM the history-wide update is compiled for (0: the compiler's choice)
+#endif
 template <int NH, bool GOLD = true>   // GOLD false: g_old = 0 (the inner solve's first gradient)
-__global__ void __launch_bounds__(NT) diag_update_kernel(DiagDev a, double* ws, double* dots_out) {
+__global__ void __launch_bounds__(NT, DU_MINB) diag_update_kernel(DiagDev a, double* ws, double* dots_out) {
     constexpr int ND = 7 + 2 * NH;
     double acc[ND];
 #pragma unroll
@@ -751,8 +760,9 @@ __global__ void __launch_bounds__(NT) diag_update_kernel(DiagDev a, double* ws, 
     const int half = a.ld >> 1;
     const int64_t n2 = a.n * half;
     const int64_t stride = (int64_t)gridDim.x * NT;
+    const bool small = n2 < (int64_t(1) << 32);   // 32-bit row division (the 64-bit one is a long call)
     for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < n2; k += stride) {
-        const int64_t row = k / half;
+        const int64_t row = DU_DIV32 && small ? (int64_t)((uint32_t)k / (uint32_t)half) : k / half;
         const bool owner = (k - row * half) == 0;
         double axr = __ldg(a.ax + row);
         if (!a.refresh) axr = axr + a.tau * __ldg(a.q1 + row) + a.tau * a.tau * __ldg(a.q2 + row);
@@ -2427,6 +2437,9 @@ int cl_diag_alm_update(const cl_diag_update_args* a, double* dots_out, double* w
     } else if (a->nh == 0) CL_DU(0);
     else if (a->nh <= 4) CL_DU(4);
     else if (a->nh <= 10) CL_DU(10);
+#if DU_B17
+    else if (a->nh <= 17) CL_DU(17);       // 2 * memory + 1 at the default L-BFGS memory 8
+#endif
     else CL_DU(CL_MAXIN);
 #undef CL_DU
     return (int)cudaGetLastError();
