@@ -746,13 +746,15 @@ struct DiagDev {
 #define DU_DIV32 1
 #endif
 #ifndef DU_B17
-#define DU_B17 0
+#define DU_B17 1            // a history bucket of exactly 17 (2 * memory + 1 at memory 8): 12.2 -> 9.6 ms at n = 1e7
 #endif
 #ifndef DU_MINB
-#define DU_MINB 0           // resident CTAs per SM the history-wide update is compiled for (0: the compiler's choice)
+#define DU_MINB 3           // resident CTAs per SM of the 4- and 10-wide buckets (10: 7.6 -> 6.5 ms at n = 1e7)
 #endif
+// (tools/diag_update_probe.py, profiles/r2_final/diag_update_probe.jsonl; the wider buckets
+// are fastest at the compiler's own register choice)
 template <int NH, bool GOLD = true>   // GOLD false: g_old = 0 (the inner solve's first gradient)
-__global__ void __launch_bounds__(NT, DU_MINB) diag_update_kernel(DiagDev a, double* ws, double* dots_out) {
+__global__ void __launch_bounds__(NT, (NH == 4 || NH == 10) ? DU_MINB : 0) diag_update_kernel(DiagDev a, double* ws, double* dots_out) {
     constexpr int ND = 7 + 2 * NH;
     double acc[ND];
 #pragma unroll
