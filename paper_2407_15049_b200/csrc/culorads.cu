@@ -147,8 +147,11 @@ struct LcDev {
 // KIN is the input capacity the instance is compiled for (the host picks the smallest that
 // holds nin): every input and accumulator lives in registers, so capacity costs occupancy --
 // a 20-input instance needs 191 registers (one CTA per SM), a 2-input one 40.
+#ifndef LC_MINB17
+#define LC_MINB17 0         // resident CTAs per SM of the 12- and 17-input instances (0: the compiler's choice)
+#endif
 template <int MODE, int KIN = (MODE == 0 ? 7 : CL_MAXIN)>
-__global__ void __launch_bounds__(NT) lincomb_kernel(LcDev a, int64_t n2, int tail, double* ws,
+__global__ void __launch_bounds__(NT, (KIN == 17 || KIN == 12) ? LC_MINB17 : 0) lincomb_kernel(LcDev a, int64_t n2, int tail, double* ws,
                                                      double* dots_out) {
     constexpr int ND = MODE == 0 ? 8 : (MODE == 1 ? KIN + 1 : 2 * KIN - 1);
     double acc[ND];
@@ -435,6 +438,9 @@ __device__ __forceinline__ double group_dot_rows(const double* __restrict__ x, c
 #define CK3_MINB 0          // the line search's three-product variant: the compiler's choice
 #endif
 #define CK_BOUNDS(NP) __launch_bounds__(NT, (NP) == 1 ? CK_MINB : CK3_MINB)   // 0: the compiler's choice
+#ifndef SE_U
+#define SE_U 4              // slots whose row gathers the single-entry operator issues together
+#endif
 #ifdef SE_MINB
 #define SE_BOUNDS __launch_bounds__(NT, SE_MINB)
 #else
@@ -1379,23 +1385,43 @@ __global__ void SE_BOUNDS single_entry_apply_kernel(int64_t nrows, const int64_t
                 aa = __ldg(slot_a + s);
             }
             const int cnt = (int)min((int64_t)G, s1 - base);
-            for (int u = 0; u < cnt; ++u) {
-                const int j = __shfl_sync(gmask, jj, (lane - gl) + u);
-                const double av = __shfl_sync(gmask, aa, (lane - gl) + u);
-                const double2 wj = active ? ld2(W + (int64_t)j * sw + col) : zr;
-                const double2 fj = active ? ld2(Wf + (int64_t)j * sw + col) : zr;
-                const bool lo_is_i = row <= j;
-                double t1 = dot2(lo_is_i ? wi : wj, lo_is_i ? fj : fi);   // W_lo . Wf_hi
-                double t2 = dot2(lo_is_i ? wj : wi, lo_is_i ? fi : fj);   // W_hi . Wf_lo
+            // SE_U slots at a time: their 2 SE_U row gathers are issued together, then
+            // reduced one slot after another (the same arithmetic as one at a time)
+            for (int u0 = 0; u0 < cnt; u0 += SE_U) {
+                int jv[SE_U];
+                double avv[SE_U];
+                double2 wv[SE_U], fv[SE_U];
 #pragma unroll
-                for (int o = G / 2; o > 0; o >>= 1) {
-                    t1 += __shfl_xor_sync(gmask, t1, o);
-                    t2 += __shfl_xor_sync(gmask, t2, o);
+                for (int q = 0; q < SE_U; ++q) {
+                    const int u = u0 + q < cnt ? u0 + q : cnt - 1;
+                    jv[q] = __shfl_sync(gmask, jj, (lane - gl) + u);
+                    avv[q] = __shfl_sync(gmask, aa, (lane - gl) + u);
                 }
-                const double y = 0.0 + av * (row == j ? t1 : t1 + t2);
-                const double coef = 0.0 + av * y;
-                acc.x = fma(coef, fj.x, acc.x);
-                acc.y = fma(coef, fj.y, acc.y);
+#pragma unroll
+                for (int q = 0; q < SE_U; ++q) {
+                    const bool ok = active && u0 + q < cnt;
+                    wv[q] = ok ? ld2(W + (int64_t)jv[q] * sw + col) : zr;
+                    fv[q] = ok ? ld2(Wf + (int64_t)jv[q] * sw + col) : zr;
+                }
+#pragma unroll
+                for (int q = 0; q < SE_U; ++q) {
+                    if (u0 + q >= cnt) break;
+                    const int j = jv[q];
+                    const double av = avv[q];
+                    const double2 wj = wv[q], fj = fv[q];
+                    const bool lo_is_i = row <= j;
+                    double t1 = dot2(lo_is_i ? wi : wj, lo_is_i ? fj : fi);   // W_lo . Wf_hi
+                    double t2 = dot2(lo_is_i ? wj : wi, lo_is_i ? fi : fj);   // W_hi . Wf_lo
+#pragma unroll
+                    for (int o = G / 2; o > 0; o >>= 1) {
+                        t1 += __shfl_xor_sync(gmask, t1, o);
+                        t2 += __shfl_xor_sync(gmask, t2, o);
+                    }
+                    const double y = 0.0 + av * (row == j ? t1 : t1 + t2);
+                    const double coef = 0.0 + av * y;
+                    acc.x = fma(coef, fj.x, acc.x);
+                    acc.y = fma(coef, fj.y, acc.y);
+                }
             }
         }
         if (active) {
