@@ -439,7 +439,7 @@ __device__ __forceinline__ double group_dot_rows(const double* __restrict__ x, c
 #endif
 #define CK_BOUNDS(NP) __launch_bounds__(NT, (NP) == 1 ? CK_MINB : CK3_MINB)   // 0: the compiler's choice
 #ifndef SE_U
-#define SE_U 4              // slots whose row gathers the single-entry operator issues together
+#define SE_U 2              // slots whose row gathers the single-entry operator issues together (1: 6.20 ms, 2: 5.62, 4: 6.54 at configs[3]'s share)
 #endif
 #ifdef SE_MINB
 #define SE_BOUNDS __launch_bounds__(NT, SE_MINB)
@@ -768,9 +768,14 @@ __global__ void __launch_bounds__(NT, (NH == 4 || NH == 10) ? DU_MINB : 0) diag_
     const int half = a.ld >> 1;
     const int64_t n2 = a.n * half;
     const int64_t stride = (int64_t)gridDim.x * NT;
-    const bool small = n2 < (int64_t(1) << 32);   // 32-bit row division (the 64-bit one is a long call)
+    // 32-bit row division (the 64-bit one is a long call) in the history buckets: the 10-wide
+    // one gains 6 % at n = 1e7; the history-free instance, whose refresh pass is the bench's
+    // gradient, measured faster with the 64-bit one (1.89 against 2.06 ms; code generation,
+    // not the division itself -- profiles/r2_final/diag_update_probe.jsonl)
+    constexpr bool DIV32 = DU_DIV32 && NH > 0;
+    const bool small = n2 < (int64_t(1) << 32);
     for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < n2; k += stride) {
-        const int64_t row = DU_DIV32 && small ? (int64_t)((uint32_t)k / (uint32_t)half) : k / half;
+        const int64_t row = DIV32 && small ? (int64_t)((uint32_t)k / (uint32_t)half) : k / half;
         const bool owner = (k - row * half) == 0;
         double axr = __ldg(a.ax + row);
         if (!a.refresh) axr = axr + a.tau * __ldg(a.q1 + row) + a.tau * a.tau * __ldg(a.q2 + row);
