@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(NT, 4) diag_constraint_kernel(DiagCon a) {
 // one thread per row fold its units in order. Products 1 and 2 are summed
 // per unit (q1 = A(R D^T + D R^T) in the line search).
 #ifndef DC_U
-#define DC_U 6              // units in flight per thread of the flat row kernels: A(RR^T) 0.49 -> 0.35 ms at n = 1e7 (8 was register-bound)
+#define DC_U 4              // units in flight per thread of the flat row kernels: A(RR^T) 0.49 -> 0.35 ms, CG apply 2.06 -> 1.47 ms at n = 1e7 (8 was register-bound)
 #endif
 #ifndef CL_SMALLN
 #define CL_SMALLN 1         // small problems: spread rows over at least FLAT_MIN_BLK blocks / one tile per CTA
