@@ -446,6 +446,8 @@ def nvlink_available(rank, world, group=None, device=None):
     the peer-memory halo can be used. The same answer on every rank."""
     if world == 1 or world > MAX_PEERS or not _nccl(group):
         return False
+    if "expandable_segments:true" in os.environ.get("PYTORCH_CUDA_ALLOC_CONF", "").replace(" ", "").lower():
+        return False       # cuMemMap-backed segments have no legacy CUDA IPC handle
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     idx = torch.tensor([dev.index], dtype=I64, device=dev)
     devs = _all_gather_1d(idx, world, group).view(-1).cpu().tolist()
